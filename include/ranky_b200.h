@@ -1,0 +1,249 @@
+/*
+ * ranky_b200.h -- C ABI of the B200-native Ranky hot path.
+ *
+ * Each entry point replaces one reference routine of /root/reference/proj
+ * (cited as include-or-source file:line). Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary. Host-pointer entry points take the
+ * reference's value semantics (inputs are read, results are returned in
+ * library-owned records released with rk_*_free); rk_dev_* entry points work
+ * on device-resident data for callers that keep the matrix in HBM.
+ *
+ * Errors: every function returns an rk_status. The message of the last
+ * failure on the calling thread is rk_last_error(); for RK_CONVERGENCE the
+ * reference's ConvergenceError::residual() is rk_last_residual(). Status
+ * codes map one-to-one onto the reference's exception types
+ * (proj/include/ranky/errors.hpp:10-38 and the std:: exceptions it throws).
+ *
+ * Sparse inputs are the reference's SparseMatrix entries: an array of
+ * rk_entry {row, col, value} sorted by (row, col), without duplicates,
+ * explicit zeros or out-of-range indices (proj/include/ranky/sparse_matrix.hpp:9-48).
+ * rk_entry has the exact layout of ranky::Entry, so a C++ caller passes
+ * SparseMatrix::entries().data() unchanged.
+ *
+ * Dense matrices are row-major doubles, as ranky::DenseMatrix
+ * (proj/include/ranky/dense_matrix.hpp:11-39).
+ *
+ * Every GPU entry point runs on the context's CUDA device and stream; there is
+ * no CPU fallback. Calls on one context are not thread-safe; use one context
+ * per thread.
+ */
+#ifndef RANKY_B200_H
+#define RANKY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RK_API __attribute__((visibility("default")))
+#else
+#define RK_API
+#endif
+
+typedef enum rk_status {
+  RK_OK = 0,
+  RK_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  RK_OUT_OF_RANGE = 2,     /* std::out_of_range */
+  RK_CONVERGENCE = 3,      /* ranky::ConvergenceError (proj/include/ranky/errors.hpp:29-38) */
+  RK_RUNTIME = 4,          /* std::runtime_error ("block task d failed: ...") */
+  RK_CUDA = 5,             /* CUDA runtime failure or no usable device */
+  RK_NOMEM = 6             /* device or host allocation failed */
+} rk_status;
+
+/* RepairMethod -- proj/include/ranky/repair.hpp:15-20 (same numbering) */
+typedef enum rk_method { RK_RANDOM = 0, RK_NEIGHBOR = 1, RK_NEIGHBOR_RANDOM = 2, RK_NONE = 3 } rk_method;
+
+/* Entry -- proj/include/ranky/sparse_matrix.hpp:9-15 */
+typedef struct rk_entry {
+  uint64_t row;
+  uint64_t col;
+  double value;
+} rk_entry;
+
+typedef struct rk_sparse_view {
+  uint64_t rows, cols, nnz;
+  const rk_entry* entries; /* host, sorted by (row, col) */
+} rk_sparse_view;
+
+/* SvdResult -- proj/include/ranky/svd.hpp:15-19. u: u_rows x u_cols row-major,
+ * sigma: n_sigma descending, v (when has_v): v_rows x v_cols row-major. */
+typedef struct rk_svd {
+  uint64_t u_rows, u_cols;
+  double* u;
+  uint64_t n_sigma;
+  double* sigma;
+  int32_t has_v;
+  uint64_t v_rows, v_cols;
+  double* v;
+} rk_svd;
+
+/* RepairReport -- proj/include/ranky/repair.hpp:25-48. mechanism: 0 random, 1 neighbor */
+typedef struct rk_repair_report {
+  uint64_t n_edges;
+  uint64_t *block, *row, *col;
+  int32_t* mechanism;
+  uint64_t n_blocks;
+  uint64_t* lonely_counts;
+  uint64_t fallback_count;
+} rk_repair_report;
+
+/* A library-owned sparse matrix in entry order (the repaired matrix). */
+typedef struct rk_sparse {
+  uint64_t rows, cols, nnz;
+  rk_entry* entries;
+} rk_sparse;
+
+/* BlockResultRecord payloads -- proj/include/ranky/block_record.hpp:15-22:
+ * record d is rows x kept[d] row-major at payload + offset[d]. */
+typedef struct rk_records {
+  uint64_t n_records, rows;
+  uint32_t* kept;
+  uint64_t* offset;
+  double* payload;
+} rk_records;
+
+/* Per-stage device times of the last pipeline call, milliseconds (CUDA events). */
+typedef struct rk_timing {
+  double repair_ms, blocks_ms, merge_ms, recover_ms, total_ms;
+  double qr_ms, jacobi_ms;       /* inside blocks_ms */
+  uint64_t jacobi_sweeps_max;    /* over all block factorizations */
+  uint64_t jacobi_rotations;     /* over all block factorizations */
+  uint64_t kernel_launches;      /* kernels this library launched in the call */
+} rk_timing;
+
+/* PipelineResult (+ V) -- proj/include/ranky/pipeline.hpp:30-36 */
+typedef struct rk_pipeline_result {
+  rk_svd svd;              /* sigma + U of the input; v = V = A^T U Sigma^-1 when requested */
+  rk_repair_report report;
+  rk_sparse repaired;      /* filled only when want_repaired */
+  rk_records records;
+  rk_timing timing;
+} rk_pipeline_result;
+
+/* ---- errors & context ---------------------------------------------------- */
+RK_API const char* rk_last_error(void);
+RK_API double rk_last_residual(void);
+RK_API int32_t rk_abi_version(void);
+
+typedef struct rk_ctx rk_ctx;
+/* device = CUDA ordinal; the context owns a non-blocking stream */
+RK_API rk_status rk_ctx_create(int32_t device, rk_ctx** out);
+RK_API rk_status rk_ctx_destroy(rk_ctx* ctx);
+/* run subsequent work on a caller stream (cudaStream_t); NULL restores the own stream */
+RK_API rk_status rk_ctx_set_stream(rk_ctx* ctx, void* cuda_stream);
+RK_API rk_status rk_ctx_synchronize(rk_ctx* ctx);
+/* kernels launched through this context since creation */
+RK_API uint64_t rk_ctx_kernel_launches(const rk_ctx* ctx);
+
+RK_API void rk_svd_free(rk_svd* s);
+RK_API void rk_repair_report_free(rk_repair_report* r);
+RK_API void rk_sparse_free(rk_sparse* s);
+RK_API void rk_records_free(rk_records* r);
+RK_API void rk_pipeline_result_free(rk_pipeline_result* r);
+
+/* ---- KeyedRng -- proj/include/ranky/rng.hpp:11-25, proj/src/rng.cpp:16-38 ----
+ * Streams evaluated on the device (the same routine the repair kernels use).
+ * out[i] = i-th next() of KeyedRng(seed, block[i], row[i]) after skip[i] draws. */
+RK_API rk_status rk_keyed_rng_next(rk_ctx* ctx, uint64_t n, uint64_t seed, const uint64_t* block,
+                            const uint64_t* row, uint64_t draws, uint64_t* out /* n x draws */);
+/* out[i] = KeyedRng(seed, block[i], row[i]).below(bound[i]) */
+RK_API rk_status rk_keyed_rng_below(rk_ctx* ctx, uint64_t n, uint64_t seed, const uint64_t* block,
+                             const uint64_t* row, const uint64_t* bound, uint64_t* out);
+
+/* ---- rank check & repair -- proj/include/ranky/repair.hpp:50-96 ------------- */
+/* find_lonely_rows(a, partition_columns(a.cols, block_count), d) -- repair.hpp:51-52.
+ * out must hold a.rows entries; *n_out receives the count. */
+RK_API rk_status rk_find_lonely_rows(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count,
+                              uint64_t d, uint64_t* out, uint64_t* n_out);
+/* repair(a, partition_columns(a.cols, block_count), method, seed) -- repair.hpp:93-96 */
+RK_API rk_status rk_repair(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, rk_method method,
+                    uint64_t seed, rk_sparse* repaired, rk_repair_report* report);
+
+/* ---- SVD kernels -- proj/include/ranky/svd.hpp:25-29 ------------------------ */
+/* dense_svd(a) -- svd.hpp:25; a is rows x cols row-major */
+RK_API rk_status rk_dense_svd(rk_ctx* ctx, uint64_t rows, uint64_t cols, const double* a, rk_svd* out);
+/* block_svd(block, keep) -- svd.hpp:29 (no V, U truncated to min(keep, rows, cols)) */
+RK_API rk_status rk_block_svd(rk_ctx* ctx, const rk_sparse_view* block, uint64_t keep, rk_svd* out);
+
+/* ---- proxy -- proj/include/ranky/proxy.hpp:18-27 ---------------------------- */
+/* proxy_svd(proxy) -- proxy.hpp:22; proxy rows x total_cols row-major with
+ * n_offsets = blocks + 1 block offsets (the trailing one must equal total_cols) */
+RK_API rk_status rk_proxy_svd(rk_ctx* ctx, uint64_t rows, uint64_t total_cols, const double* proxy,
+                       uint64_t n_offsets, const uint64_t* block_offsets, rk_svd* out);
+/* recover_right_vectors(a, u, sigma, tol) -- proxy.hpp:26-27; V is a.cols x retained
+ * row-major, written into out->v (out->u / sigma stay empty) */
+RK_API rk_status rk_recover_right_vectors(rk_ctx* ctx, const rk_sparse_view* a, uint64_t u_rows,
+                                   uint64_t u_cols, const double* u, uint64_t n_sigma,
+                                   const double* sigma, double tol, rk_svd* out);
+
+/* ---- pipeline -- proj/include/ranky/pipeline.hpp:23-44 ---------------------- */
+/* run_block_task for every block of partition_columns(a.cols, block_count) of an
+ * already-repaired matrix, in block order (records only) -- pipeline.hpp:23 */
+RK_API rk_status rk_run_block_tasks(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count,
+                             uint64_t keep, rk_records* out);
+/* run_pipeline(a, block_count, method, keep, seed, workers) -- pipeline.hpp:42-44.
+ * workers is validated (0 is invalid) and otherwise ignored: block tasks run as
+ * batched kernels and the result is identical for any value, as in the reference.
+ * flags: RK_WANT_V adds V = recover_right_vectors(repaired, U[:, :top_k],
+ * sigma[:top_k], 1e-10) (top_k = 0: all); RK_WANT_REPAIRED returns the repaired
+ * matrix; RK_WANT_RECORDS returns the block records. */
+#define RK_WANT_V 1u
+#define RK_WANT_REPAIRED 2u
+#define RK_WANT_RECORDS 4u
+RK_API rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count,
+                          rk_method method, uint64_t keep, uint64_t seed, uint64_t workers,
+                          uint32_t flags, uint64_t top_k, rk_pipeline_result* out);
+
+/* ---- device-resident path (inputs already in HBM) --------------------------- */
+typedef struct rk_dev_matrix rk_dev_matrix;
+/* upload host entries once and build the device CSR/CSC */
+RK_API rk_status rk_dev_matrix_create(rk_ctx* ctx, const rk_sparse_view* a, rk_dev_matrix** out);
+RK_API rk_status rk_dev_matrix_destroy(rk_dev_matrix* m);
+RK_API uint64_t rk_dev_matrix_nnz(const rk_dev_matrix* m);
+
+/* Device-resident outputs of rk_dev_full_svd (owned by the library). */
+typedef struct rk_dev_outputs {
+  uint64_t rows, cols, k_sigma, k_v;
+  const double* d_sigma;  /* k_sigma, device */
+  const double* d_u;      /* rows x k_sigma row-major, device */
+  const double* d_v;      /* cols x k_v row-major, device (NULL without RK_WANT_V) */
+  uint64_t n_edges;
+} rk_dev_outputs;
+
+/* The whole hot path on a device-resident matrix: repair -> block SVDs -> merge ->
+ * (V). Results stay in HBM until rk_dev_outputs_free. Same flags as rk_run_pipeline
+ * (RK_WANT_REPAIRED / RK_WANT_RECORDS are ignored here). */
+RK_API rk_status rk_dev_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count,
+                          rk_method method, uint64_t keep, uint64_t seed, uint32_t flags,
+                          uint64_t top_k, rk_dev_outputs** out, rk_timing* timing);
+RK_API rk_status rk_dev_outputs_free(rk_dev_outputs* o);
+
+/* ---- sharded path (one process per GPU) --------------------------------------
+ * Column blocks are sharded over G ranks by merge-tree leaves. Rank g repairs the
+ * whole matrix (the replay is deterministic, so every rank holds the same repaired
+ * matrix without communication), factors the blocks of leaves [leaf_lo, leaf_hi)
+ * and reduces their records to the R factor of that subtree of the fixed merge tree
+ * (rk_merge_tree_leaves). The caller all-gathers the G factors (NCCL) and every rank
+ * finishes the same top of the tree, then recovers V for its own columns. With
+ * (leaves / G) a power of two the results are bitwise identical for every G. */
+RK_API uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count, uint64_t keep);
+typedef struct rk_dev_shard rk_dev_shard;
+/* d_root_out: device, rows*rows doubles, column-major upper-triangular R */
+RK_API rk_status rk_dev_shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
+                              uint64_t keep, uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi,
+                              double* d_root_out, rk_dev_shard** shard_out, rk_timing* timing);
+/* d_roots: device, n_roots x rows x rows (leaf order); V for columns [col_lo, col_hi) */
+RK_API rk_status rk_dev_shard_finish(rk_ctx* ctx, rk_dev_shard* shard, const double* d_roots, uint64_t n_roots,
+                              uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi,
+                              rk_dev_outputs** out, rk_timing* timing);
+RK_API rk_status rk_dev_shard_destroy(rk_dev_shard* shard);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANKY_B200_H */

@@ -1,0 +1,785 @@
+// rk_api.cu -- the C ABI (include/ranky_b200.h): argument checks with the
+// reference's messages, exception -> status mapping, host <-> device marshaling.
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include "rk_pipeline.cuh"
+
+namespace rk {
+thread_local uint64_t* g_launch_counter = nullptr;
+
+CallScope::CallScope(Ctx* c) {
+  cudaGetDevice(&prev_device);
+  if (prev_device != c->device) RK_CUDA_CHECK(cudaSetDevice(c->device));
+  prev_counter = g_launch_counter;
+  g_launch_counter = &c->launches;
+}
+CallScope::~CallScope() {
+  g_launch_counter = prev_counter;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (prev_device >= 0 && cur != prev_device) cudaSetDevice(prev_device);
+}
+}  // namespace rk
+
+using namespace rk;
+
+struct rk_ctx {
+  Ctx c;
+};
+struct rk_dev_matrix {
+  rk_ctx* owner;
+  DevMatrix m;
+};
+struct DevOutputsImpl {
+  rk_dev_outputs pub;
+  DBuf<double> sigma, u, v;
+};
+struct rk_dev_shard {
+  rk_ctx* owner;
+  const rk_dev_matrix* a;
+  Partition p;
+  rk_method method;
+  uint64_t seed;
+  std::unique_ptr<DevMatrix> repaired;  // null: the input itself (no edges)
+  const DevMatrix* rep() const { return repaired ? repaired.get() : &a->m; }
+};
+
+namespace {
+
+thread_local std::string g_error;
+thread_local double g_residual = 0.0;
+
+template <class F>
+rk_status guarded(F&& body) {
+  try {
+    body();
+    return RK_OK;
+  } catch (const Error& e) {
+    g_error = e.what();
+    g_residual = e.residual;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return RK_NOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return RK_RUNTIME;
+  }
+}
+
+template <class T>
+T* host_alloc(size_t n) {
+  T* p = static_cast<T*>(std::malloc((n ? n : 1) * sizeof(T)));
+  if (!p) fail(RK_NOMEM, "host allocation failed");
+  return p;
+}
+
+template <class T>
+T* host_copy(const T* d, size_t n, cudaStream_t s) {
+  T* h = host_alloc<T>(n);
+  if (n) RK_CUDA_CHECK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  return h;
+}
+
+void check_ctx(rk_ctx* ctx) {
+  if (!ctx) fail(RK_INVALID_ARGUMENT, "rk_ctx is NULL");
+}
+void check_view(const rk_sparse_view* a) {
+  if (!a) fail(RK_INVALID_ARGUMENT, "sparse view is NULL");
+}
+
+void report_to_host(const RepairOut& r, const Partition& p, rk_repair_report* out, cudaStream_t s) {
+  std::memset(out, 0, sizeof *out);
+  const uint64_t n = r.edges.n;
+  out->n_edges = n;
+  std::vector<uint32_t> b, rw, cl;
+  std::vector<int32_t> mech;
+  to_host(b, r.edges.block.get(), n, s);
+  to_host(rw, r.edges.row.get(), n, s);
+  to_host(cl, r.edges.col.get(), n, s);
+  to_host(mech, r.edges.mech.get(), n, s);
+  sync(s);
+  out->block = host_alloc<uint64_t>(n);
+  out->row = host_alloc<uint64_t>(n);
+  out->col = host_alloc<uint64_t>(n);
+  out->mechanism = host_alloc<int32_t>(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    out->block[i] = b[i];
+    out->row[i] = rw[i];
+    out->col[i] = cl[i];
+    out->mechanism[i] = mech[i];
+  }
+  out->n_blocks = p.blocks;
+  out->lonely_counts = host_alloc<uint64_t>(p.blocks);
+  for (uint64_t d = 0; d < p.blocks; ++d) out->lonely_counts[d] = r.lonely_counts[d];
+  out->fallback_count = r.fallback;
+}
+
+// repair + the repaired matrix (null = unchanged input)
+std::unique_ptr<DevMatrix> repair_and_apply(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method,
+                                            uint64_t seed, RepairOut& rep) {
+  repair_device(a, p, method, seed, rep, c.stream);
+  if (rep.edges.n == 0) return nullptr;
+  auto out = std::make_unique<DevMatrix>();
+  apply_edges(a, rep.edges, *out, c.stream);
+  return out;
+}
+
+[[noreturn]] void throw_block_failure(const BlockStageResult& b, uint64_t d_lo) {
+  for (size_t i = 0; i < b.failures.size(); ++i)
+    if (!b.failures[i].empty())
+      fail(RK_RUNTIME, "block task " + std::to_string(d_lo + i) + " failed: " + b.failures[i]);
+  fail(RK_RUNTIME, "block task failed");
+}
+bool any_failure(const BlockStageResult& b) {
+  for (const auto& f : b.failures)
+    if (!f.empty()) return true;
+  return false;
+}
+
+// retained columns of recover_right_vectors (proxy.cpp:53-59)
+std::vector<uint32_t> retained_of(const double* sigma, uint64_t n, double tol) {
+  double smax = 0.0;
+  for (uint64_t j = 0; j < n; ++j) smax = std::max(smax, sigma[j]);
+  std::vector<uint32_t> ret;
+  for (uint64_t j = 0; j < n; ++j)
+    if (sigma[j] > tol * smax && sigma[j] > 0.0) ret.push_back((uint32_t)j);
+  return ret;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+struct FullRun {
+  RepairOut rep;
+  std::unique_ptr<DevMatrix> repaired;
+  BlockStageResult blocks;
+  MergeOut merge;
+  DBuf<double> v;
+  uint32_t r = 0;  // V columns
+};
+
+// repair -> blocks -> merge -> (V); everything device-resident
+void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, uint64_t keep, uint64_t seed,
+              uint32_t flags, uint64_t top_k, FullRun& fr, rk_timing* t) {
+  cudaStream_t s = c.stream;
+  const uint64_t launches0 = c.launches;
+  cudaEvent_t ev0 = c.ev[3], ev1 = c.ev[4], ev2 = c.ev[5], ev3 = c.ev[6], ev4 = c.ev[7];
+  RK_CUDA_CHECK(cudaEventRecord(ev0, s));
+  fr.repaired = repair_and_apply(c, a, p, method, seed, fr.rep);
+  const DevMatrix& rep = fr.repaired ? *fr.repaired : a;
+  RK_CUDA_CHECK(cudaEventRecord(ev1, s));
+  block_stage(c, rep, p, 0, p.blocks, keep, fr.blocks, nullptr);
+  if (any_failure(fr.blocks)) throw_block_failure(fr.blocks, 0);
+  RK_CUDA_CHECK(cudaEventRecord(ev2, s));
+  merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
+  RK_CUDA_CHECK(cudaEventRecord(ev3, s));
+  if (flags & RK_WANT_V) {
+    const uint32_t k = fr.merge.k;
+    const uint32_t kk = (top_k && top_k < k) ? (uint32_t)top_k : k;
+    std::vector<double> sig;
+    to_host(sig, fr.merge.sigma.get(), kk, s);
+    sync(s);
+    std::vector<uint32_t> ret = retained_of(sig.data(), kk, 1e-10);
+    fr.r = (uint32_t)ret.size();
+    fr.v.alloc(rep.csc.cols * (uint64_t)std::max<uint32_t>(fr.r, 1), s);
+    if (fr.r) {
+      DBuf<uint32_t> dret(fr.r, s);
+      to_device(dret.get(), ret.data(), ret.size(), s);
+      recover_v_device(rep.csc, fr.merge.u.get(), k, dret.get(), fr.merge.sigma.get(), fr.r, fr.v.get(), 0,
+                       rep.csc.cols, s);
+      sync(s);
+    }
+  }
+  RK_CUDA_CHECK(cudaEventRecord(ev4, s));
+  sync(s);
+  if (t) {
+    std::memset(t, 0, sizeof *t);
+    t->repair_ms = elapsed(ev0, ev1);
+    t->blocks_ms = elapsed(ev1, ev2);
+    t->merge_ms = elapsed(ev2, ev3);
+    t->recover_ms = elapsed(ev3, ev4);
+    t->total_ms = elapsed(ev0, ev4);
+    t->qr_ms = fr.blocks.qr_ms;
+    t->jacobi_ms = fr.blocks.jacobi_ms;
+    t->jacobi_sweeps_max = fr.blocks.sweeps_max;
+    t->jacobi_rotations = fr.blocks.rotations;
+    t->kernel_launches = c.launches - launches0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rk_last_error(void) { return g_error.c_str(); }
+double rk_last_residual(void) { return g_residual; }
+int32_t rk_abi_version(void) { return RK_ABI_VERSION; }
+
+rk_status rk_ctx_create(int32_t device, rk_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(RK_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= n) fail(RK_INVALID_ARGUMENT, "device ordinal out of range");
+    auto ctx = std::make_unique<rk_ctx>();
+    Ctx& c = ctx->c;
+    c.device = device;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    RK_CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RK_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      fail(RK_CUDA, std::string("libranky_b200 is built for sm_100a; device is ") + prop.name);
+    c.num_sms = prop.multiProcessorCount;
+    c.smem_optin = prop.sharedMemPerBlockOptin;
+    RK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.own, cudaStreamNonBlocking));
+    c.stream = c.own;
+    for (auto& ev : c.ev) RK_CUDA_CHECK(cudaEventCreate(&ev));
+    cudaSetDevice(prev);
+    *out = ctx.release();
+  });
+}
+
+rk_status rk_ctx_destroy(rk_ctx* ctx) {
+  if (!ctx) return RK_OK;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (auto& ev : ctx->c.ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(ctx->c.own);
+  delete ctx;
+  return RK_OK;
+}
+
+rk_status rk_ctx_set_stream(rk_ctx* ctx, void* stream) {
+  return guarded([&] {
+    check_ctx(ctx);
+    ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own;
+  });
+}
+
+rk_status rk_ctx_synchronize(rk_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    CallScope sc(&ctx->c);
+    sync(ctx->c.stream);
+  });
+}
+
+uint64_t rk_ctx_kernel_launches(const rk_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+void rk_svd_free(rk_svd* s) {
+  if (!s) return;
+  std::free(s->u); std::free(s->sigma); std::free(s->v);
+  std::memset(s, 0, sizeof *s);
+}
+void rk_repair_report_free(rk_repair_report* r) {
+  if (!r) return;
+  std::free(r->block); std::free(r->row); std::free(r->col); std::free(r->mechanism); std::free(r->lonely_counts);
+  std::memset(r, 0, sizeof *r);
+}
+void rk_sparse_free(rk_sparse* s) {
+  if (!s) return;
+  std::free(s->entries);
+  std::memset(s, 0, sizeof *s);
+}
+void rk_records_free(rk_records* r) {
+  if (!r) return;
+  std::free(r->kept); std::free(r->offset); std::free(r->payload);
+  std::memset(r, 0, sizeof *r);
+}
+void rk_pipeline_result_free(rk_pipeline_result* r) {
+  if (!r) return;
+  rk_svd_free(&r->svd);
+  rk_repair_report_free(&r->report);
+  rk_sparse_free(&r->repaired);
+  rk_records_free(&r->records);
+}
+
+rk_status rk_keyed_rng_next(rk_ctx* ctx, uint64_t n, uint64_t seed, const uint64_t* block, const uint64_t* row,
+                            uint64_t draws, uint64_t* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    if (!n || !draws) return;
+    DBuf<uint64_t> db(n, s), dr(n, s), dout(n * draws, s);
+    to_device(db.get(), block, n, s);
+    to_device(dr.get(), row, n, s);
+    rng_eval_device(n, seed, db.get(), dr.get(), draws, nullptr, dout.get(), s);
+    RK_CUDA_CHECK(cudaMemcpyAsync(out, dout.get(), n * draws * 8, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+rk_status rk_keyed_rng_below(rk_ctx* ctx, uint64_t n, uint64_t seed, const uint64_t* block, const uint64_t* row,
+                             const uint64_t* bound, uint64_t* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    if (!n) return;
+    for (uint64_t i = 0; i < n; ++i)
+      if (bound[i] == 0) fail(RK_INVALID_ARGUMENT, "KeyedRng::below: bound must be nonzero");
+    DBuf<uint64_t> db(n, s), dr(n, s), dbd(n, s), dout(n, s);
+    to_device(db.get(), block, n, s);
+    to_device(dr.get(), row, n, s);
+    to_device(dbd.get(), bound, n, s);
+    rng_eval_device(n, seed, db.get(), dr.get(), 1, dbd.get(), dout.get(), s);
+    RK_CUDA_CHECK(cudaMemcpyAsync(out, dout.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+rk_status rk_find_lonely_rows(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, uint64_t d, uint64_t* out,
+                              uint64_t* n_out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    CallScope sc(&ctx->c);
+    Partition p = make_partition(a->cols, block_count);
+    if (d >= block_count)
+      fail(RK_OUT_OF_RANGE, "block index " + std::to_string(d) + " of " + std::to_string(block_count));
+    DevMatrix m;
+    upload_entries(*a, m, ctx->c.stream);
+    std::vector<uint64_t> rows;
+    lonely_rows_device(m, p, d, rows, ctx->c.stream);
+    for (size_t i = 0; i < rows.size(); ++i) out[i] = rows[i];
+    *n_out = rows.size();
+  });
+}
+
+rk_status rk_repair(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, rk_method method, uint64_t seed,
+                    rk_sparse* repaired, rk_repair_report* report) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    if ((int)method < 0 || (int)method > 3) fail(RK_INVALID_ARGUMENT, "bad repair method");
+    Partition p = make_partition(a->cols, block_count);
+    DevMatrix m;
+    upload_entries(*a, m, c.stream);
+    RepairOut rep;
+    std::unique_ptr<DevMatrix> out = repair_and_apply(c, m, p, method, seed, rep);
+    if (repaired) csr_to_entries_host(out ? out->csr : m.csr, *repaired, c.stream);
+    if (report) report_to_host(rep, p, report, c.stream);
+  });
+}
+
+rk_status rk_dense_svd(rk_ctx* ctx, uint64_t rows, uint64_t cols, const double* a, rk_svd* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    std::memset(out, 0, sizeof *out);
+    if (rows > 0xffffffffull || cols > 0xffffffffull) fail(RK_INVALID_ARGUMENT, "dense_svd: matrix too large");
+    DBuf<double> da(rows * cols ? rows * cols : 1, c.stream);
+    to_device(da.get(), a, rows * cols, c.stream);
+    DenseSvdOut r;
+    dense_svd_dev(c, da.get(), (uint32_t)rows, (uint32_t)cols, r);
+    out->u_rows = rows;
+    out->u_cols = r.k;
+    out->n_sigma = r.k;
+    out->has_v = 1;
+    out->v_rows = cols;
+    out->v_cols = r.k;
+    out->u = host_copy(r.u.get(), rows * r.k, c.stream);
+    out->sigma = host_copy(r.sigma.get(), r.k, c.stream);
+    out->v = host_copy(r.v.get(), cols * r.k, c.stream);
+    sync(c.stream);
+  });
+}
+
+rk_status rk_block_svd(rk_ctx* ctx, const rk_sparse_view* block, uint64_t keep, rk_svd* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(block);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    std::memset(out, 0, sizeof *out);
+    if (keep == 0) fail(RK_INVALID_ARGUMENT, "block_svd: keep must be >= 1");
+    const uint64_t M = block->rows, N = block->cols;
+    if (M != 0 && (M * N) / M != N) fail(RK_INVALID_ARGUMENT, "dense_of: dimension overflow");
+    if (M * N > (uint64_t(1) << 26))
+      fail(RK_INVALID_ARGUMENT, "dense_of: " + std::to_string(M) + "x" + std::to_string(N) +
+                                    " exceeds the densification cap");
+    const uint64_t k_full = std::min(M, N);
+    if (k_full == 0) {
+      out->u_rows = M;
+      out->u = host_alloc<double>(0);
+      out->sigma = host_alloc<double>(0);
+      return;
+    }
+    DevMatrix m;
+    upload_entries(*block, m, c.stream);
+    Partition p = make_partition(N, 1);
+    BlockApiOut api;
+    const uint64_t k = std::min(keep, k_full);
+    api.u.alloc(M * k, c.stream);
+    api.sigma.alloc(M, c.stream);
+    api.deficient.alloc(M, c.stream);
+    api.deficient.zero();
+    BlockStageResult br;
+    block_stage(c, m, p, 0, 1, keep, br, &api);
+    if (!br.failures[0].empty()) {
+      const std::string& f = br.failures[0];
+      if (f.rfind("one-sided Jacobi", 0) == 0) fail(RK_CONVERGENCE, f, br.conv_residual);
+      fail(RK_INVALID_ARGUMENT, f);
+    }
+    std::vector<uint8_t> def;
+    to_host(def, api.deficient.get(), k, c.stream);
+    sync(c.stream);
+    bool any = false;
+    for (uint8_t x : def) any |= x != 0;
+    if (any) {
+      DBuf<int> fl(1, c.stream);
+      fl.zero();
+      complete_columns_device(api.u.get(), (uint32_t)M, (uint32_t)k, api.deficient.get(), fl.get(), c.stream);
+      int h = 0;
+      RK_CUDA_CHECK(cudaMemcpyAsync(&h, fl.get(), sizeof h, cudaMemcpyDeviceToHost, c.stream));
+      sync(c.stream);
+      if (h) fail(RK_CONVERGENCE, "orthonormal completion has no independent direction (residual 0.000000)", 0.0);
+      sign_rows(api.u.get(), (uint32_t)M, (uint32_t)k, nullptr, 0, c.stream);
+    }
+    out->u_rows = M;
+    out->u_cols = k;
+    out->n_sigma = k;
+    out->u = host_copy(api.u.get(), M * k, c.stream);
+    out->sigma = host_copy(api.sigma.get(), k, c.stream);
+    sync(c.stream);
+  });
+}
+
+rk_status rk_proxy_svd(rk_ctx* ctx, uint64_t rows, uint64_t total_cols, const double* proxy, uint64_t n_offsets,
+                       const uint64_t* block_offsets, rk_svd* out) {
+  if (n_offsets == 0 || !block_offsets || block_offsets[n_offsets - 1] != total_cols) {
+    g_error = "proxy_svd: malformed block offsets";
+    return RK_INVALID_ARGUMENT;
+  }
+  return rk_dense_svd(ctx, rows, total_cols, proxy, out);
+}
+
+rk_status rk_recover_right_vectors(rk_ctx* ctx, const rk_sparse_view* a, uint64_t u_rows, uint64_t u_cols,
+                                   const double* u, uint64_t n_sigma, const double* sigma, double tol,
+                                   rk_svd* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    std::memset(out, 0, sizeof *out);
+    if (u_rows != a->rows || u_cols != n_sigma)
+      fail(RK_INVALID_ARGUMENT, "recover_right_vectors: factor shapes disagree");
+    std::vector<uint32_t> ret = retained_of(sigma, n_sigma, tol);
+    const uint32_t r = (uint32_t)ret.size();
+    out->has_v = 1;
+    out->v_rows = a->cols;
+    out->v_cols = r;
+    out->u = host_alloc<double>(0);
+    out->sigma = host_alloc<double>(0);
+    if (r == 0 || a->cols == 0) {
+      out->v = static_cast<double*>(std::calloc(a->cols * r ? a->cols * r : 1, sizeof(double)));
+      return;
+    }
+    DevMatrix m;
+    upload_entries(*a, m, c.stream);
+    DBuf<double> du(u_rows * u_cols, c.stream), ds(n_sigma, c.stream), dv(a->cols * r, c.stream);
+    DBuf<uint32_t> dret(r, c.stream);
+    to_device(du.get(), u, u_rows * u_cols, c.stream);
+    to_device(ds.get(), sigma, n_sigma, c.stream);
+    to_device(dret.get(), ret.data(), r, c.stream);
+    recover_v_device(m.csc, du.get(), (uint32_t)u_cols, dret.get(), ds.get(), r, dv.get(), 0, a->cols, c.stream);
+    out->v = host_copy(dv.get(), a->cols * r, c.stream);
+    sync(c.stream);
+  });
+}
+
+rk_status rk_run_block_tasks(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, uint64_t keep,
+                             rk_records* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    std::memset(out, 0, sizeof *out);
+    Partition p = make_partition(a->cols, block_count);
+    DevMatrix m;
+    upload_entries(*a, m, c.stream);
+    BlockStageResult br;
+    block_stage(c, m, p, 0, p.blocks, keep, br, nullptr);
+    if (any_failure(br)) throw_block_failure(br, 0);
+    out->n_records = p.blocks;
+    out->rows = a->rows;
+    out->kept = host_alloc<uint32_t>(p.blocks);
+    out->offset = host_alloc<uint64_t>(p.blocks);
+    for (uint64_t d = 0; d < p.blocks; ++d) {
+      out->kept[d] = br.kept[d];
+      out->offset[d] = br.offset[d];
+    }
+    out->payload = host_copy(br.payload.get(), br.payload.n, c.stream);
+    sync(c.stream);
+  });
+}
+
+rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, rk_method method, uint64_t keep,
+                          uint64_t seed, uint64_t workers, uint32_t flags, uint64_t top_k, rk_pipeline_result* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    std::memset(out, 0, sizeof *out);
+    if (workers == 0) fail(RK_INVALID_ARGUMENT, "workers must be >= 1");
+    if ((int)method < 0 || (int)method > 3) fail(RK_INVALID_ARGUMENT, "bad repair method");
+    Partition p = make_partition(a->cols, block_count);
+    DevMatrix m;
+    upload_entries(*a, m, c.stream);
+    FullRun fr;
+    full_run(c, m, p, method, keep, seed, flags, top_k, fr, &out->timing);
+    cudaStream_t s = c.stream;
+    const uint64_t M = a->rows;
+    const uint32_t k = fr.merge.k;
+    out->svd.u_rows = M;
+    out->svd.u_cols = k;
+    out->svd.n_sigma = k;
+    out->svd.u = host_copy(fr.merge.u.get(), M * k, s);
+    out->svd.sigma = host_copy(fr.merge.sigma.get(), k, s);
+    if (flags & RK_WANT_V) {
+      out->svd.has_v = 1;
+      out->svd.v_rows = a->cols;
+      out->svd.v_cols = fr.r;
+      out->svd.v = host_copy(fr.v.get(), a->cols * (uint64_t)fr.r, s);
+    }
+    report_to_host(fr.rep, p, &out->report, s);
+    if (flags & RK_WANT_REPAIRED) csr_to_entries_host(fr.repaired ? fr.repaired->csr : m.csr, out->repaired, s);
+    if (flags & RK_WANT_RECORDS) {
+      out->records.n_records = p.blocks;
+      out->records.rows = M;
+      out->records.kept = host_alloc<uint32_t>(p.blocks);
+      out->records.offset = host_alloc<uint64_t>(p.blocks);
+      for (uint64_t d = 0; d < p.blocks; ++d) {
+        out->records.kept[d] = fr.blocks.kept[d];
+        out->records.offset[d] = fr.blocks.offset[d];
+      }
+      out->records.payload = host_copy(fr.blocks.payload.get(), fr.blocks.payload.n, s);
+    }
+    sync(s);
+  });
+}
+
+rk_status rk_dev_matrix_create(rk_ctx* ctx, const rk_sparse_view* a, rk_dev_matrix** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    CallScope sc(&ctx->c);
+    auto m = std::make_unique<rk_dev_matrix>();
+    m->owner = ctx;
+    upload_entries(*a, m->m, ctx->c.stream);
+    sync(ctx->c.stream);
+    *out = m.release();
+  });
+}
+
+rk_status rk_dev_matrix_destroy(rk_dev_matrix* m) {
+  if (!m) return RK_OK;
+  return guarded([&] {
+    CallScope sc(&m->owner->c);
+    sync(m->owner->c.stream);
+    delete m;
+  });
+}
+
+uint64_t rk_dev_matrix_nnz(const rk_dev_matrix* m) { return m ? m->m.csr.nnz : 0; }
+
+rk_status rk_dev_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method, uint64_t keep,
+                          uint64_t seed, uint32_t flags, uint64_t top_k, rk_dev_outputs** out, rk_timing* timing) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!a || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    Partition p = make_partition(a->m.csr.cols, block_count);
+    FullRun fr;
+    full_run(c, a->m, p, method, keep, seed, flags, top_k, fr, timing);
+    auto o = std::make_unique<DevOutputsImpl>();
+    o->pub.rows = a->m.csr.rows;
+    o->pub.cols = a->m.csr.cols;
+    o->pub.k_sigma = fr.merge.k;
+    o->pub.k_v = fr.r;
+    o->pub.n_edges = fr.rep.edges.n;
+    o->sigma = std::move(fr.merge.sigma);
+    o->u = std::move(fr.merge.u);
+    o->v = std::move(fr.v);
+    o->pub.d_sigma = o->sigma.get();
+    o->pub.d_u = o->u.get();
+    o->pub.d_v = (flags & RK_WANT_V) ? o->v.get() : nullptr;
+    *out = &o.release()->pub;
+  });
+}
+
+rk_status rk_dev_outputs_free(rk_dev_outputs* o) {
+  if (!o) return RK_OK;
+  delete reinterpret_cast<DevOutputsImpl*>(o);
+  return RK_OK;
+}
+
+uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count, uint64_t keep) {
+  try {
+    Partition p = make_partition(cols, block_count);
+    std::vector<uint32_t> kept(block_count);
+    for (uint64_t d = 0; d < block_count; ++d) {
+      const uint64_t w = p.end(d) - p.begin(d), k_full = std::min(rows, w);
+      kept[d] = (uint32_t)(keep == 0 ? k_full : std::min(keep, k_full));
+    }
+    return merge_leaves(kept, (uint32_t)rows).size();
+  } catch (...) {
+    return 0;
+  }
+}
+
+rk_status rk_dev_shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
+                              uint64_t keep, uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi, double* d_root_out,
+                              rk_dev_shard** shard_out, rk_timing* timing) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!a || !shard_out || !d_root_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    cudaStream_t s = c.stream;
+    const uint64_t launches0 = c.launches;
+    auto sh = std::make_unique<rk_dev_shard>();
+    sh->owner = ctx;
+    sh->a = a;
+    sh->p = make_partition(a->m.csr.cols, block_count);
+    sh->method = method;
+    sh->seed = seed;
+    const uint32_t M = (uint32_t)a->m.csr.rows;
+    // the tree's leaves from the per-block kept counts
+    std::vector<uint32_t> kept(block_count);
+    for (uint64_t d = 0; d < block_count; ++d) {
+      const uint64_t w = sh->p.end(d) - sh->p.begin(d), k_full = std::min<uint64_t>(M, w);
+      kept[d] = (uint32_t)(keep == 0 ? k_full : std::min(keep, k_full));
+    }
+    std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
+    if (leaf_lo >= leaf_hi || leaf_hi > leaves.size()) fail(RK_OUT_OF_RANGE, "leaf range outside the merge tree");
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
+    RepairOut rep;
+    sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, rep);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
+    const uint64_t d_lo = leaves[leaf_lo].r0, d_hi = leaves[leaf_hi - 1].r1;
+    BlockStageResult br;
+    block_stage(c, *sh->rep(), sh->p, d_lo, d_hi, keep, br, nullptr);
+    if (any_failure(br)) throw_block_failure(br, d_lo);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
+    // leaves re-indexed to the shard's records
+    std::vector<TreeLeaf> local(leaves.begin() + leaf_lo, leaves.begin() + leaf_hi);
+    for (TreeLeaf& L : local) { L.r0 -= (uint32_t)d_lo; L.r1 -= (uint32_t)d_lo; }
+    DBuf<double> R;
+    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, local, 0, local.size(), R);
+    RK_CUDA_CHECK(cudaMemcpyAsync(d_root_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice, s));
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[6], s));
+    sync(s);
+    if (timing) {
+      std::memset(timing, 0, sizeof *timing);
+      timing->repair_ms = elapsed(c.ev[3], c.ev[4]);
+      timing->blocks_ms = elapsed(c.ev[4], c.ev[5]);
+      timing->merge_ms = elapsed(c.ev[5], c.ev[6]);
+      timing->total_ms = elapsed(c.ev[3], c.ev[6]);
+      timing->qr_ms = br.qr_ms;
+      timing->jacobi_ms = br.jacobi_ms;
+      timing->jacobi_sweeps_max = br.sweeps_max;
+      timing->jacobi_rotations = br.rotations;
+      timing->kernel_launches = c.launches - launches0;
+    }
+    *shard_out = sh.release();
+  });
+}
+
+rk_status rk_dev_shard_finish(rk_ctx* ctx, rk_dev_shard* shard, const double* d_roots, uint64_t n_roots,
+                              uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi, rk_dev_outputs** out,
+                              rk_timing* timing) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!shard || !d_roots || !out || n_roots == 0) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    cudaStream_t s = c.stream;
+    const uint64_t launches0 = c.launches;
+    const DevMatrix& rep = *shard->rep();
+    const uint32_t M = (uint32_t)rep.csr.rows;
+    if (col_hi > rep.csc.cols || col_lo > col_hi) fail(RK_OUT_OF_RANGE, "column range outside the matrix");
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
+    std::vector<DBuf<double>> roots;
+    for (uint64_t g = 0; g < n_roots; ++g) {
+      roots.emplace_back((uint64_t)M * M, s);
+      RK_CUDA_CHECK(cudaMemcpyAsync(roots.back().get(), d_roots + g * (uint64_t)M * M, sizeof(double) * M * M,
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+    MergeOut mo;
+    merge_finish(c, roots, M, mo);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
+    auto o = std::make_unique<DevOutputsImpl>();
+    uint32_t r = 0;
+    if (flags & RK_WANT_V) {
+      const uint32_t kk = (top_k && top_k < mo.k) ? (uint32_t)top_k : mo.k;
+      std::vector<double> sig;
+      to_host(sig, mo.sigma.get(), kk, s);
+      sync(s);
+      std::vector<uint32_t> ret = retained_of(sig.data(), kk, 1e-10);
+      r = (uint32_t)ret.size();
+      o->v.alloc((col_hi - col_lo) * (uint64_t)std::max<uint32_t>(r, 1), s);
+      if (r) {
+        DBuf<uint32_t> dret(r, s);
+        to_device(dret.get(), ret.data(), r, s);
+        recover_v_device(rep.csc, mo.u.get(), mo.k, dret.get(), mo.sigma.get(), r, o->v.get(), col_lo, col_hi, s);
+        sync(s);
+      }
+    }
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
+    sync(s);
+    o->pub.rows = M;
+    o->pub.cols = col_hi - col_lo;
+    o->pub.k_sigma = mo.k;
+    o->pub.k_v = r;
+    o->sigma = std::move(mo.sigma);
+    o->u = std::move(mo.u);
+    o->pub.d_sigma = o->sigma.get();
+    o->pub.d_u = o->u.get();
+    o->pub.d_v = (flags & RK_WANT_V) ? o->v.get() : nullptr;
+    if (timing) {
+      std::memset(timing, 0, sizeof *timing);
+      timing->merge_ms = elapsed(c.ev[3], c.ev[4]);
+      timing->recover_ms = elapsed(c.ev[4], c.ev[5]);
+      timing->total_ms = elapsed(c.ev[3], c.ev[5]);
+      timing->kernel_launches = c.launches - launches0;
+    }
+    *out = &o.release()->pub;
+  });
+}
+
+rk_status rk_dev_shard_destroy(rk_dev_shard* shard) {
+  if (!shard) return RK_OK;
+  return guarded([&] {
+    CallScope sc(&shard->owner->c);
+    sync(shard->owner->c.stream);
+    delete shard;
+  });
+}
+
+}  // extern "C"

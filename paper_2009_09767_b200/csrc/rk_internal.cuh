@@ -1,0 +1,312 @@
+// rk_internal.cuh -- shared internals of libranky_b200 (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ranky_b200.h"
+
+namespace rk {
+
+// ---------------------------------------------------------------------------
+// errors: internal C++ exceptions, mapped to rk_status at the C boundary
+
+struct Error : std::runtime_error {
+  rk_status code;
+  double residual;
+  Error(rk_status c, const std::string& what, double res = 0.0)
+      : std::runtime_error(what), code(c), residual(res) {}
+};
+
+[[noreturn]] inline void fail(rk_status c, const std::string& what, double residual = 0.0) {
+  throw Error(c, what, residual);
+}
+
+#define RK_CUDA_CHECK(expr)                                                                  \
+  do {                                                                                      \
+    cudaError_t rk_e_ = (expr);                                                             \
+    if (rk_e_ != cudaSuccess)                                                               \
+      ::rk::fail(RK_CUDA, std::string(#expr) + ": " + cudaGetErrorString(rk_e_));          \
+  } while (0)
+
+// launch bookkeeping: every kernel launch goes through RK_LAUNCH so the context
+// can report how many of its kernels ran (bench.py "gpu_launches")
+extern thread_local uint64_t* g_launch_counter;
+#define RK_LAUNCH_CHECK()                                                                    \
+  do {                                                                                      \
+    if (::rk::g_launch_counter) ++*::rk::g_launch_counter;                                   \
+    cudaError_t rk_e_ = cudaGetLastError();                                                 \
+    if (rk_e_ != cudaSuccess)                                                               \
+      ::rk::fail(RK_CUDA, std::string("kernel launch: ") + cudaGetErrorString(rk_e_));     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// stream-ordered device buffer
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st);
+      if (e != cudaSuccess) {
+        p = nullptr;
+        n = 0;
+        cudaGetLastError();
+        fail(RK_NOMEM, std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
+                           " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
+  }
+  void zero() {
+    if (n) RK_CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  T* get() const { return p; }
+};
+
+template <class T>
+inline void to_host(std::vector<T>& dst, const T* src, size_t n, cudaStream_t s) {
+  dst.resize(n);
+  if (n) RK_CUDA_CHECK(cudaMemcpyAsync(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+template <class T>
+inline void to_device(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) RK_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+inline void sync(cudaStream_t s) { RK_CUDA_CHECK(cudaStreamSynchronize(s)); }
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// KeyedRng -- proj/src/rng.cpp:8-38, usable on host and device
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+struct KeyedRng {
+  uint64_t state;
+  __host__ __device__ __forceinline__ KeyedRng(uint64_t seed, uint64_t block, uint64_t row) {
+    state = mix64(seed + 0x9e3779b97f4a7c15ull);
+    state = mix64(state ^ (block + 0xbf58476d1ce4e5b9ull));
+    state = mix64(state ^ (row + 0x94d049bb133111ebull));
+  }
+  __host__ __device__ __forceinline__ uint64_t next() {
+    state += 0x9e3779b97f4a7c15ull;
+    return mix64(state);
+  }
+  // unbiased: reject draws below 2^64 mod bound
+  __host__ __device__ __forceinline__ uint64_t below(uint64_t bound) {
+    const uint64_t threshold = (0 - bound) % bound;
+    for (;;) {
+      const uint64_t r = next();
+      if (r >= threshold) return r % bound;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// column partition -- proj/src/partition.cpp:38-51: width floor(N/D), the last
+// block absorbs the remainder
+
+struct Partition {
+  uint64_t n_cols = 0, blocks = 0, width = 0;
+  __host__ __device__ uint64_t begin(uint64_t d) const { return d * width; }
+  __host__ __device__ uint64_t end(uint64_t d) const { return d + 1 == blocks ? n_cols : (d + 1) * width; }
+  __host__ __device__ uint64_t block_of(uint64_t col) const {
+    uint64_t d = col / width;
+    return d < blocks ? d : blocks - 1;
+  }
+};
+
+inline Partition make_partition(uint64_t n_cols, uint64_t blocks) {
+  if (blocks == 0 || blocks > n_cols)
+    fail(RK_INVALID_ARGUMENT, "cannot split " + std::to_string(n_cols) + " columns into " +
+                                  std::to_string(blocks) + " blocks");
+  Partition p;
+  p.n_cols = n_cols;
+  p.blocks = blocks;
+  p.width = n_cols / blocks;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// device sparse matrix: CSR (row order) and CSC (column order), both with
+// 64-bit offsets, 32-bit indices and FP64 values
+
+struct DevCsr {
+  uint64_t rows = 0, cols = 0, nnz = 0;
+  DBuf<uint64_t> ptr;   // rows + 1
+  DBuf<uint32_t> idx;   // column index
+  DBuf<double> val;
+};
+struct DevCsc {
+  uint64_t rows = 0, cols = 0, nnz = 0;
+  DBuf<uint64_t> ptr;   // cols + 1
+  DBuf<uint32_t> idx;   // row index, ascending within a column
+  DBuf<double> val;
+};
+
+struct DevMatrix {
+  DevCsr csr;
+  DevCsc csc;
+};
+
+// ---------------------------------------------------------------------------
+// context
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  uint64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+// RAII: activates the context's device and launch counter for one API call
+struct CallScope {
+  int prev_device = -1;
+  uint64_t* prev_counter = nullptr;
+  explicit CallScope(Ctx* c);
+  ~CallScope();
+};
+
+// ---------------------------------------------------------------------------
+// kernels & launchers (one .cu per group)
+
+// rk_scan.cu -- exclusive prefix sums (deterministic)
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);  // out has n+1
+void exclusive_scan_u32to64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
+
+// rk_ingest.cu -- entries -> CSR, CSR -> CSC, CSC + edges -> repaired CSC/CSR
+void upload_entries(const rk_sparse_view& a, DevMatrix& m, cudaStream_t s);
+void csr_to_csc(const DevCsr& a, DevCsc& out, cudaStream_t s);
+void csr_to_entries_host(const DevCsr& a, rk_sparse& out, cudaStream_t s);
+
+struct DevEdges {  // repair edges in report order
+  uint64_t n = 0;
+  DBuf<uint32_t> block, row, col;
+  DBuf<int32_t> mech;
+};
+void apply_edges(const DevMatrix& a, const DevEdges& e, DevMatrix& out, cudaStream_t s);
+
+// rk_repair.cu
+struct RepairOut {
+  DevEdges edges;
+  std::vector<uint64_t> lonely_counts;
+  uint64_t fallback = 0;
+};
+void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uint64_t seed,
+                   RepairOut& out, cudaStream_t s);
+void lonely_rows_device(const DevMatrix& a, const Partition& p, uint64_t d, std::vector<uint64_t>& out,
+                        cudaStream_t s);
+void rng_eval_device(uint64_t n, uint64_t seed, const uint64_t* block, const uint64_t* row,
+                     uint64_t draws, const uint64_t* bound, uint64_t* out, cudaStream_t s);
+
+// rk_dense.cu -- QR, Jacobi, finalize, completion, apply_q (batched)
+struct QrJob {        // one tall matrix, column-major, in place
+  double* a;          // m x n, leading dimension lda
+  uint64_t lda;
+  uint32_t m, n;
+  double* diag;       // n: R's diagonal
+  double* beta;       // n: Householder betas (0 = identity)
+  double* tmat;       // ceil(n/NB) * NB * NB: compact-WY T factors
+};
+void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms);
+
+// W := R^T (transpose=true) or R (false) from a factored QrJob; W is n x n col-major,
+// zero-filled outside the triangle. rows: number of R rows (min(m, n)).
+struct RJob {
+  const double* a; uint64_t lda; const double* diag; uint32_t m, n;
+  double* w; uint64_t ldw;
+};
+void r_extract_batched(const std::vector<RJob>& jobs, bool transpose, cudaStream_t s);
+
+struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-major)
+  double* w;          // rows x cols_pad, ldw = rows
+  double* v;          // optional: cols x cols_pad accumulated rotations (col-major, ld = cols_pad) or null
+  uint32_t rows, cols, cols_pad;
+  double* alpha;      // cols_pad scratch
+  uint64_t* stats;    // [0] sweeps, [1] rotations, [2] status (0 ok, 1 not converged), [3] residual bits, [4..7] scratch
+};
+void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin);
+
+// finalize: sigma = column norms, stable descending sort, u = w/sigma, sign
+// convention; optional payload (rows x k row-major, u*sigma) and U/sigma outputs
+struct FinalJob {
+  const double* w;    // rows x cols (ld = rows)
+  uint32_t rows, cols, k;
+  double* payload;    // rows x k row-major (nullable)
+  double* u;          // rows x k row-major (nullable)
+  double* sigma;      // k (nullable), descending
+  double* sigma_all;  // cols (nullable): all singular values, descending
+  uint32_t* order;    // cols scratch
+  double* scratch;    // cols scratch
+  const double* v_in; // optional cols x cols col-major rotations (ld = ldv) to permute into v_out
+  uint64_t ldv;
+  double* v_out;      // cols x k row-major (nullable)
+  uint8_t* deficient; // k flags out (nullable): sigma <= kRankTol * sigma_max or zero
+};
+void finalize_batched(const std::vector<FinalJob>& jobs, cudaStream_t s);
+// deterministic orthonormal completion of flagged columns -- svd.cpp:150-201
+void complete_columns_device(double* u_rowmajor, uint32_t rows, uint32_t cols, const uint8_t* deficient,
+                             int* d_fail, cudaStream_t s);
+// Jacobi planning: padded column count for rows x cols
+uint32_t jacobi_cols_pad(uint32_t rows, uint32_t cols, bool with_v, size_t smem_optin);
+// out (m x ncols col-major) = Q [x; 0] for a factored QrJob (svd.cpp:111-132)
+void apply_q_device(const QrJob& qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out,
+                    cudaStream_t s);
+
+// rk_spmm.cu -- V = A^T U Sigma^-1 over the CSC
+void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const uint32_t* retained,
+                      const double* sigma, uint32_t r, double* v, uint64_t col_lo, uint64_t col_hi,
+                      cudaStream_t s);
+
+// rk_compact.cu -- per-block compaction of the sparse block into the tall
+// factor input
+struct BlockPlan {
+  uint64_t block;
+  uint32_t n_multi, n_single;  // compacted rows
+  uint32_t n_rows;             // n_multi + n_single
+  bool tall;                   // n_rows > M: QR first; else W = T^T directly
+  uint64_t offset;             // doubles into the staging buffer
+};
+void compaction_counts(const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t d_hi,
+                       uint32_t* d_counts /* 2 * nblocks */, double* d_single /* nblocks * M */,
+                       cudaStream_t s);
+void compaction_fill(const DevMatrix& a, const Partition& p, const std::vector<BlockPlan>& plans,
+                     uint64_t d_lo, const double* d_single, double* staging, cudaStream_t s);
+
+}  // namespace rk

@@ -1,0 +1,680 @@
+// rk_pipeline.cu -- host orchestration of the device kernels.
+//
+//  block_stage    run_block_task for a range of blocks (proj/src/pipeline.cpp:11-16):
+//                 compaction -> batched QR (tall blocks) -> W = R^T -> batched
+//                 Jacobi -> finalize into the record payloads U*Sigma
+//                 (block_record.cpp:69-84).
+//  merge_*        proxy_svd of the concatenated records (proj/src/proxy.cpp:40-46):
+//                 P^T = [payload_0^T; payload_1^T; ...] is reduced by a TSQR tree
+//                 (leaves = consecutive records, fixed pairwise tree) to R_P, and a
+//                 Jacobi on W = R_P^T yields sigma and U of P directly -- V of P,
+//                 which run_pipeline discards (proj/src/pipeline.cpp:112), is never
+//                 formed.
+//  dense_svd_dev  dense_svd (proj/src/svd.cpp:365-379) with V: QR -> Jacobi on R
+//                 with accumulated rotations -> completion -> apply_q -> sign.
+#include <algorithm>
+#include <cstring>
+
+#include "rk_pipeline.cuh"
+
+namespace rk {
+
+size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
+
+namespace {
+
+unsigned grid_for(uint64_t n, unsigned cap = 65535 * 4) {
+  uint64_t g = ceil_div(n, 256);
+  if (g == 0) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+__global__ void nonfinite_blocks(const uint64_t* col_ptr, const double* val, uint64_t cols, Partition p,
+                                 uint32_t* bad) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cols;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t k = col_ptr[c]; k < col_ptr[c + 1]; ++k)
+      if (!isfinite(val[k])) { bad[p.block_of(c)] = 1u; break; }
+  }
+}
+
+__global__ void count_nonfinite(const double* x, uint64_t n, unsigned* flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *flag = 1u;
+}
+
+// [ra; rb] (heights ha, hb; column-major with ld n) -> column-major (ha+hb) x n
+__global__ void stack_r(const double* ra, uint32_t ha, const double* rb, uint32_t hb, uint32_t n, double* out) {
+  const uint32_t h = ha + hb;
+  const uint64_t total = (uint64_t)h * n;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t % h), c = (uint32_t)(t / h);
+    out[t] = i < ha ? ra[i + (uint64_t)c * n] : rb[(i - ha) + (uint64_t)c * n];
+  }
+}
+
+// leaf = records [r0, r1) of P^T stacked: column-major h x n
+__global__ void gather_leaf(const double* payload, const uint64_t* off, const uint32_t* kept, uint32_t r0,
+                            uint32_t r1, uint32_t n, uint32_t h, double* out) {
+  uint32_t base = 0;
+  for (uint32_t rec = r0; rec < r1; ++rec) {
+    const uint32_t k = kept[rec];
+    const double* src = payload + off[rec];
+    const uint64_t total = (uint64_t)k * n;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t j = (uint32_t)(t % k), col = (uint32_t)(t / k);  // payload: row-major n x k
+      out[(base + j) + (uint64_t)col * h] = src[(uint64_t)col * k + j];
+    }
+    base += k;
+  }
+}
+
+// row-major rows x k (payload) -> column-major rows x k at dst (ld rows)
+__global__ void rowmajor_to_colmajor(const double* src, uint32_t rows, uint32_t k, double* dst) {
+  const uint64_t total = (uint64_t)rows * k;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t % rows), c = (uint32_t)(t / rows);
+    dst[t] = src[(uint64_t)i * k + c];
+  }
+}
+
+// square column-major transpose (out = in^T), out has leading dimension n
+__global__ void transpose_sq(const double* in, uint32_t n, double* out) {
+  const uint64_t total = (uint64_t)n * n;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t % n), c = (uint32_t)(t / n);
+    out[t] = in[c + (uint64_t)i * n];
+  }
+}
+
+__global__ void sign_kernel(double* u, uint32_t rows, uint32_t k, double* v, uint32_t vrows) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < k; j += (gridDim.x * blockDim.x) >> 5) {
+    double best = -1.0;
+    uint32_t arg = 0;
+    for (uint32_t i = lane; i < rows; i += 32) {
+      const double mag = fabs(u[(uint64_t)i * k + j]);
+      if (mag > best) { best = mag; arg = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint32_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    if (rows && u[(uint64_t)arg * k + j] < 0.0) {
+      for (uint32_t i = lane; i < rows; i += 32) u[(uint64_t)i * k + j] = -u[(uint64_t)i * k + j];
+      if (v)
+        for (uint32_t i = lane; i < vrows; i += 32) v[(uint64_t)i * k + j] = -v[(uint64_t)i * k + j];
+    }
+  }
+}
+
+__global__ void identity_colmajor(double* v, uint32_t n, uint32_t ld, uint32_t ncols) {
+  const uint64_t total = (uint64_t)ld * ncols;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t % ld), c = (uint32_t)(t / ld);
+    v[t] = (i == c && i < n) ? 1.0 : 0.0;
+  }
+}
+
+// column-major (rows x cols, ld) -> row-major rows x cols
+__global__ void colmajor_to_rowmajor(const double* src, uint64_t ld, uint32_t rows, uint32_t cols, double* dst) {
+  const uint64_t total = (uint64_t)rows * cols;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t / cols), c = (uint32_t)(t % cols);
+    dst[t] = src[i + (uint64_t)c * ld];
+  }
+}
+
+struct JacobiStats {
+  uint64_t sweeps = 0, rotations = 0;
+  bool failed = false;
+  double residual = 0.0;
+};
+
+std::vector<JacobiStats> read_stats(const uint64_t* d_stats, size_t n, cudaStream_t s) {
+  std::vector<uint64_t> h;
+  to_host(h, d_stats, 8 * n, s);
+  sync(s);
+  std::vector<JacobiStats> out(n);
+  for (size_t i = 0; i < n; ++i) {
+    out[i].sweeps = h[8 * i];
+    out[i].rotations = h[8 * i + 1];
+    out[i].failed = h[8 * i + 2] != 0;
+    std::memcpy(&out[i].residual, &h[8 * i + 3], 8);
+  }
+  return out;
+}
+
+std::string residual_text(double r) { return std::to_string(r); }
+
+[[noreturn]] void throw_convergence(double residual) {
+  fail(RK_CONVERGENCE, "one-sided Jacobi did not converge (residual " + residual_text(residual) + ")", residual);
+}
+
+void complete_and_sign(Ctx& c, double* u, uint32_t rows, uint32_t k, const uint8_t* d_def, double* v,
+                       uint32_t vrows) {
+  cudaStream_t s = c.stream;
+  DBuf<int> fail_flag(1, s);
+  fail_flag.zero();
+  complete_columns_device(u, rows, k, d_def, fail_flag.get(), s);
+  int h = 0;
+  RK_CUDA_CHECK(cudaMemcpyAsync(&h, fail_flag.get(), sizeof h, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (h) fail(RK_CONVERGENCE, "orthonormal completion has no independent direction (residual 0.000000)", 0.0);
+  sign_rows(u, rows, k, v, vrows, s);
+}
+
+bool any_flag(const uint8_t* d, uint64_t n, cudaStream_t s) {
+  std::vector<uint8_t> h;
+  to_host(h, d, n, s);
+  sync(s);
+  for (uint8_t x : h)
+    if (x) return true;
+  return false;
+}
+
+}  // namespace
+
+void sign_rows(double* u, uint32_t rows, uint32_t k, double* v, uint32_t vrows, cudaStream_t s) {
+  if (!k) return;
+  sign_kernel<<<grid_for((uint64_t)k * 32), 256, 0, s>>>(u, rows, k, v, vrows);
+  RK_LAUNCH_CHECK();
+}
+
+void check_finite_or_throw(const double* x, uint64_t n, const char* what, cudaStream_t s) {
+  if (!n) return;
+  DBuf<unsigned> flag(1, s);
+  flag.zero();
+  count_nonfinite<<<grid_for(n), 256, 0, s>>>(x, n, flag.get());
+  RK_LAUNCH_CHECK();
+  unsigned h = 0;
+  RK_CUDA_CHECK(cudaMemcpyAsync(&h, flag.get(), sizeof h, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (h) fail(RK_INVALID_ARGUMENT, what);
+}
+
+// ---------------------------------------------------------------------------
+// block stage
+
+void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t d_hi, uint64_t keep,
+                 BlockStageResult& out, BlockApiOut* api) {
+  cudaStream_t s = c.stream;
+  const uint32_t M = (uint32_t)a.csr.rows;
+  const uint64_t nblk = d_hi - d_lo;
+  out.offset.assign(nblk, 0);
+  out.kept.assign(nblk, 0);
+  out.failures.assign(nblk, std::string());
+  if (nblk == 0) return;
+
+  // k per block (run_block_task, pipeline.cpp:12-13) and the densify cap (dense_matrix.cpp:62-75)
+  std::vector<char> skip(nblk, 0);
+  for (uint64_t i = 0; i < nblk; ++i) {
+    const uint64_t d = d_lo + i;
+    const uint64_t w = p.end(d) - p.begin(d);
+    const uint64_t k_full = std::min<uint64_t>(M, w);
+    const uint64_t k = keep == 0 ? k_full : std::min(keep, k_full);
+    if (k == 0) {
+      out.failures[i] = "block_svd: keep must be >= 1";
+      skip[i] = 1;
+    } else if ((uint64_t)M * w > (uint64_t(1) << 26)) {
+      out.failures[i] = "dense_of: " + std::to_string(M) + "x" + std::to_string(w) + " exceeds the densification cap";
+      skip[i] = 1;
+    }
+    out.kept[i] = skip[i] ? 0 : (uint32_t)k;
+  }
+  // non-finite values (svd.cpp:384-386)
+  {
+    DBuf<uint32_t> bad(p.blocks, s);
+    bad.zero();
+    if (a.csc.nnz) {
+      nonfinite_blocks<<<grid_for(a.csc.cols), 256, 0, s>>>(a.csc.ptr.get(), a.csc.val.get(), a.csc.cols, p,
+                                                            bad.get());
+      RK_LAUNCH_CHECK();
+    }
+    std::vector<uint32_t> hb;
+    to_host(hb, bad.get() + d_lo, nblk, s);
+    sync(s);
+    for (uint64_t i = 0; i < nblk; ++i)
+      if (hb[i] && !skip[i]) {
+        out.failures[i] = "block_svd: block has non-finite values";
+        skip[i] = 1;
+        out.kept[i] = 0;
+      }
+  }
+  uint64_t total_payload = 0;
+  for (uint64_t i = 0; i < nblk; ++i) {
+    out.offset[i] = total_payload;
+    total_payload += (uint64_t)M * out.kept[i];
+  }
+  out.payload.alloc(total_payload ? total_payload : 1, s);
+  if (M == 0) return;
+
+  // compaction plan
+  DBuf<uint32_t> counts(2 * nblk, s);
+  DBuf<double> single(nblk * (uint64_t)M, s);
+  compaction_counts(a, p, d_lo, d_hi, counts.get(), single.get(), s);
+  std::vector<uint32_t> hc;
+  to_host(hc, counts.get(), 2 * nblk, s);
+  sync(s);
+
+  size_t free_b = 0, total_b = 0;
+  RK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t budget = std::max<uint64_t>((uint64_t)(free_b * 0.4), 256ull << 20);
+  const uint32_t cols_pad_full = jacobi_cols_pad(M, M, false, c.smem_optin);
+  const uint64_t aux_sz = 2 * (uint64_t)M + (ceil_div(M, 16) + 1) * 256;
+
+  uint64_t i0 = 0;
+  while (i0 < nblk) {
+    std::vector<BlockPlan> plans;
+    uint64_t staging = 0, wdoubles = 0;
+    uint32_t max_cols = 1;
+    uint64_t i1 = i0;
+    for (; i1 < nblk; ++i1) {
+      if (skip[i1]) continue;
+      BlockPlan pl;
+      pl.block = d_lo + i1;
+      pl.n_multi = hc[2 * i1];
+      pl.n_single = hc[2 * i1 + 1];
+      pl.n_rows = pl.n_multi + pl.n_single;
+      pl.tall = pl.n_rows > M;
+      const uint64_t need = (pl.tall ? (uint64_t)pl.n_rows * M : 0) + (uint64_t)M * cols_pad_full + aux_sz;
+      if (!plans.empty() && (staging + wdoubles + need) * 8 > budget) break;
+      pl.offset = staging;
+      staging += pl.tall ? (uint64_t)pl.n_rows * M : 0;
+      wdoubles += (uint64_t)M * cols_pad_full + aux_sz;
+      max_cols = std::max(max_cols, std::min<uint32_t>(pl.n_rows, M));
+      plans.push_back(pl);
+    }
+    if (plans.empty()) { i0 = i1; continue; }
+    const size_t nb = plans.size();
+    const uint32_t cols_pad = jacobi_cols_pad(M, max_cols, false, c.smem_optin);
+    DBuf<double> st(staging ? staging : 1, s);
+    DBuf<double> W((uint64_t)nb * M * cols_pad, s);
+    DBuf<double> qr_aux((uint64_t)nb * aux_sz, s);
+    DBuf<double> alpha((uint64_t)nb * cols_pad, s);
+    DBuf<uint64_t> stats(8 * nb, s);
+    DBuf<uint32_t> order((uint64_t)nb * cols_pad, s);
+    DBuf<double> fscratch((uint64_t)nb * cols_pad, s);
+    if (staging) st.zero();
+    W.zero();
+    stats.zero();
+    std::vector<BlockPlan> fill_tall, fill_wide;
+    for (size_t q = 0; q < nb; ++q) {
+      if (plans[q].tall) {
+        fill_tall.push_back(plans[q]);
+      } else {
+        BlockPlan w = plans[q];
+        w.offset = (uint64_t)q * M * cols_pad;  // W = T^T written straight into the Jacobi slot
+        fill_wide.push_back(w);
+      }
+    }
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[0], s));
+    compaction_fill(a, p, fill_tall, d_lo, single.get(), st.get(), s);
+    compaction_fill(a, p, fill_wide, d_lo, single.get(), W.get(), s);
+    std::vector<QrJob> qj;
+    std::vector<RJob> rj;
+    for (size_t q = 0; q < nb; ++q) {
+      if (!plans[q].tall) continue;
+      double* aux = qr_aux.get() + (uint64_t)q * aux_sz;
+      QrJob j;
+      j.a = st.get() + plans[q].offset;
+      j.lda = plans[q].n_rows;
+      j.m = plans[q].n_rows;
+      j.n = M;
+      j.diag = aux;
+      j.beta = aux + M;
+      j.tmat = aux + 2 * M;
+      qj.push_back(j);
+      RJob r;
+      r.a = j.a; r.lda = j.lda; r.diag = j.diag; r.m = j.m; r.n = j.n;
+      r.w = W.get() + (uint64_t)q * M * cols_pad;
+      r.ldw = M;
+      rj.push_back(r);
+    }
+    qr_batched(qj, s, c.num_sms);
+    r_extract_batched(rj, /*transpose=*/true, s);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[1], s));
+    std::vector<JacobiJob> jj(nb);
+    for (size_t q = 0; q < nb; ++q) {
+      jj[q].w = W.get() + (uint64_t)q * M * cols_pad;
+      jj[q].v = nullptr;
+      jj[q].rows = M;
+      jj[q].cols = max_cols;
+      jj[q].cols_pad = cols_pad;
+      jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad;
+      jj[q].stats = stats.get() + 8 * q;
+    }
+    jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[2], s));
+    std::vector<FinalJob> fj(nb);
+    for (size_t q = 0; q < nb; ++q) {
+      const uint64_t i = plans[q].block - d_lo;
+      FinalJob& f = fj[q];
+      std::memset(&f, 0, sizeof f);
+      f.w = jj[q].w;
+      f.rows = M;
+      f.cols = cols_pad;
+      f.k = out.kept[i];
+      f.payload = out.payload.get() + out.offset[i];
+      f.order = order.get() + (uint64_t)q * cols_pad;
+      f.scratch = fscratch.get() + (uint64_t)q * cols_pad;
+      if (api) {
+        f.u = api->u.get() + out.offset[i];
+        f.sigma = api->sigma.get() + i * (uint64_t)M;
+        f.deficient = api->deficient.get() + i * (uint64_t)M;
+      }
+    }
+    finalize_batched(fj, s);
+    std::vector<JacobiStats> js = read_stats(stats.get(), nb, s);  // synchronizes
+    float ms_qr = 0, ms_j = 0;
+    cudaEventElapsedTime(&ms_qr, c.ev[0], c.ev[1]);
+    cudaEventElapsedTime(&ms_j, c.ev[1], c.ev[2]);
+    out.qr_ms += ms_qr;
+    out.jacobi_ms += ms_j;
+    for (size_t q = 0; q < nb; ++q) {
+      out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
+      out.rotations += js[q].rotations;
+      if (js[q].failed) {
+        const uint64_t i = plans[q].block - d_lo;
+        out.failures[i] = "one-sided Jacobi did not converge (residual " + residual_text(js[q].residual) + ")";
+        out.conv_residual = js[q].residual;
+      }
+    }
+    i0 = i1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// merge tree
+
+std::vector<TreeLeaf> merge_leaves(const std::vector<uint32_t>& kept, uint32_t M) {
+  std::vector<TreeLeaf> leaves;
+  size_t r0 = 0;
+  while (r0 < kept.size()) {
+    size_t r1 = r0;
+    uint32_t h = 0;
+    while (r1 < kept.size() && h < M) h += kept[r1++];
+    if (h > 0) leaves.push_back({(uint32_t)r0, (uint32_t)r1, h});
+    r0 = r1;
+  }
+  return leaves;
+}
+
+namespace {
+
+// QR every matrix of a level; returns their R factors (n x n column-major)
+void qr_level(Ctx& c, std::vector<DBuf<double>>& mats, std::vector<uint32_t>& hs, uint32_t n) {
+  cudaStream_t s = c.stream;
+  const size_t cnt = mats.size();
+  const uint64_t aux_sz = 2 * (uint64_t)n + (ceil_div(n, 16) + 1) * 256;
+  DBuf<double> aux(cnt * aux_sz, s);
+  std::vector<QrJob> qj;
+  std::vector<RJob> rj;
+  std::vector<DBuf<double>> rs;
+  rs.reserve(cnt);
+  for (size_t q = 0; q < cnt; ++q) {
+    QrJob j;
+    j.a = mats[q].get(); j.lda = hs[q]; j.m = hs[q]; j.n = n;
+    j.diag = aux.get() + q * aux_sz; j.beta = j.diag + n; j.tmat = j.diag + 2 * n;
+    qj.push_back(j);
+    rs.emplace_back((uint64_t)n * n, s);
+    RJob r;
+    r.a = j.a; r.lda = j.lda; r.diag = j.diag; r.m = j.m; r.n = n; r.w = rs.back().get(); r.ldw = n;
+    rj.push_back(r);
+  }
+  qr_batched(qj, s, c.num_sms);
+  r_extract_batched(rj, /*transpose=*/false, s);
+  for (size_t q = 0; q < cnt; ++q) hs[q] = std::min<uint32_t>(hs[q], n);
+  mats = std::move(rs);
+}
+
+// pairwise tree over R factors (heights <= n): returns the root
+void tree_reduce(Ctx& c, std::vector<DBuf<double>>& nodes, std::vector<uint32_t>& heights, uint32_t n) {
+  cudaStream_t s = c.stream;
+  while (nodes.size() > 1) {
+    std::vector<DBuf<double>> next;
+    std::vector<uint32_t> nh;
+    for (size_t q = 0; q + 1 < nodes.size(); q += 2) {
+      const uint32_t h = heights[q] + heights[q + 1];
+      next.emplace_back((uint64_t)h * n, s);
+      stack_r<<<grid_for((uint64_t)h * n), 256, 0, s>>>(nodes[q].get(), heights[q], nodes[q + 1].get(),
+                                                         heights[q + 1], n, next.back().get());
+      RK_LAUNCH_CHECK();
+      nh.push_back(h);
+    }
+    qr_level(c, next, nh, n);
+    if (nodes.size() & 1) {
+      next.push_back(std::move(nodes.back()));
+      nh.push_back(heights.back());
+    }
+    nodes = std::move(next);
+    heights = std::move(nh);
+  }
+}
+
+}  // namespace
+
+void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
+                   const std::vector<uint32_t>& kept, uint32_t M, const std::vector<TreeLeaf>& leaves,
+                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out) {
+  cudaStream_t s = c.stream;
+  DBuf<uint64_t> doff(offset.size(), s);
+  DBuf<uint32_t> dkept(kept.size(), s);
+  to_device(doff.get(), offset.data(), offset.size(), s);
+  to_device(dkept.get(), kept.data(), kept.size(), s);
+  std::vector<DBuf<double>> nodes;
+  std::vector<uint32_t> heights;
+  for (size_t l = leaf_lo; l < leaf_hi; ++l) {
+    const TreeLeaf& L = leaves[l];
+    nodes.emplace_back((uint64_t)L.height * M, s);
+    heights.push_back(L.height);
+    gather_leaf<<<grid_for((uint64_t)L.height * M), 256, 0, s>>>(payload, doff.get(), dkept.get(), L.r0, L.r1, M,
+                                                                 L.height, nodes.back().get());
+    RK_LAUNCH_CHECK();
+  }
+  qr_level(c, nodes, heights, M);
+  tree_reduce(c, nodes, heights, M);
+  r_out = std::move(nodes[0]);
+  sync(s);  // host vectors (offset copies) are released
+}
+
+void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut& out) {
+  cudaStream_t s = c.stream;
+  std::vector<uint32_t> heights(roots.size(), M);
+  tree_reduce(c, roots, heights, M);
+  const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
+  DBuf<double> W((uint64_t)M * cp, s);
+  W.zero();
+  transpose_sq<<<grid_for((uint64_t)M * M), 256, 0, s>>>(roots[0].get(), M, W.get());
+  RK_LAUNCH_CHECK();
+  out.k = M;
+  out.sigma.alloc(M, s);
+  out.u.alloc((uint64_t)M * M, s);
+  DBuf<double> alpha(cp, s);
+  DBuf<uint64_t> stats(8, s);
+  stats.zero();
+  std::vector<JacobiJob> jj(1);
+  jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = M; jj[0].cols_pad = cp;
+  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
+  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+  JacobiStats js = read_stats(stats.get(), 1, s)[0];
+  out.sweeps = js.sweeps;
+  out.rotations = js.rotations;
+  if (js.failed) throw_convergence(js.residual);
+  DBuf<uint32_t> order(cp, s);
+  DBuf<double> scratch(cp, s);
+  DBuf<uint8_t> def(M, s);
+  FinalJob f;
+  std::memset(&f, 0, sizeof f);
+  f.w = W.get(); f.rows = M; f.cols = cp; f.k = M;
+  f.u = out.u.get(); f.sigma = out.sigma.get();
+  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
+  finalize_batched({f}, s);
+  if (any_flag(def.get(), M, s)) complete_and_sign(c, out.u.get(), M, M, def.get(), nullptr, 0);
+}
+
+void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
+                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out) {
+  cudaStream_t s = c.stream;
+  uint64_t total = 0;
+  for (uint32_t k : kept) total += k;
+  if (M == 0 || total == 0) {
+    out.k = 0;
+    out.sigma.alloc(1, s);
+    out.u.alloc(1, s);
+    return;
+  }
+  if (total > M) {
+    std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
+    std::vector<DBuf<double>> roots(1);
+    merge_subtree(c, payload, offset, kept, M, leaves, 0, leaves.size(), roots[0]);
+    merge_finish(c, roots, M, out);
+    return;
+  }
+  // P^T is not taller than wide: Jacobi straight on P's columns (W = P)
+  const uint32_t tc = (uint32_t)total;
+  const uint32_t cp = jacobi_cols_pad(M, tc, false, c.smem_optin);
+  DBuf<double> W((uint64_t)M * cp, s);
+  W.zero();
+  uint64_t col = 0;
+  for (size_t r = 0; r < kept.size(); ++r) {
+    if (!kept[r]) continue;
+    rowmajor_to_colmajor<<<grid_for((uint64_t)M * kept[r]), 256, 0, s>>>(payload + offset[r], M, kept[r],
+                                                                         W.get() + col * M);
+    RK_LAUNCH_CHECK();
+    col += kept[r];
+  }
+  out.k = tc;
+  out.sigma.alloc(tc, s);
+  out.u.alloc((uint64_t)M * tc, s);
+  DBuf<double> alpha(cp, s);
+  DBuf<uint64_t> stats(8, s);
+  stats.zero();
+  std::vector<JacobiJob> jj(1);
+  jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = tc; jj[0].cols_pad = cp;
+  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
+  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+  JacobiStats js = read_stats(stats.get(), 1, s)[0];
+  out.sweeps = js.sweeps;
+  out.rotations = js.rotations;
+  if (js.failed) throw_convergence(js.residual);
+  DBuf<uint32_t> order(cp, s);
+  DBuf<double> scratch(cp, s);
+  DBuf<uint8_t> def(tc, s);
+  FinalJob f;
+  std::memset(&f, 0, sizeof f);
+  f.w = W.get(); f.rows = M; f.cols = cp; f.k = tc;
+  f.u = out.u.get(); f.sigma = out.sigma.get();
+  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
+  finalize_batched({f}, s);
+  if (any_flag(def.get(), tc, s)) complete_and_sign(c, out.u.get(), M, tc, def.get(), nullptr, 0);
+}
+
+// ---------------------------------------------------------------------------
+// dense_svd with V (svd.cpp:365-379 / svd_tall :316-332)
+
+void dense_svd_dev(Ctx& c, const double* a, uint32_t rows, uint32_t cols, DenseSvdOut& out) {
+  cudaStream_t s = c.stream;
+  check_finite_or_throw(a, (uint64_t)rows * cols, "dense_svd: input has non-finite values", s);
+  const uint32_t k = std::min(rows, cols);
+  out.k = k;
+  if (k == 0) {
+    out.u.alloc(1, s); out.sigma.alloc(1, s); out.v.alloc(1, s);
+    return;
+  }
+  const bool transposed = rows < cols;
+  const uint32_t m = transposed ? cols : rows, n = k;  // B = transposed ? A^T : A, column-major m x n
+  DBuf<double> B((uint64_t)m * n, s);
+  // colmat_of (svd.cpp:39-49): column-major of A^T is A row-major as is
+  if (transposed) {
+    RK_CUDA_CHECK(cudaMemcpyAsync(B.get(), a, sizeof(double) * (uint64_t)m * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    rowmajor_to_colmajor<<<grid_for((uint64_t)m * n), 256, 0, s>>>(a, m, n, B.get());
+    RK_LAUNCH_CHECK();
+  }
+  const bool with_qr = m > n;
+  const uint64_t aux_sz = 2 * (uint64_t)n + (ceil_div(n, 16) + 1) * 256;
+  DBuf<double> aux(aux_sz, s);
+  QrJob qj;
+  qj.a = B.get(); qj.lda = m; qj.m = m; qj.n = n; qj.diag = aux.get(); qj.beta = qj.diag + n; qj.tmat = qj.diag + 2 * n;
+  const uint32_t cp = jacobi_cols_pad(n, n, true, c.smem_optin);
+  DBuf<double> W((uint64_t)n * cp, s), Vr((uint64_t)cp * cp, s);
+  W.zero();
+  if (with_qr) {
+    qr_batched({qj}, s, c.num_sms);
+    RJob r;
+    r.a = qj.a; r.lda = qj.lda; r.diag = qj.diag; r.m = m; r.n = n; r.w = W.get(); r.ldw = n;
+    r_extract_batched({r}, /*transpose=*/false, s);
+  } else {
+    RK_CUDA_CHECK(cudaMemcpyAsync(W.get(), B.get(), sizeof(double) * (uint64_t)n * n, cudaMemcpyDeviceToDevice, s));
+  }
+  identity_colmajor<<<grid_for((uint64_t)cp * cp), 256, 0, s>>>(Vr.get(), n, cp, cp);
+  RK_LAUNCH_CHECK();
+  DBuf<double> alpha(cp, s);
+  DBuf<uint64_t> stats(8, s);
+  stats.zero();
+  std::vector<JacobiJob> jj(1);
+  jj[0].w = W.get(); jj[0].v = Vr.get(); jj[0].rows = n; jj[0].cols = n; jj[0].cols_pad = cp;
+  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
+  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+  JacobiStats js = read_stats(stats.get(), 1, s)[0];
+  if (js.failed) throw_convergence(js.residual);
+  // sort, U_R = columns / sigma (+ completion), V_R permuted
+  DBuf<double> ur((uint64_t)n * n, s), vr((uint64_t)n * n, s);  // row-major n x n
+  DBuf<uint32_t> order(cp, s);
+  DBuf<double> scratch(cp, s);
+  DBuf<uint8_t> def(n, s);
+  out.sigma.alloc(n, s);
+  FinalJob f;
+  std::memset(&f, 0, sizeof f);
+  f.w = W.get(); f.rows = n; f.cols = n; f.k = n;
+  f.u = ur.get(); f.sigma = out.sigma.get();
+  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
+  f.v_in = Vr.get(); f.ldv = cp; f.v_out = vr.get();
+  finalize_batched({f}, s);
+  // the finalize sign flips are undone by the final sign convention below only
+  // through U_A; completion must see the unflipped basis, which it does not
+  // depend on (it only needs orthonormal placed columns)
+  if (any_flag(def.get(), n, s)) {
+    DBuf<int> fl(1, s);
+    fl.zero();
+    complete_columns_device(ur.get(), n, n, def.get(), fl.get(), s);
+    int h = 0;
+    RK_CUDA_CHECK(cudaMemcpyAsync(&h, fl.get(), sizeof h, cudaMemcpyDeviceToHost, s));
+    sync(s);
+    if (h) fail(RK_CONVERGENCE, "orthonormal completion has no independent direction (residual 0.000000)", 0.0);
+  }
+  // U_B (m x n row-major) = Q U_R when QR was used, else U_R
+  DBuf<double> ub((uint64_t)m * n, s);
+  if (with_qr) {
+    DBuf<double> urc((uint64_t)n * n, s), ubc((uint64_t)m * n, s);
+    rowmajor_to_colmajor<<<grid_for((uint64_t)n * n), 256, 0, s>>>(ur.get(), n, n, urc.get());
+    RK_LAUNCH_CHECK();
+    apply_q_device(qj, urc.get(), n, n, ubc.get(), s);
+    colmajor_to_rowmajor<<<grid_for((uint64_t)m * n), 256, 0, s>>>(ubc.get(), m, m, n, ub.get());
+    RK_LAUNCH_CHECK();
+  } else {
+    RK_CUDA_CHECK(cudaMemcpyAsync(ub.get(), ur.get(), sizeof(double) * (uint64_t)n * n, cudaMemcpyDeviceToDevice, s));
+  }
+  if (transposed) {  // U_A = V_B (n x n), V_A = U_B (m x n)
+    out.u = std::move(vr);
+    out.v = std::move(ub);
+    sign_rows(out.u.get(), n, n, out.v.get(), m, s);
+  } else {           // U_A = U_B (m x n), V_A = V_B
+    out.u = std::move(ub);
+    out.v = std::move(vr);
+    sign_rows(out.u.get(), m, n, out.v.get(), n, s);
+  }
+  sync(s);
+}
+
+}  // namespace rk

@@ -1,0 +1,62 @@
+// rk_pipeline.cuh -- orchestration interfaces shared by rk_pipeline.cu and rk_api.cu
+#pragma once
+
+#include "rk_internal.cuh"
+
+namespace rk {
+
+// optional per-block outputs for the block_svd API (U, sigma, deficient flags)
+struct BlockApiOut {
+  DBuf<double> u;          // per block: M x kept row-major at offset_u[i]
+  DBuf<double> sigma;      // per block: M entries (first kept valid)
+  DBuf<uint8_t> deficient; // per block: M flags
+};
+
+struct BlockStageResult {
+  DBuf<double> payload;               // records back to back (M x kept row-major each)
+  std::vector<uint64_t> offset;       // doubles into payload, per block
+  std::vector<uint32_t> kept;
+  std::vector<std::string> failures;  // per block, empty = ok (reference "block task d failed: ...")
+  double conv_residual = 0.0;
+  uint64_t sweeps_max = 0, rotations = 0;
+  float qr_ms = 0, jacobi_ms = 0;
+};
+
+void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t d_hi, uint64_t keep,
+                 BlockStageResult& out, BlockApiOut* api);
+
+struct MergeOut {
+  uint32_t k = 0;          // min(M, total kept)
+  DBuf<double> sigma;      // k, descending
+  DBuf<double> u;          // M x k row-major, sign convention applied
+  uint64_t sweeps = 0, rotations = 0;
+};
+
+// leaves of the merge tree: consecutive records, each leaf at least M rows of P^T
+struct TreeLeaf {
+  uint32_t r0, r1, height;
+};
+std::vector<TreeLeaf> merge_leaves(const std::vector<uint32_t>& kept, uint32_t M);
+
+// R factor (M x M column-major, upper) of the stacked leaves [leaf_lo, leaf_hi)
+void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
+                   const std::vector<uint32_t>& kept, uint32_t M, const std::vector<TreeLeaf>& leaves,
+                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out);
+// top of the tree over R factors (each M x M column-major), then Jacobi on R^T
+void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut& out);
+// the whole proxy SVD of the records (sigma, U of P)
+void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
+                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out);
+
+// dense_svd on the device: a is rows x cols row-major (device). Outputs row-major.
+struct DenseSvdOut {
+  uint32_t k = 0;
+  DBuf<double> u, sigma, v;  // u rows x k, v cols x k
+};
+void dense_svd_dev(Ctx& c, const double* a, uint32_t rows, uint32_t cols, DenseSvdOut& out);
+
+// small launch helpers
+void sign_rows(double* u, uint32_t rows, uint32_t k, double* v, uint32_t vrows, cudaStream_t s);
+void check_finite_or_throw(const double* x, uint64_t n, const char* what, cudaStream_t s);
+
+}  // namespace rk

@@ -1,0 +1,121 @@
+// rk_spmm.cu -- right-vector recovery V = A^T U Sigma^-1 (reference:
+// recover_right_vectors, proj/src/proxy.cpp:48-72).
+//
+// One warp per column c of A (= row c of V): the column's CSC entries are
+// visited in ascending row order -- the order in which the reference's
+// (row, col)-sorted entry loop accumulates into V(c, :) -- and every product
+// and sum uses round-to-nearest without contraction, then the row is scaled by
+// 1/sigma. Given identical U and sigma the result is bit-identical to the
+// reference. U's retained columns are gathered once into a compact M x r table
+// (L2-resident); V rows are written once, 16-byte vectorised, with streaming
+// stores: the kernel is bound by the 8*N*r-byte V write.
+#include "rk_internal.cuh"
+
+namespace rk {
+namespace {
+
+__global__ void gather_u(const double* u, uint32_t rows, uint32_t u_cols, const uint32_t* retained, uint32_t r,
+                         const double* sigma, double* u_ret, double* inv) {
+  const uint64_t total = (uint64_t)rows * r;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = t / r, jj = t % r;
+    u_ret[t] = u[i * u_cols + retained[jj]];
+    if (i == 0) inv[jj] = __ddiv_rn(1.0, sigma[retained[jj]]);
+  }
+}
+
+// r even: each lane owns column pairs (2*lane + 64*k, +1)
+template <bool kPairs>
+__global__ void __launch_bounds__(256) spmm_kernel(const uint64_t* __restrict__ col_ptr,
+                                                   const uint32_t* __restrict__ row_idx,
+                                                   const double* __restrict__ val, const double* __restrict__ u_ret,
+                                                   const double* __restrict__ inv, uint32_t r, uint64_t col_lo,
+                                                   uint64_t col_hi, double* __restrict__ v) {
+  constexpr int kMax = 16;  // up to 32 * kMax (pairs: 64 * kMax/2 ... ) columns in registers per pass
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = col_lo + warp0; c < col_hi; c += nwarps) {
+    const uint64_t e0 = col_ptr[c], e1 = col_ptr[c + 1];
+    double* vrow = v + (c - col_lo) * r;
+    if (kPairs) {
+      for (uint32_t base = 0; base < r; base += 64 * (kMax / 2)) {
+        double2 acc[kMax / 2];
+#pragma unroll
+        for (int k = 0; k < kMax / 2; ++k) acc[k] = make_double2(0.0, 0.0);
+        for (uint64_t e = e0; e < e1; ++e) {
+          const double x = val[e];
+          const double2* ur = reinterpret_cast<const double2*>(u_ret + (uint64_t)row_idx[e] * r);
+#pragma unroll
+          for (int k = 0; k < kMax / 2; ++k) {
+            const uint32_t j = base + 64 * k + 2 * lane;
+            if (j < r) {
+              const double2 uu = ur[j / 2];
+              acc[k].x = __dadd_rn(acc[k].x, __dmul_rn(x, uu.x));
+              acc[k].y = __dadd_rn(acc[k].y, __dmul_rn(x, uu.y));
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kMax / 2; ++k) {
+          const uint32_t j = base + 64 * k + 2 * lane;
+          if (j < r) {
+            double2 o;
+            o.x = __dmul_rn(acc[k].x, inv[j]);
+            o.y = __dmul_rn(acc[k].y, inv[j + 1]);
+            __stcs(reinterpret_cast<double2*>(vrow + j), o);
+          }
+        }
+      }
+    } else {
+      for (uint32_t base = 0; base < r; base += 32 * kMax) {
+        double acc[kMax];
+#pragma unroll
+        for (int k = 0; k < kMax; ++k) acc[k] = 0.0;
+        for (uint64_t e = e0; e < e1; ++e) {
+          const double x = val[e];
+          const double* ur = u_ret + (uint64_t)row_idx[e] * r;
+#pragma unroll
+          for (int k = 0; k < kMax; ++k) {
+            const uint32_t j = base + 32 * k + lane;
+            if (j < r) acc[k] = __dadd_rn(acc[k], __dmul_rn(x, ur[j]));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kMax; ++k) {
+          const uint32_t j = base + 32 * k + lane;
+          if (j < r) __stcs(vrow + j, __dmul_rn(acc[k], inv[j]));
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const uint32_t* retained,
+                      const double* sigma, uint32_t r, double* v, uint64_t col_lo, uint64_t col_hi,
+                      cudaStream_t s) {
+  if (r == 0 || col_hi <= col_lo) return;
+  DBuf<double> u_ret((uint64_t)a.rows * r, s), inv(r, s);
+  const uint64_t tot = (uint64_t)a.rows * r;
+  unsigned g1 = (unsigned)std::min<uint64_t>(ceil_div(tot ? tot : 1, 256), 65535);
+  gather_u<<<g1, 256, 0, s>>>(u, (uint32_t)a.rows, u_cols, retained, r, sigma, u_ret.get(), inv.get());
+  RK_LAUNCH_CHECK();
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t cols = col_hi - col_lo;
+  unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(cols * 32, 256), (uint64_t)sms * 16);
+  if (grid == 0) grid = 1;
+  if ((r & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0)
+    spmm_kernel<true><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
+                                           col_hi, v);
+  else
+    spmm_kernel<false><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
+                                            col_hi, v);
+  RK_LAUNCH_CHECK();
+}
+
+}  // namespace rk
