@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the full Ranky SVD hot path (repair -> block SVDs -> UΣ merge -> V).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one full pass of the hot path over the BASELINE workload (configs[1],
+c2: M=256, N=262144, 64 blocks, RandomChecker, full Σ, U, V) with the input
+matrix already resident in HBM. For N>1 (torchrun, one process per GPU) the
+blocks are sharded by merge-tree leaves, each rank factors its leaves, the
+subtree R factors are all-gathered over NCCL and every rank finishes the same
+tree top and recovers V for its own columns; time is the max over ranks.
+
+`e2e` is the same metric through the reference-facing C-ABI call
+(rk_run_pipeline with RK_WANT_V) on host buffers: entries H2D and sigma/U/V
+D2H inside the timed region. `--impl reference` times the reference's own CPU
+implementation (oracle/_ref: run_pipeline + recover_right_vectors, all host
+threads) on the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full Ranky SVD nnz/s"
+UNIT = "nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_dict(cfg, n_gpus, extra=None):
+    d = {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols, "blocks": cfg.blocks, "method": cfg.method,
+         "keep": cfg.keep, "top_k": cfg.top_k, "seed": cfg.seed, "description": cfg.description,
+         "parallelism": f"block-shard x{n_gpus}" if n_gpus > 1 else "single GPU",
+         "l2": "flushed between steps (256 MiB write)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rk_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- peaks
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak_tflops(torch):
+    """FP64 peak is not in MEASURED_PEAKS.json: measured here as a cuBLAS DGEMM
+    burst (torch.matmul float64, 8192^3, best of 5)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def reference_arm(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    a = cfg.generate()
+    r, c, v = a.coo()
+    coo = (a.rows(), a.cols(), r, c, v)
+    cores = os.cpu_count() or 1
+    run = (lambda: orc.full_svd(coo, cfg.blocks, cfg.method, cfg.keep, cfg.seed, cores, cfg.top_k)) \
+        if kind == "reference" else (lambda: orc.run_pipeline(coo, cfg.blocks, cfg.method, cfg.keep, cfg.seed))
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = a.nnz() / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": config_dict(cfg, 1, {"nnz": a.nnz()}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"full {cfg.name} per step (run_pipeline workers={cores} + "
+                                       f"recover_right_vectors), {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, a):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    r, c, v = a.coo()
+    coo = (a.rows(), a.cols(), r, c, v)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if kind == "reference":
+        orc.full_svd(coo, cfg.blocks, cfg.method, cfg.keep, cfg.seed, cores, cfg.top_k)
+    else:
+        orc.run_pipeline(coo, cfg.blocks, cfg.method, cfg.keep, cfg.seed)
+        cores = 1
+    dt = time.perf_counter() - t0
+    return {"value": a.nnz() / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"one full {cfg.name} run (run_pipeline workers={cores} + recover_right_vectors), {dt:.2f} s"}
+
+
+# --------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    from paper_2009_09767_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import paper_2009_09767_b200 as rk
+    from paper_2009_09767_b200 import ranky as R
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = rk.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    a = cfg.generate()
+    dm = rk.DeviceMatrix(a, ctx)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    L = R.lib()
+    M = cfg.rows
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    if ws == 1:
+        def step():
+            out, t = R.dev_full_svd(dm, cfg.blocks, cfg.method, cfg.keep, cfg.seed, True, cfg.top_k)
+            R.dev_outputs_free(out)
+            return t
+    else:
+        leaves = int(L.rk_merge_tree_leaves(M, cfg.cols, cfg.blocks, cfg.keep))
+        per = leaves // ws
+        lo, hi = rank * per, (rank + 1) * per if rank + 1 < ws else leaves
+        width = cfg.cols // cfg.blocks
+        roots = torch.empty((ws, M, M), dtype=torch.float64, device="cuda")
+        mine = torch.empty((M, M), dtype=torch.float64, device="cuda")
+
+        def step():
+            shard = C.c_void_p()
+            t = R.Timing()
+            R._check(L.rk_dev_shard_factor(ctx.handle, dm.handle, cfg.blocks, R._method(cfg.method), cfg.keep,
+                                           cfg.seed, lo, hi, C.c_void_p(mine.data_ptr()), C.byref(shard),
+                                           C.byref(t)))
+            torch.distributed.all_gather_into_tensor(roots, mine)
+            # columns owned by this rank: its leaves' blocks (uniform kept -> blocks per leaf)
+            bpl = cfg.blocks // leaves
+            c_lo, c_hi = lo * bpl * width, (hi * bpl * width if rank + 1 < ws else cfg.cols)
+            out = C.POINTER(R.DevOutputs)()
+            t2 = R.Timing()
+            R._check(L.rk_dev_shard_finish(ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V,
+                                           cfg.top_k, c_lo, c_hi, C.byref(out), C.byref(t2)))
+            R.dev_outputs_free(out)
+            L.rk_dev_shard_destroy(shard)
+            t.merge_ms += t2.merge_ms
+            t.recover_ms = t2.recover_ms
+            t.kernel_launches += t2.kernel_launches
+            return t
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_steps, launches, timings = [], 0, []
+    barrier()
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t = step()
+        e1.record(stream)
+        flush.zero_()  # outside the step's events
+        torch.cuda.synchronize()
+        ms_steps.append(e0.elapsed_time(e1))
+        launches += int(t.kernel_launches)
+        timings.append(t.as_dict())
+    barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    ms = sum(ms_steps) / len(ms_steps)
+    if ws > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = a.nnz() / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (by device time) --------------------------
+    med = {k: statistics.median([t[k] for t in timings]) for k in timings[0]}
+    peaks, peak_src = measured_peaks()
+    fp64 = fp64_peak_tflops(torch) if rank == 0 else 0.0
+    cand = {"block_jacobi": (med["jacobi_ms"], med["jacobi_flops"]), "block_qr": (med["qr_ms"], med["qr_flops"])}
+    dom = max(cand, key=lambda k: cand[k][0])
+    d_ms, d_flops = cand[dom]
+    achieved = d_flops / (d_ms * 1e-3) / 1e12 if d_ms > 0 else 0.0
+    roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64 if fp64 else None, "traffic": None,
+                "peak_source": "measured in bench.py: cuBLAS DGEMM burst (torch.matmul f64 8192^3, best of 5); "
+                               "FP64 is not in MEASURED_PEAKS.json",
+                "flops_per_launch": d_flops, "ms_per_launch": d_ms,
+                "flops_model": "QR: sum_d 2 n_d M^2 - 2/3 M^3; Jacobi: per block sweeps*(c(c-1)/2*2M + 2Mc) "
+                               "+ rotations*6M"}
+    stages = {k: med[k] for k in ("repair_ms", "blocks_ms", "qr_ms", "jacobi_ms", "merge_ms", "recover_ms",
+                                  "total_ms")}
+    stages["jacobi_sweeps_max"] = med["jacobi_sweeps_max"]
+    v_bytes = 8.0 * cfg.cols * M
+    stages["recover_hbm_frac"] = (v_bytes / (med["recover_ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"] \
+        if med["recover_ms"] > 0 else None
+
+    # ---- e2e through the C ABI with host buffers -----------------------------------
+    e2e = None
+    if not args.no_e2e and ws == 1:
+        pinned = torch.empty(a.nnz() * R.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+        host_e = pinned.numpy().view(R.ENTRY_DTYPE)
+        host_e[:] = a.entries()
+        ha = R.SparseMatrix._trusted(a.rows(), a.cols(), host_e)
+        for _ in range(max(1, args.warmup)):
+            rk.run_pipeline(ha, cfg.blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True, top_k=cfg.top_k,
+                            want_repaired=False, want_records=False, ctx=ctx)
+        e2e_ms = []
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = rk.run_pipeline(ha, cfg.blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True, top_k=cfg.top_k,
+                                  want_repaired=False, want_records=False, ctx=ctx)
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            h2d = a.nnz() * R.ENTRY_DTYPE.itemsize
+            d2h = 8 * (res.svd.u.size + res.svd.sigma.size + res.svd.v.size) + \
+                28 * len(res.report.added_edges) + 8 * cfg.blocks
+        e_ms = sum(e2e_ms) / len(e2e_ms)
+        e2e = {"value": a.nnz() / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "path": "rk_run_pipeline(host entries, RK_WANT_V) via ctypes"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, a)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, csrc/gen.c)",
+                "config": config_dict(cfg, ws, {"nnz": a.nnz()}), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages_ms_median": stages,
+                "wall_s_timed_region": wall, "peaks_source": peak_src}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -114,6 +114,10 @@ typedef struct rk_timing {
   uint64_t jacobi_sweeps_max;    /* over all block factorizations */
   uint64_t jacobi_rotations;     /* over all block factorizations */
   uint64_t kernel_launches;      /* kernels this library launched in the call */
+  uint64_t jacobi_sweeps_sum;    /* sweeps summed over the block factorizations */
+  double qr_flops;               /* algorithmic FP64 flops of the block QRs: sum 2 n_d M^2 - 2/3 M^3 */
+  double jacobi_flops;           /* algorithmic FP64 flops of the block Jacobi: per block
+                                    sweeps*(c(c-1)/2*2M + 2Mc) + rotations*6M, c = active columns */
 } rk_timing;
 
 /* PipelineResult (+ V) -- proj/include/ranky/pipeline.hpp:30-36 */

@@ -3,11 +3,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <unordered_set>
 
 #include "rk_pipeline.cuh"
 
 namespace rk {
 thread_local uint64_t* g_launch_counter = nullptr;
+void* host_alloc_bytes(size_t bytes);
 
 CallScope::CallScope(Ctx* c) {
   cudaGetDevice(&prev_device);
@@ -69,11 +72,40 @@ rk_status guarded(F&& body) {
   }
 }
 
+// Output buffers above 1 MiB are page-locked so device->host copies of V run at
+// full PCIe rate; the registry lets rk_*_free release either kind.
+std::mutex g_pinned_mu;
+std::unordered_set<void*> g_pinned;
+
 template <class T>
 T* host_alloc(size_t n) {
-  T* p = static_cast<T*>(std::malloc((n ? n : 1) * sizeof(T)));
+  const size_t bytes = (n ? n : 1) * sizeof(T);
+  if (bytes >= (1u << 20)) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_pinned_mu);
+      g_pinned.insert(p);
+      return static_cast<T*>(p);
+    }
+    cudaGetLastError();
+  }
+  T* p = static_cast<T*>(std::malloc(bytes));
   if (!p) fail(RK_NOMEM, "host allocation failed");
   return p;
+}
+
+void host_free(void* p) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    auto it = g_pinned.find(p);
+    if (it != g_pinned.end()) {
+      g_pinned.erase(it);
+      cudaFreeHost(p);
+      return;
+    }
+  }
+  std::free(p);
 }
 
 template <class T>
@@ -210,10 +242,15 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
     t->jacobi_sweeps_max = fr.blocks.sweeps_max;
     t->jacobi_rotations = fr.blocks.rotations;
     t->kernel_launches = c.launches - launches0;
+    t->jacobi_sweeps_sum = fr.blocks.sweeps_sum;
+    t->qr_flops = fr.blocks.qr_flops;
+    t->jacobi_flops = fr.blocks.jacobi_flops;
   }
 }
 
 }  // namespace
+
+void* rk::host_alloc_bytes(size_t bytes) { return host_alloc<char>(bytes); }
 
 extern "C" {
 
@@ -243,6 +280,12 @@ rk_status rk_ctx_create(int32_t device, rk_ctx** out) {
       fail(RK_CUDA, std::string("libranky_b200 is built for sm_100a; device is ") + prop.name);
     c.num_sms = prop.multiProcessorCount;
     c.smem_optin = prop.sharedMemPerBlockOptin;
+    // keep freed blocks in the stream-ordered pool: repeated pipeline calls reuse
+    // their buffers instead of paying cudaMalloc/cudaFree every step
+    cudaMemPool_t pool;
+    RK_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    RK_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     RK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.own, cudaStreamNonBlocking));
     c.stream = c.own;
     for (auto& ev : c.ev) RK_CUDA_CHECK(cudaEventCreate(&ev));
@@ -280,22 +323,22 @@ uint64_t rk_ctx_kernel_launches(const rk_ctx* ctx) { return ctx ? ctx->c.launche
 
 void rk_svd_free(rk_svd* s) {
   if (!s) return;
-  std::free(s->u); std::free(s->sigma); std::free(s->v);
+  host_free(s->u); host_free(s->sigma); host_free(s->v);
   std::memset(s, 0, sizeof *s);
 }
 void rk_repair_report_free(rk_repair_report* r) {
   if (!r) return;
-  std::free(r->block); std::free(r->row); std::free(r->col); std::free(r->mechanism); std::free(r->lonely_counts);
+  host_free(r->block); host_free(r->row); host_free(r->col); host_free(r->mechanism); host_free(r->lonely_counts);
   std::memset(r, 0, sizeof *r);
 }
 void rk_sparse_free(rk_sparse* s) {
   if (!s) return;
-  std::free(s->entries);
+  host_free(s->entries);
   std::memset(s, 0, sizeof *s);
 }
 void rk_records_free(rk_records* r) {
   if (!r) return;
-  std::free(r->kept); std::free(r->offset); std::free(r->payload);
+  host_free(r->kept); host_free(r->offset); host_free(r->payload);
   std::memset(r, 0, sizeof *r);
 }
 void rk_pipeline_result_free(rk_pipeline_result* r) {
@@ -492,7 +535,7 @@ rk_status rk_recover_right_vectors(rk_ctx* ctx, const rk_sparse_view* a, uint64_
     out->u = host_alloc<double>(0);
     out->sigma = host_alloc<double>(0);
     if (r == 0 || a->cols == 0) {
-      out->v = static_cast<double*>(std::calloc(a->cols * r ? a->cols * r : 1, sizeof(double)));
+      out->v = host_alloc<double>(a->cols * r);
       return;
     }
     DevMatrix m;
@@ -706,6 +749,9 @@ rk_status rk_dev_shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t bloc
       timing->jacobi_sweeps_max = br.sweeps_max;
       timing->jacobi_rotations = br.rotations;
       timing->kernel_launches = c.launches - launches0;
+      timing->jacobi_sweeps_sum = br.sweeps_sum;
+      timing->qr_flops = br.qr_flops;
+      timing->jacobi_flops = br.jacobi_flops;
     }
     *shard_out = sh.release();
   });

@@ -692,17 +692,19 @@ size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v) {
 
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin) {
   if (jobs.empty()) return;
-  // jobs in one launch share rows / cols / with_v (the caller groups them)
-  const uint32_t rows = jobs[0].rows, cols = jobs[0].cols;
+  // jobs in one launch share rows / cols_pad / with_v (the caller groups them);
+  // the group layout is a function of (rows, cols_pad) only
+  const uint32_t rows = jobs[0].rows, cols_pad = jobs[0].cols_pad;
   const bool with_v = jobs[0].v != nullptr;
   uint32_t g, G;
   const size_t budget = std::min<size_t>(smem_optin, 200 * 1024);
-  jacobi_plan(rows, cols, with_v, budget, g, G);
+  jacobi_plan(rows, cols_pad, with_v, budget, g, G);
   for (JacobiJob& j : jobs) {
-    if (j.rows != rows || j.cols != cols || (j.v != nullptr) != with_v)
+    if (j.rows != rows || j.cols_pad != cols_pad || (j.v != nullptr) != with_v)
       fail(RK_RUNTIME, "jacobi_batched: heterogeneous batch");
-    if (j.cols_pad != g * G) fail(RK_RUNTIME, "jacobi_batched: cols_pad mismatch");
+    if (j.cols > cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols > cols_pad");
   }
+  if (g * G != cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols_pad is not a planned width");
   const size_t smem = jacobi_smem(rows, g, g * G, with_v);
   RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -719,9 +721,14 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
 }
 
 uint32_t jacobi_cols_pad(uint32_t rows, uint32_t cols, bool with_v, size_t smem_optin) {
-  uint32_t g, G;
-  jacobi_plan(rows, cols, with_v, std::min<size_t>(smem_optin, 200 * 1024), g, G);
-  return g * G;
+  // a width that re-plans to itself, so jacobi_batched can recover (g, G) from it
+  uint32_t g, G, cp = cols;
+  for (int it = 0; it < 16; ++it) {
+    jacobi_plan(rows, cp, with_v, std::min<size_t>(smem_optin, 200 * 1024), g, G);
+    if (g * G == cp) return cp;
+    cp = g * G;
+  }
+  fail(RK_RUNTIME, "jacobi_cols_pad: no stable padded width");
 }
 
 void finalize_batched(const std::vector<FinalJob>& jobs, cudaStream_t s) {

@@ -295,8 +295,7 @@ void csr_to_entries_host(const DevCsr& a, rk_sparse& out, cudaStream_t s) {
   out.rows = a.rows;
   out.cols = a.cols;
   out.nnz = a.nnz;
-  out.entries = static_cast<rk_entry*>(std::malloc((a.nnz ? a.nnz : 1) * sizeof(rk_entry)));
-  if (!out.entries) fail(RK_NOMEM, "host allocation failed");
+  out.entries = static_cast<rk_entry*>(host_alloc_bytes((a.nnz ? a.nnz : 1) * sizeof(rk_entry)));
   if (!a.nnz) return;
   DBuf<rk_entry> tmp(a.nnz, s);
   csr_to_entry_array<<<blocks_for(a.rows * 32), kT, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), a.rows,

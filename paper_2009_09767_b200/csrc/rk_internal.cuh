@@ -206,6 +206,9 @@ struct CallScope {
 // ---------------------------------------------------------------------------
 // kernels & launchers (one .cu per group)
 
+// rk_api.cu -- library-owned host output buffers (pinned above 1 MiB)
+void* host_alloc_bytes(size_t bytes);
+
 // rk_scan.cu -- exclusive prefix sums (deterministic)
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);  // out has n+1
 void exclusive_scan_u32to64(const uint32_t* in, uint64_t* out, uint64_t n, cudaStream_t s);

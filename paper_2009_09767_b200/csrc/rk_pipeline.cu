@@ -296,7 +296,9 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     }
     if (plans.empty()) { i0 = i1; continue; }
     const size_t nb = plans.size();
-    const uint32_t cols_pad = jacobi_cols_pad(M, max_cols, false, c.smem_optin);
+    // one padded width per M (not per chunk): the Jacobi group layout, and with it
+    // the rotation order and rounding, depends only on the block's own data
+    const uint32_t cols_pad = cols_pad_full;
     DBuf<double> st(staging ? staging : 1, s);
     DBuf<double> W((uint64_t)nb * M * cols_pad, s);
     DBuf<double> qr_aux((uint64_t)nb * aux_sz, s);
@@ -348,7 +350,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       jj[q].w = W.get() + (uint64_t)q * M * cols_pad;
       jj[q].v = nullptr;
       jj[q].rows = M;
-      jj[q].cols = max_cols;
+      jj[q].cols = std::max<uint32_t>(std::min<uint32_t>(plans[q].n_rows, M), 1);
       jj[q].cols_pad = cols_pad;
       jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad;
       jj[q].stats = stats.get() + 8 * q;
@@ -382,7 +384,13 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     out.jacobi_ms += ms_j;
     for (size_t q = 0; q < nb; ++q) {
       out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
+      out.sweeps_sum += js[q].sweeps;
       out.rotations += js[q].rotations;
+      const double cA = std::min<uint32_t>(plans[q].n_rows, M), Md = M;
+      out.jacobi_flops += (double)js[q].sweeps * (cA * (cA - 1) / 2 * 2 * Md + 2 * Md * cA) +
+                          (double)js[q].rotations * 6 * Md;
+      if (plans[q].tall)
+        out.qr_flops += 2.0 * plans[q].n_rows * Md * Md - 2.0 / 3.0 * Md * Md * Md;
       if (js[q].failed) {
         const uint64_t i = plans[q].block - d_lo;
         out.failures[i] = "one-sided Jacobi did not converge (residual " + residual_text(js[q].residual) + ")";

@@ -18,7 +18,8 @@ struct BlockStageResult {
   std::vector<uint32_t> kept;
   std::vector<std::string> failures;  // per block, empty = ok (reference "block task d failed: ...")
   double conv_residual = 0.0;
-  uint64_t sweeps_max = 0, rotations = 0;
+  uint64_t sweeps_max = 0, rotations = 0, sweeps_sum = 0;
+  double qr_flops = 0, jacobi_flops = 0;
   float qr_ms = 0, jacobi_ms = 0;
 };
 

@@ -1,0 +1,159 @@
+"""GPU run_pipeline (+ V) against the reference: the acceptance criteria
+(proj/tests/acceptance_main.cpp) and the BASELINE configs c1/c2 end to end."""
+import numpy as np
+import pytest
+
+import paper_2009_09767_b200 as rk
+from paper_2009_09767_b200 import configs
+from test_gpu_svd import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def sigma_error(a, b):
+    """metrics.cpp:32-42"""
+    n = max(len(a), len(b))
+    a = np.pad(np.asarray(a, float), (0, n - len(a)))
+    b = np.pad(np.asarray(b, float), (0, n - len(b)))
+    return float(np.abs(a - b).sum())
+
+
+def test_proxy_equivalence():
+    # acceptance 1: dense 16x256, D in {2,4,8}, method none
+    rng = np.random.default_rng(0)
+    for seed in range(20):
+        dense = rng.uniform(-1, 1, (16, 256))
+        a = rk.sparse_of(dense)
+        o = rk.dense_svd(dense)
+        for d in (2, 4, 8):
+            res = rk.run_pipeline(a, d, "none", 0, seed, 1)
+            rel = np.abs(res.svd.sigma - o.sigma) / o.sigma
+            assert rel.max() <= 1e-10
+            assert abs(float(res.svd.u[:, 0] @ o.u[:, 0])) >= 1 - 1e-8
+
+
+def repair_demo_instance():
+    # acceptance_main.cpp:85-99 structure (8x64, row 7 lonely in block 0)
+    rng = np.random.default_rng(123)
+    e = []
+    for r in range(7):
+        for c in range(64):
+            if rng.uniform() < 0.6:
+                e.append((r, c, 1.0 + rng.uniform()))
+    e += [(7, 40, 1.5), (7, 50, 2.0), (7, 63, 1.25)]
+    return rk.SparseMatrix(8, 64, e)
+
+
+def test_repair_necessity():
+    # acceptance 2
+    a = repair_demo_instance()
+    none = rk.run_pipeline(a, 2, "none", 0, 0, 1)
+    for m in ("random", "neighbor", "neighbor-random"):
+        for seed in range(3):
+            res = rk.run_pipeline(a, 2, m, 0, seed, 1)
+            assert res.report.added_edges
+            o = rk.dense_svd(res.repaired.to_dense())
+            assert sigma_error(res.svd.sigma, o.sigma) <= 1e-9
+            assert sigma_error(none.svd.sigma, o.sigma) > 1e-3
+
+
+def test_table_regime(ref):
+    # acceptance 3 (seeds 0-3 of 0-9), against the reference pipeline
+    for seed in range(4):
+        a = configs.synth_bipartite(64, 8192, 0.002, seed)
+        r, c, v = a.coo()
+        for d in (2, 8, 32):
+            for m in ("random", "neighbor", "neighbor-random"):
+                res = rk.run_pipeline(a, d, m, 0, seed, 1)
+                o = ref.run_pipeline((64, 8192, r, c, v), d, m, 0, seed)
+                assert np.array_equal(res.report.edges_array(), o.edges)
+                assert sigma_error(res.svd.sigma, o.sigma) <= 1e-9
+                compare(res.svd, o.sigma, o.u, f"seed {seed} D {d} {m}")
+
+
+def test_determinism_and_workers():
+    # acceptance 6: bitwise identical for any workers value and repeated runs
+    for config in range(8):
+        rows, cols = 4 + (config % 5) * 3, 32 + (config % 4) * 24
+        a = configs.synth_bipartite(rows, cols, 0.04 + 0.03 * (config % 3), config)
+        method = ["random", "neighbor", "neighbor-random", "none"][config % 4]
+        keep = 3 if config % 6 == 5 else 0
+        blocks = 1 + config % 8
+        base = rk.run_pipeline(a, blocks, method, keep, config, 1)
+        for workers in (4, 8):
+            res = rk.run_pipeline(a, blocks, method, keep, config, workers)
+            assert np.array_equal(res.svd.sigma, base.svd.sigma) and np.array_equal(res.svd.u, base.svd.u)
+            assert all(x == y for x, y in zip(res.records, base.records))
+            assert res.report.to_log() == base.report.to_log() and res.repaired == base.repaired
+
+
+def test_single_block_equals_dense():
+    # harness_test.cpp:146-156
+    rng = np.random.default_rng(123)
+    dense = rng.uniform(-1, 1, (5, 9))
+    res = rk.run_pipeline(rk.sparse_of(dense), 1, "none", 0, 0, 1)
+    o = rk.dense_svd(dense)
+    assert np.max(np.abs(res.svd.sigma - o.sigma)) <= 1e-12 * o.sigma[0]
+
+
+def test_pipeline_errors():
+    # harness_test.cpp:174-194
+    a = configs.synth_bipartite(4, 16, 0.5, 0)
+    with pytest.raises(rk.InvalidArgument):
+        rk.run_pipeline(a, 0, "none", 0, 0, 1)
+    with pytest.raises(rk.InvalidArgument):
+        rk.run_pipeline(a, 17, "none", 0, 0, 1)
+    with pytest.raises(rk.InvalidArgument):
+        rk.run_pipeline(a, 2, "none", 0, 0, 0)
+    bad = rk.SparseMatrix(2, 8, [(0, 0, 1.0), (0, 5, np.inf), (1, 2, 1.0), (1, 7, 1.0)])
+    with pytest.raises(rk.RankyRuntimeError, match="block task 1"):
+        rk.run_pipeline(bad, 2, "none", 0, 0, 1)
+
+
+def test_pipeline_records_shape():
+    # harness_test.cpp:196-208
+    a = configs.synth_bipartite(8, 64, 0.03, 10)
+    res = rk.run_pipeline(a, 8, "neighbor", 0, 2, 2)
+    for d in range(8):
+        assert rk.find_lonely_rows(res.repaired, res.partition, d) == []
+        assert res.records[d].block_index == d and res.records[d].rows == 8 and res.records[d].kept == 8
+
+
+def test_reference_fixture_pipelines(golden, garrays):
+    for name, p in golden["pipelines"].items():
+        shape = garrays[f"pipe_{name}_shape"]
+        a = rk.SparseMatrix._trusted(int(shape[0]), int(shape[1]), rk.ranky._entries(
+            garrays[f"pipe_{name}_r"], garrays[f"pipe_{name}_c"], garrays[f"pipe_{name}_v"]))
+        res = rk.run_pipeline(a, p["D"], p["method"], p["keep"], p["seed"], 1, want_v=True)
+        assert np.array_equal(res.report.edges_array(), garrays[f"pipe_{name}_edges"])
+        compare(res.svd, garrays[f"pipe_{name}_sigma"], garrays[f"pipe_{name}_u"], name)
+        for d in range(p["records"]):
+            # a record is U*Sigma of one block: its column norms are the block's
+            # singular values and P P^T = A_d A_d^T is independent of the basis
+            # chosen inside degenerate clusters (value-1.0 blocks have many)
+            want = garrays[f"pipe_{name}_rec{d}"]
+            got = res.records[d].payload.reshape(want.shape)
+            scale = max(1.0, float(np.abs(want).max())) ** 2
+            assert np.allclose(np.linalg.norm(got, axis=0), np.linalg.norm(want, axis=0), rtol=1e-10,
+                               atol=1e-12 * scale), (name, d)
+            assert np.max(np.abs(got @ got.T - want @ want.T)) <= 1e-12 * scale * want.shape[0], (name, d)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_baseline_config_end_to_end(name, ref):
+    cfg = configs.CONFIGS[name]
+    a = cfg.generate()
+    r, c, v = a.coo()
+    res = rk.run_pipeline(a, cfg.blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True, top_k=cfg.top_k)
+    o = ref.full_svd((a.rows(), a.cols(), r, c, v), cfg.blocks, cfg.method, cfg.keep, cfg.seed, 8, cfg.top_k) \
+        if ref.kind == "reference" else None
+    if o is None:
+        o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), cfg.blocks, cfg.method, cfg.keep, cfg.seed)
+        o.v = ref.recover_right_vectors(o.matrix, o.u, o.sigma, 1e-10)
+    compare(res.svd, o.sigma, o.u, name)
+    # V columns: same direction as the reference's (cosine), reconstruction residual
+    cos = np.sum(res.svd.v * o.v, axis=0) / (np.linalg.norm(res.svd.v, axis=0) * np.linalg.norm(o.v, axis=0))
+    assert np.all(np.abs(cos) >= 1 - 1e-8)
+    # bit-exact V given identical U, sigma and repaired matrix
+    vr = ref.recover_right_vectors((a.rows(), a.cols(), *res.repaired.coo()), res.svd.u, res.svd.sigma, 1e-10)
+    assert np.array_equal(res.svd.v, vr)
