@@ -1,11 +1,6 @@
 // rk_dense.cu -- batched dense FP64 factorizations on sm_100a.
 //
-//  qr_cluster_kernel   blocked Householder QR (reference: householder_qr,
-//                      proj/src/svd.cpp:77-107) of a tall column-major matrix,
-//                      one thread-block cluster per matrix. Compact-WY panels of
-//                      NB reflectors (LAPACK dlarft form); rank 0 factors each
-//                      panel, every CTA of the cluster updates its share of the
-//                      trailing column tiles; cluster barriers separate phases.
+//  (the blocked Householder QR lives in rk_qr.cu)
 //  jacobi_cluster_kernel
 //                      one-sided (Hestenes) Jacobi (reference: jacobi_svd,
 //                      proj/src/svd.cpp:214-306) with the same rotation formulas,
@@ -25,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "rk_internal.cuh"
 
@@ -41,193 +37,6 @@ __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
-}
-
-// ===========================================================================
-// QR
-// ===========================================================================
-
-constexpr int kQrThreads = 256;
-constexpr int kQrWarps = kQrThreads / 32;
-constexpr int NB = 16;      // reflectors per panel
-constexpr int kTileCols = 4;
-
-struct QrArgs {
-  const QrJob* jobs;
-};
-
-// CTA-wide sum of up to NB values held per thread; result broadcast via smem
-__device__ __forceinline__ void block_sum_vec(double* vals, int n, double* s_part, double* s_out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    if (q < n) {
-      double x = warp_sum(vals[q]);
-      if (lane == 0) s_part[warp * NB + q] = x;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < n) {
-    double t = 0.0;
-    for (int w = 0; w < kQrWarps; ++w) t += s_part[w * NB + threadIdx.x];
-    s_out[threadIdx.x] = t;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kQrThreads) qr_cluster_kernel(QrArgs args) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
-  const QrJob job = args.jobs[blockIdx.x / csize];
-  double* __restrict__ A = job.a;
-  const uint64_t lda = job.lda;
-  const int m = (int)job.m, n = (int)job.n;
-  const int K = m < n ? m : n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  __shared__ double s_part[kQrWarps * NB];
-  __shared__ double s_red[NB];
-  __shared__ double s_T[NB * NB];  // T(r, c) at [r * NB + c], upper triangular
-  __shared__ double s_beta;
-
-  for (int k0 = 0; k0 < K; k0 += NB) {
-    const int nbk = min(NB, K - k0);
-    double* tglob = job.tmat + (uint64_t)(k0 / NB) * NB * NB;
-    if (rank == 0) {
-      // ---- panel factorization (unblocked, columns k0 .. k0+nbk-1) ----
-      for (int t = tid; t < NB * NB; t += kQrThreads) s_T[t] = 0.0;
-      for (int jj = 0; jj < nbk; ++jj) {
-        const int kk = k0 + jj;
-        double* ak = A + (uint64_t)kk * lda;
-        double part[NB];
-        part[0] = 0.0;
-        for (int i = kk + tid; i < m; i += kQrThreads) {
-          double x = __ldcg(ak + i);
-          part[0] += x * x;
-        }
-        block_sum_vec(part, 1, s_part, s_red);
-        if (tid == 0) {
-          const double norm2 = s_red[0];
-          double beta = 0.0, alpha = 0.0;
-          if (norm2 > 0.0) {
-            const double norm = sqrt(norm2);
-            const double x0 = __ldcg(ak + kk);
-            alpha = x0 >= 0.0 ? -norm : norm;
-            const double v0 = x0 - alpha;
-            const double vsq = 2.0 * norm * (norm + fabs(x0));  // = ||x - alpha e1||^2
-            beta = 2.0 / vsq;
-            ak[kk] = v0;  // v stored in place, v0 on the diagonal
-          }
-          job.diag[kk] = alpha;  // R(kk, kk); 0 for a zero column
-          job.beta[kk] = beta;
-          s_beta = beta;
-        }
-        __syncthreads();
-        const double beta = s_beta;
-        if (beta != 0.0) {
-          // one reduction: dots with the remaining panel columns (kk+1 ..) and
-          // with the earlier reflectors of this panel (for T)
-          const int n_after = nbk - 1 - jj;
-          const int n_vals = n_after + jj;
-          double acc[NB];
-#pragma unroll
-          for (int q = 0; q < NB; ++q) acc[q] = 0.0;
-          for (int i = kk + tid; i < m; i += kQrThreads) {
-            const double vi = __ldcg(ak + i);
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-              if (q < n_after) acc[q] += vi * __ldcg(A + (uint64_t)(kk + 1 + q) * lda + i);
-              else if (q < n_vals) acc[q] += vi * __ldcg(A + (uint64_t)(k0 + q - n_after) * lda + i);
-            }
-          }
-          block_sum_vec(acc, n_vals, s_part, s_red);
-          // apply H to the remaining panel columns
-          for (int i = kk + tid; i < m; i += kQrThreads) {
-            const double vi = __ldcg(ak + i);
-            for (int q = 0; q < n_after; ++q) {
-              double* aj = A + (uint64_t)(kk + 1 + q) * lda;
-              aj[i] = __ldcg(aj + i) - beta * s_red[q] * vi;
-            }
-          }
-          // T(0:jj, jj) = -beta T(0:jj,0:jj) z,  T(jj,jj) = beta  (dlarft, forward columnwise)
-          if (tid < jj) {
-            double t = 0.0;
-            for (int s = tid; s < jj; ++s) t += s_T[tid * NB + s] * s_red[n_after + s];
-            s_part[tid] = -beta * t;  // reuse scratch (after the reduction consumed it)
-          }
-          __syncthreads();
-          if (tid < jj) s_T[tid * NB + jj] = s_part[tid];
-          if (tid == 0) s_T[jj * NB + jj] = beta;
-          __syncthreads();
-        } else {
-          // identity reflector: v = 0 (the column below the diagonal is zero)
-          if (tid == 0) ak[kk] = 0.0;
-          __syncthreads();
-        }
-      }
-      for (int t = tid; t < NB * NB; t += kQrThreads) tglob[t] = s_T[t];
-    }
-    cluster.sync();
-    if (rank != 0) {
-      for (int t = tid; t < NB * NB; t += kQrThreads) s_T[t] = __ldcg(tglob + t);
-      __syncthreads();
-    }
-    // ---- trailing update: C = (I - V T V^T)^T C for columns >= k0 + nbk ----
-    const int c0 = k0 + nbk;
-    const int ntiles = (n - c0 + kTileCols - 1) / kTileCols;
-    for (int tile = rank * kQrWarps + warp; tile < ntiles; tile += csize * kQrWarps) {
-      const int j0 = c0 + tile * kTileCols;
-      double acc[NB][kTileCols];
-#pragma unroll
-      for (int r = 0; r < NB; ++r)
-#pragma unroll
-        for (int q = 0; q < kTileCols; ++q) acc[r][q] = 0.0;
-      for (int i = k0 + lane; i < m; i += 32) {
-        double vr[NB];
-#pragma unroll
-        for (int r = 0; r < NB; ++r)
-          vr[r] = (r < nbk && i >= k0 + r) ? __ldcg(A + (uint64_t)(k0 + r) * lda + i) : 0.0;
-#pragma unroll
-        for (int q = 0; q < kTileCols; ++q) {
-          const double c = (j0 + q < n) ? __ldcg(A + (uint64_t)(j0 + q) * lda + i) : 0.0;
-#pragma unroll
-          for (int r = 0; r < NB; ++r) acc[r][q] += vr[r] * c;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < NB; ++r)
-#pragma unroll
-        for (int q = 0; q < kTileCols; ++q) acc[r][q] = warp_sum(acc[r][q]);
-      // W' = T^T W, in place from the bottom row up
-#pragma unroll
-      for (int r = NB - 1; r >= 0; --r) {
-#pragma unroll
-        for (int q = 0; q < kTileCols; ++q) {
-          double t = 0.0;
-#pragma unroll
-          for (int s = 0; s <= r; ++s) t += s_T[s * NB + r] * acc[s][q];
-          acc[r][q] = t;
-        }
-      }
-      for (int i = k0 + lane; i < m; i += 32) {
-        double vr[NB];
-#pragma unroll
-        for (int r = 0; r < NB; ++r)
-          vr[r] = (r < nbk && i >= k0 + r) ? __ldcg(A + (uint64_t)(k0 + r) * lda + i) : 0.0;
-#pragma unroll
-        for (int q = 0; q < kTileCols; ++q) {
-          if (j0 + q < n) {
-            double* cp = A + (uint64_t)(j0 + q) * lda + i;
-            double c = __ldcg(cp);
-#pragma unroll
-            for (int r = 0; r < NB; ++r) c -= vr[r] * acc[r][q];
-            *cp = c;
-          }
-        }
-      }
-    }
-    cluster.sync();
-  }
 }
 
 // R (rows < K) from a factored job into W (n x n col-major): transpose ? R^T : R
@@ -267,47 +76,159 @@ __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_
   return pos == 0 ? 0 : 1 + (pos - 1 + step) % (n - 1);
 }
 
-// rotate one pair (p, q) of staged columns; returns 1 when rotated
-__device__ __forceinline__ int rotate_pair(double* __restrict__ wp, double* __restrict__ wq, double* vp, double* vq,
-                                           uint32_t rows, uint32_t vrows, double* alpha, int p, int q,
-                                           double freeze, double& max_ratio) {
-  const int lane = threadIdx.x & 31;
+// Rotate one pair (p, q) of staged columns with a group of Q lanes (Q | 32);
+// returns 1 when rotated. Same decision rule as the reference (svd.cpp:232-260):
+// frozen columns are skipped before the dot; the pair rotates when
+// |gamma| > tol * sqrt(alpha_p alpha_q) (tested squared); t, c, s follow
+// zeta = (alpha_q - alpha_p) / (2 gamma), written without the division by gamma:
+// t = sign(zeta) |2 gamma| / (|d| + sqrt(d^2 + 4 gamma^2)), c = rsqrt(1 + t^2).
+// Each group starts its sweep over the rows at a different offset so the
+// lane groups of a warp hit different shared-memory banks.
+template <int Q>
+__device__ __forceinline__ int rotate_pair_q(double* __restrict__ wp, double* __restrict__ wq, double* vp,
+                                             double* vq, uint32_t rows, uint32_t vrows, double* alpha, int p,
+                                             int q, double freeze, double& max_r2, uint32_t stagger) {
+  const int lq = threadIdx.x & (Q - 1);
+  // the Q lanes of one pair synchronize among themselves only: other groups of
+  // the warp may take different branches or have no pair this round
+  const unsigned gmask = (Q == 32) ? 0xffffffffu : (((1u << Q) - 1u) << ((threadIdx.x & 31) & ~(Q - 1)));
   const double ap = alpha[p], aq = alpha[q];
   if (ap <= freeze || aq <= freeze) return 0;
-  double g = 0.0;
-  for (uint32_t i = lane; i < rows; i += 32) g += wp[i] * wq[i];
-  const double gamma = warp_sum(g);
-  const double ratio = fabs(gamma) / sqrt(ap * aq);
-  max_ratio = fmax(max_ratio, ratio);
-  if (ratio <= kJacobiTol) return 0;
-  const double zeta = (aq - ap) / (2.0 * gamma);
-  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-  const double c = 1.0 / sqrt(1.0 + t * t);
+  const uint32_t off = stagger % rows;
+  double g0 = 0.0, g1 = 0.0;
+  uint32_t i = lq + off;
+  uint32_t k = lq;
+  for (; k + Q < rows; k += 2 * Q) {
+    uint32_t i0 = i >= rows ? i - rows : i;
+    uint32_t i1 = i0 + Q >= rows ? i0 + Q - rows : i0 + Q;
+    g0 += wp[i0] * wq[i0];
+    g1 += wp[i1] * wq[i1];
+    i += 2 * Q;
+    if (i >= 2 * rows) i -= rows;
+  }
+  if (k < rows) {
+    uint32_t i0 = i >= rows ? i - rows : i;
+    g0 += wp[i0] * wq[i0];
+  }
+  double gamma = g0 + g1;
+#pragma unroll
+  for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(gmask, gamma, o);
+  const double prod = ap * aq;
+  const double r2 = gamma * gamma / prod;
+  max_r2 = fmax(max_r2, r2);
+  if (!(gamma * gamma > kJacobiTol * kJacobiTol * prod)) return 0;
+  const double d = aq - ap, e = 2.0 * gamma;
+  const double sgn = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? 1.0 : -1.0;
+  const double t = sgn * fabs(e) / (fabs(d) + sqrt(fma(d, d, e * e)));
+  const double c = rsqrt(fma(t, t, 1.0));
   const double s = c * t;
-  for (uint32_t i = lane; i < rows; i += 32) {
-    const double xp = wp[i], xq = wq[i];
-    wp[i] = c * xp - s * xq;
-    wq[i] = s * xp + c * xq;
+  i = lq + off;
+  for (k = lq; k < rows; k += Q) {
+    const uint32_t ii = i >= rows ? i - rows : i;
+    const double xp = wp[ii], xq = wq[ii];
+    wp[ii] = c * xp - s * xq;
+    wq[ii] = s * xp + c * xq;
+    i += Q;
   }
   if (vp) {
-    for (uint32_t i = lane; i < vrows; i += 32) {
-      const double xp = vp[i], xq = vq[i];
-      vp[i] = c * xp - s * xq;
-      vq[i] = s * xp + c * xq;
+    for (uint32_t j = lq; j < vrows; j += Q) {
+      const double xp = vp[j], xq = vq[j];
+      vp[j] = c * xp - s * xq;
+      vq[j] = s * xp + c * xq;
     }
   }
-  __syncwarp();
-  if (lane == 0) {
+  __syncwarp(gmask);
+  if (lq == 0) {
     const double na = c * c * ap - 2.0 * c * s * gamma + s * s * aq;
     const double nq = s * s * ap + 2.0 * c * s * gamma + c * c * aq;
     alpha[p] = na > 0.0 ? na : 0.0;
     alpha[q] = nq > 0.0 ? nq : 0.0;
   }
-  __syncwarp();
+  __syncwarp(gmask);
   return 1;
 }
 
-__global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams P) {
+// Cross round r pairs A_t with B_{(t+r) mod g}. Group t keeps A_t (and its alpha)
+// in registers for all g rounds of the step and streams the B columns through
+// shared memory: per element-pair one 8-byte shared load and one store (the
+// B value), instead of re-reading and re-writing both columns.
+template <int Q, int E>
+__device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint32_t rows, uint32_t g, double* sAlpha,
+                                                 double freeze, double& max_r2, unsigned long long& my_rot) {
+  const int tid = threadIdx.x;
+  const int grp = tid / Q, lq = tid & (Q - 1);
+  const unsigned gmask = (Q == 32) ? 0xffffffffu : (((1u << Q) - 1u) << ((tid & 31) & ~(Q - 1)));
+  const bool active = (uint32_t)grp < g;
+  double a[E];
+  double aA = 0.0;
+  if (active) {
+    const double* pa = sW + (uint64_t)grp * ldS;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const uint32_t i = lq + Q * k;
+      a[k] = i < rows ? pa[i] : 0.0;
+    }
+    aA = sAlpha[grp];
+  }
+  for (uint32_t r = 0; r < g; ++r) {
+    if (active) {
+      const uint32_t j = g + ((uint32_t)grp + r) % g;
+      double* pb = sW + (uint64_t)j * ldS;
+      const double aB = sAlpha[j];
+      if (!(aA <= freeze || aB <= freeze)) {
+        double b[E];
+        double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          const uint32_t i = lq + Q * k;
+          b[k] = i < rows ? pb[i] : 0.0;
+          if (k & 1) g1 += a[k] * b[k];
+          else g0 += a[k] * b[k];
+        }
+        double gamma = g0 + g1;
+#pragma unroll
+        for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(gmask, gamma, o);
+        const double prod = aA * aB;
+        max_r2 = fmax(max_r2, gamma * gamma / prod);
+        if (gamma * gamma > kJacobiTol * kJacobiTol * prod) {
+          const double d = aB - aA, e = 2.0 * gamma;
+          const double sgn = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? 1.0 : -1.0;
+          const double t = sgn * fabs(e) / (fabs(d) + sqrt(fma(d, d, e * e)));
+          const double c = rsqrt(fma(t, t, 1.0));
+          const double sn = c * t;
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            const uint32_t i = lq + Q * k;
+            const double xp = a[k], xq = b[k];
+            a[k] = c * xp - sn * xq;
+            if (i < rows) pb[i] = sn * xp + c * xq;
+          }
+          const double na = c * c * aA - 2.0 * c * sn * gamma + sn * sn * aB;
+          const double nq = sn * sn * aA + 2.0 * c * sn * gamma + c * c * aB;
+          aA = na > 0.0 ? na : 0.0;
+          if (lq == 0) {
+            sAlpha[j] = nq > 0.0 ? nq : 0.0;
+            ++my_rot;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (active) {
+    double* pa = sW + (uint64_t)grp * ldS;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const uint32_t i = lq + Q * k;
+      if (i < rows) pa[i] = a[k];
+    }
+    if (lq == 0) sAlpha[grp] = aA;
+  }
+  __syncthreads();
+}
+
+template <int Q, int E>
+__global__ void __launch_bounds__(kJThreads, 1) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
@@ -317,19 +238,21 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool with_v = P.with_v && job.v;
   const uint32_t vrows = cols_pad;
+  const uint32_t ldS = rows + 8, ldV = vrows + 8;  // padded: consecutive columns start in alternate bank halves
 
-  double* sW = smem;                                    // 2g columns x rows
-  double* sV = sW + (uint64_t)2 * g * rows;             // 2g columns x vrows (optional)
-  double* sAlpha = sV + (with_v ? (uint64_t)2 * g * vrows : 0);  // 2g
+  double* sW = smem;                                          // 2g columns, stride ldS
+  double* sV = sW + (uint64_t)2 * g * ldS;                    // 2g columns, stride ldV (optional)
+  double* sAlpha = sV + (with_v ? (uint64_t)2 * g * ldV : 0);  // 2g
   __shared__ double s_red[kJWarps];
   __shared__ double s_amax;
   __shared__ unsigned long long s_rot;
-  __shared__ double s_maxratio;
 
-  unsigned long long* counters = reinterpret_cast<unsigned long long*>(job.stats + 4);  // [3] rotations per sweep mod 3
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(job.stats + 4);  // rotations per sweep, mod 3
   double* W = job.w;
   double* V = job.v;
   double* alpha_g = job.alpha;
+  constexpr int kGroups = kJThreads / Q;
+  const int grp_id = tid / Q;
 
   unsigned long long total_rot = 0;
   double last_max_ratio = 0.0;
@@ -353,7 +276,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
     for (uint32_t j = tid; j < cols_pad; j += kJThreads) amax = fmax(amax, __ldcg(alpha_g + j));
     for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if (lane == 0) s_red[warp] = amax;
-    if (tid == 0) { s_rot = 0ull; s_maxratio = 0.0; }
+    if (tid == 0) s_rot = 0ull;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
@@ -372,11 +295,11 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
         for (uint32_t c = warp; c < 2 * g; c += kJWarps) {
           const uint32_t col = (c < g ? gA * g + c : gB * g + (c - g));
           const double* src = W + (uint64_t)col * rows;
-          double* dst = sW + (uint64_t)c * rows;
+          double* dst = sW + (uint64_t)c * ldS;
           for (uint32_t i = lane; i < rows; i += 32) dst[i] = __ldcg(src + i);
           if (with_v) {
             const double* vs = V + (uint64_t)col * vrows;
-            double* vd = sV + (uint64_t)c * vrows;
+            double* vd = sV + (uint64_t)c * ldV;
             for (uint32_t i = lane; i < vrows; i += 32) vd[i] = __ldcg(vs + i);
           }
           if (lane == 0) sAlpha[c] = __ldcg(alpha_g + col);
@@ -385,40 +308,44 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
         // intra-group rounds (first step only: every group appears once)
         if (step == 0) {
           for (uint32_t r = 0; r + 1 < g; ++r) {
-            for (uint32_t t = warp; t < g; t += kJWarps) {
+            for (uint32_t t = grp_id; t < g; t += kGroups) {
               const uint32_t half = g / 2;
               const uint32_t grp = t / half, i = t % half;
               const uint32_t p = grp * g + rr_slot(i, r, g), q = grp * g + rr_slot(g - 1 - i, r, g);
-              double* vp = with_v ? sV + (uint64_t)p * vrows : nullptr;
-              double* vq = with_v ? sV + (uint64_t)q * vrows : nullptr;
-              int rot = rotate_pair(sW + (uint64_t)p * rows, sW + (uint64_t)q * rows, vp, vq, rows, vrows, sAlpha,
-                                    p, q, freeze, my_ratio);
-              my_rot += (lane == 0) ? rot : 0;
+              double* vp = with_v ? sV + (uint64_t)p * ldV : nullptr;
+              double* vq = with_v ? sV + (uint64_t)q * ldV : nullptr;
+              int rot = rotate_pair_q<Q>(sW + (uint64_t)p * ldS, sW + (uint64_t)q * ldS, vp, vq, rows, vrows,
+                                         sAlpha, p, q, freeze, my_ratio, 0);
+              my_rot += ((tid & (Q - 1)) == 0) ? rot : 0;
             }
             __syncthreads();
           }
         }
         // cross rounds: (A_i, B_{(i + r) mod g})
-        for (uint32_t r = 0; r < g; ++r) {
-          for (uint32_t i = warp; i < g; i += kJWarps) {
-            const uint32_t p = i, q = g + (i + r) % g;
-            double* vp = with_v ? sV + (uint64_t)p * vrows : nullptr;
-            double* vq = with_v ? sV + (uint64_t)q * vrows : nullptr;
-            int rot = rotate_pair(sW + (uint64_t)p * rows, sW + (uint64_t)q * rows, vp, vq, rows, vrows, sAlpha, p,
-                                  q, freeze, my_ratio);
-            my_rot += (lane == 0) ? rot : 0;
+        if constexpr (E > 0) {
+          cross_rounds_reg<Q, E>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
+        } else {
+          for (uint32_t r = 0; r < g; ++r) {
+            for (uint32_t t = grp_id; t < g; t += kGroups) {
+              const uint32_t p = t, q = g + (t + r) % g;
+              double* vp = with_v ? sV + (uint64_t)p * ldV : nullptr;
+              double* vq = with_v ? sV + (uint64_t)q * ldV : nullptr;
+              int rot = rotate_pair_q<Q>(sW + (uint64_t)p * ldS, sW + (uint64_t)q * ldS, vp, vq, rows, vrows,
+                                         sAlpha, p, q, freeze, my_ratio, 0);
+              my_rot += ((tid & (Q - 1)) == 0) ? rot : 0;
+            }
+            __syncthreads();
           }
-          __syncthreads();
         }
         // write back
         for (uint32_t c = warp; c < 2 * g; c += kJWarps) {
           const uint32_t col = (c < g ? gA * g + c : gB * g + (c - g));
           double* dst = W + (uint64_t)col * rows;
-          const double* src = sW + (uint64_t)c * rows;
+          const double* src = sW + (uint64_t)c * ldS;
           for (uint32_t i = lane; i < rows; i += 32) dst[i] = src[i];
           if (with_v) {
             double* vd = V + (uint64_t)col * vrows;
-            const double* vs = sV + (uint64_t)c * vrows;
+            const double* vs = sV + (uint64_t)c * ldV;
             for (uint32_t i = lane; i < vrows; i += 32) vd[i] = vs[i];
           }
           if (lane == 0) alpha_g[col] = sAlpha[c];
@@ -427,7 +354,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
       }
       if (step + 2 == G) {
         // last step of the sweep: publish this CTA's rotation count and max ratio
-        if (lane == 0 && my_rot) atomicAdd(&s_rot, my_rot);
+        if (my_rot) atomicAdd(&s_rot, my_rot);
         for (int o = 16; o; o >>= 1) my_ratio = fmax(my_ratio, __shfl_xor_sync(0xffffffffu, my_ratio, o));
         if (lane == 0) s_red[warp] = my_ratio;
         __syncthreads();
@@ -435,8 +362,9 @@ __global__ void __launch_bounds__(kJThreads) jacobi_cluster_kernel(JacobiParams 
           double t = 0.0;
           for (int w = 0; w < kJWarps; ++w) t = fmax(t, s_red[w]);
           if (s_rot) atomicAdd(&counters[sweep % 3], s_rot);
-          // max ratio across the cluster: doubles >= 0 order like their bit patterns
-          atomicMax(reinterpret_cast<unsigned long long*>(job.stats + 3), __double_as_longlong(t));
+          // max ratio across the cluster (my_ratio holds ratio^2); doubles >= 0
+          // order like their bit patterns
+          atomicMax(reinterpret_cast<unsigned long long*>(job.stats + 3), __double_as_longlong(sqrt(t)));
         }
       }
       cluster.sync();
@@ -615,49 +543,7 @@ __global__ void apply_q_kernel(QrJob qr, const double* x, uint32_t x_rows, uint3
   }
 }
 
-template <class K>
-void launch_cluster(K kernel, unsigned grid, unsigned cluster, unsigned threads, size_t smem, cudaStream_t s,
-                    void** args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(threads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  RK_CUDA_CHECK(cudaLaunchKernelExC(&cfg, (const void*)kernel, args));
-  RK_LAUNCH_CHECK();
-}
-
 }  // namespace
-
-void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
-  if (jobs.empty()) return;
-  static bool configured = false;
-  if (!configured) {
-    RK_CUDA_CHECK(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
-  // cluster size: spread the batch over the SMs, at most 8 CTAs per matrix
-  unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)(2 * sms) / jobs.size());
-  unsigned widest = 0;
-  for (const QrJob& j : jobs) widest = std::max(widest, j.n);
-  const unsigned useful = std::max(1u, (widest / kTileCols + kQrWarps - 1) / kQrWarps);
-  cl = std::min({cl, 8u, useful});
-  unsigned p2 = 1;
-  while (p2 * 2 <= cl) p2 *= 2;
-  cl = p2;
-  DBuf<QrJob> dj(jobs.size(), s);
-  to_device(dj.get(), jobs.data(), jobs.size(), s);
-  QrArgs args{dj.get()};
-  void* kargs[] = {&args};
-  launch_cluster(qr_cluster_kernel, (unsigned)jobs.size() * cl, cl, kQrThreads, 0, s, kargs);
-}
 
 void r_extract_batched(const std::vector<RJob>& jobs, bool transpose, cudaStream_t s) {
   if (jobs.empty()) return;
@@ -673,8 +559,14 @@ void r_extract_batched(const std::vector<RJob>& jobs, bool transpose, cudaStream
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
 
 void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, uint32_t& g, uint32_t& G) {
-  // largest even group size (<= 32) whose two staged groups fit the shared-memory budget
-  for (uint32_t gmax = 32; gmax >= 2; gmax -= 2) {
+  // largest even group size (<= gcap) whose two staged groups fit the budget; a
+  // smaller cap trades longer tournaments for more CTAs per SM (latency hiding)
+  static const uint32_t gcap = [] {
+    const char* e = std::getenv("RK_JACOBI_GMAX");
+    const long v = e ? std::strtol(e, nullptr, 10) : 16;
+    return (uint32_t)std::max<long>(2, std::min<long>(32, v & ~1L));
+  }();
+  for (uint32_t gmax = gcap; gmax >= 2; gmax -= 2) {
     G = (uint32_t)ceil_div(cols ? cols : 1, gmax);
     if (G < 2) G = 2;
     if (G & 1) ++G;
@@ -687,9 +579,8 @@ void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, 
 }
 
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v) {
-  return (size_t)2 * g * rows * 8 + (with_v ? (size_t)2 * g * cols_pad * 8 : 0) + (size_t)2 * g * 8;
+  return (size_t)2 * g * (rows + 8) * 8 + (with_v ? (size_t)2 * g * (cols_pad + 8) * 8 : 0) + (size_t)2 * g * 8;
 }
-
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin) {
   if (jobs.empty()) return;
   // jobs in one launch share rows / cols_pad / with_v (the caller groups them);
@@ -706,9 +597,9 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   }
   if (g * G != cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols_pad is not a planned width");
   const size_t smem = jacobi_smem(rows, g, g * G, with_v);
-  RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)sms / jobs.size());
+  // cluster size: enough CTAs for the SMs at the occupancy the shared memory allows
+  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (smem + 2048)));
+  unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)sms * per_sm / jobs.size());
   cl = std::min<unsigned>({cl, G / 2, 8u});
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
@@ -717,7 +608,31 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   JacobiParams P{dj.get(), g, G, with_v ? 1 : 0};
   void* kargs[] = {&P};
-  launch_cluster(jacobi_cluster_kernel, (unsigned)jobs.size() * cl, cl, kJThreads, smem, s, kargs);
+  // lanes per pair: enough lane groups for the g pairs of a round; E = column
+  // elements per lane held in registers by the cross rounds (0: shared-memory path)
+  int Q = 32;
+  while (Q > 8 && (kJThreads / Q) < (int)g) Q /= 2;
+  int E = 1;
+  while (E * Q < (int)rows) E *= 2;
+  if (E < 4) E = 4;
+  if (E > 32 || with_v) E = 0;  // a[E] + b[E] must stay in registers
+  auto launch = [&](auto kern) {
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    launch_cluster_kernel((const void*)kern, (unsigned)jobs.size() * cl, cl, kJThreads, smem, s, kargs);
+  };
+#define RK_JAC_E(QQ)                                                  \
+  switch (E) {                                                        \
+    case 4: launch(jacobi_cluster_kernel<QQ, 4>); break;              \
+    case 8: launch(jacobi_cluster_kernel<QQ, 8>); break;              \
+    case 16: launch(jacobi_cluster_kernel<QQ, 16>); break;            \
+    case 32: launch(jacobi_cluster_kernel<QQ, 32>); break;            \
+    default: launch(jacobi_cluster_kernel<QQ, 0>); break;             \
+  }
+  if (Q == 8) { RK_JAC_E(8) }
+  else if (Q == 16) { RK_JAC_E(16) }
+  else { RK_JAC_E(32) }
+#undef RK_JAC_E
 }
 
 uint32_t jacobi_cols_pad(uint32_t rows, uint32_t cols, bool with_v, size_t smem_optin) {

@@ -105,6 +105,25 @@ inline void sync(cudaStream_t s) { RK_CUDA_CHECK(cudaStreamSynchronize(s)); }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// launch `kern` as clusters of `cluster` CTAs along x
+inline void launch_cluster_kernel(const void* kern, unsigned grid, unsigned cluster, unsigned threads, size_t smem,
+                                  cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RK_CUDA_CHECK(cudaLaunchKernelExC(&cfg, kern, args));
+  RK_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------------------
 // KeyedRng -- proj/src/rng.cpp:8-38, usable on host and device
 
@@ -247,7 +266,8 @@ struct QrJob {        // one tall matrix, column-major, in place
   double* beta;       // n: Householder betas (0 = identity)
   double* tmat;       // ceil(n/NB) * NB * NB: compact-WY T factors
 };
-void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms);
+void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms);  // rk_qr.cu
+uint32_t qr_max_rows();  // tallest matrix a panel can stage
 
 // W := R^T (transpose=true) or R (false) from a factored QrJob; W is n x n col-major,
 // zero-filled outside the triangle. rows: number of R rows (min(m, n)).

@@ -301,7 +301,6 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     const uint32_t cols_pad = cols_pad_full;
     DBuf<double> st(staging ? staging : 1, s);
     DBuf<double> W((uint64_t)nb * M * cols_pad, s);
-    DBuf<double> qr_aux((uint64_t)nb * aux_sz, s);
     DBuf<double> alpha((uint64_t)nb * cols_pad, s);
     DBuf<uint64_t> stats(8 * nb, s);
     DBuf<uint32_t> order((uint64_t)nb * cols_pad, s);
@@ -322,28 +321,34 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     RK_CUDA_CHECK(cudaEventRecord(c.ev[0], s));
     compaction_fill(a, p, fill_tall, d_lo, single.get(), st.get(), s);
     compaction_fill(a, p, fill_wide, d_lo, single.get(), W.get(), s);
-    std::vector<QrJob> qj;
-    std::vector<RJob> rj;
-    for (size_t q = 0; q < nb; ++q) {
-      if (!plans[q].tall) continue;
-      double* aux = qr_aux.get() + (uint64_t)q * aux_sz;
-      QrJob j;
-      j.a = st.get() + plans[q].offset;
-      j.lda = plans[q].n_rows;
-      j.m = plans[q].n_rows;
-      j.n = M;
-      j.diag = aux;
-      j.beta = aux + M;
-      j.tmat = aux + 2 * M;
-      qj.push_back(j);
-      RJob r;
-      r.a = j.a; r.lda = j.lda; r.diag = j.diag; r.m = j.m; r.n = j.n;
-      r.w = W.get() + (uint64_t)q * M * cols_pad;
-      r.ldw = M;
-      rj.push_back(r);
+    // tall blocks: TSQR of T_d over row leaves of at most kLeafRows rows (factored in
+    // place), pairwise tree, then W = R^T into the block's Jacobi slot
+    {
+      constexpr uint32_t kLeafRows = 1024;
+      std::vector<std::vector<LeafRef>> trees;
+      std::vector<size_t> tree_q;
+      for (size_t q = 0; q < nb; ++q) {
+        if (!plans[q].tall) continue;
+        const uint32_t nr = plans[q].n_rows;
+        const uint32_t L = (uint32_t)ceil_div(nr, kLeafRows);
+        std::vector<LeafRef> leaves;
+        for (uint32_t i = 0; i < L; ++i) {
+          const uint64_t r0 = (uint64_t)nr * i / L, r1 = (uint64_t)nr * (i + 1) / L;
+          leaves.push_back({st.get() + plans[q].offset + r0, nr, (uint32_t)(r1 - r0)});
+        }
+        trees.push_back(std::move(leaves));
+        tree_q.push_back(q);
+      }
+      if (!trees.empty()) {
+        std::vector<DBuf<double>> roots;
+        tsqr_forest(c, M, trees, roots);
+        for (size_t t = 0; t < trees.size(); ++t) {
+          transpose_sq<<<grid_for((uint64_t)M * M), 256, 0, s>>>(roots[t].get(), M,
+                                                                 W.get() + (uint64_t)tree_q[t] * M * cols_pad);
+          RK_LAUNCH_CHECK();
+        }
+      }
     }
-    qr_batched(qj, s, c.num_sms);
-    r_extract_batched(rj, /*transpose=*/true, s);
     RK_CUDA_CHECK(cudaEventRecord(c.ev[1], s));
     std::vector<JacobiJob> jj(nb);
     for (size_t q = 0; q < nb; ++q) {
@@ -419,19 +424,20 @@ std::vector<TreeLeaf> merge_leaves(const std::vector<uint32_t>& kept, uint32_t M
 
 namespace {
 
-// QR every matrix of a level; returns their R factors (n x n column-major)
-void qr_level(Ctx& c, std::vector<DBuf<double>>& mats, std::vector<uint32_t>& hs, uint32_t n) {
+// QR every matrix of a level in place and extract the R factors (n x n column-major,
+// rows >= min(h, n) zero); heights become min(h, n)
+void qr_level(Ctx& c, std::vector<LeafRef>& mats, std::vector<DBuf<double>>& rs, uint32_t n) {
   cudaStream_t s = c.stream;
   const size_t cnt = mats.size();
   const uint64_t aux_sz = 2 * (uint64_t)n + (ceil_div(n, 16) + 1) * 256;
   DBuf<double> aux(cnt * aux_sz, s);
   std::vector<QrJob> qj;
   std::vector<RJob> rj;
-  std::vector<DBuf<double>> rs;
+  rs.clear();
   rs.reserve(cnt);
   for (size_t q = 0; q < cnt; ++q) {
     QrJob j;
-    j.a = mats[q].get(); j.lda = hs[q]; j.m = hs[q]; j.n = n;
+    j.a = mats[q].a; j.lda = mats[q].lda; j.m = mats[q].m; j.n = n;
     j.diag = aux.get() + q * aux_sz; j.beta = j.diag + n; j.tmat = j.diag + 2 * n;
     qj.push_back(j);
     rs.emplace_back((uint64_t)n * n, s);
@@ -441,35 +447,77 @@ void qr_level(Ctx& c, std::vector<DBuf<double>>& mats, std::vector<uint32_t>& hs
   }
   qr_batched(qj, s, c.num_sms);
   r_extract_batched(rj, /*transpose=*/false, s);
-  for (size_t q = 0; q < cnt; ++q) hs[q] = std::min<uint32_t>(hs[q], n);
-  mats = std::move(rs);
+  for (size_t q = 0; q < cnt; ++q) mats[q].m = std::min<uint32_t>(mats[q].m, n);
 }
 
-// pairwise tree over R factors (heights <= n): returns the root
-void tree_reduce(Ctx& c, std::vector<DBuf<double>>& nodes, std::vector<uint32_t>& heights, uint32_t n) {
+}  // namespace
+
+// pairwise levels over the nodes of every tree, batched across trees: (0,1), (2,3), ...;
+// an odd last node is carried up unchanged. Leaves each tree with one node.
+void forest_reduce(Ctx& c, uint32_t n, std::vector<std::vector<DBuf<double>>>& nodes,
+                   std::vector<std::vector<uint32_t>>& heights) {
   cudaStream_t s = c.stream;
-  while (nodes.size() > 1) {
-    std::vector<DBuf<double>> next;
-    std::vector<uint32_t> nh;
-    for (size_t q = 0; q + 1 < nodes.size(); q += 2) {
-      const uint32_t h = heights[q] + heights[q + 1];
-      next.emplace_back((uint64_t)h * n, s);
-      stack_r<<<grid_for((uint64_t)h * n), 256, 0, s>>>(nodes[q].get(), heights[q], nodes[q + 1].get(),
-                                                         heights[q + 1], n, next.back().get());
-      RK_LAUNCH_CHECK();
-      nh.push_back(h);
+  const size_t T = nodes.size();
+  for (;;) {
+    std::vector<LeafRef> stacked;
+    std::vector<DBuf<double>> bufs;
+    std::vector<std::pair<size_t, size_t>> where;  // (tree, pair index)
+    for (size_t t = 0; t < T; ++t) {
+      for (size_t q = 0; q + 1 < nodes[t].size(); q += 2) {
+        const uint32_t h = heights[t][q] + heights[t][q + 1];
+        bufs.emplace_back((uint64_t)h * n, s);
+        stack_r<<<grid_for((uint64_t)h * n), 256, 0, s>>>(nodes[t][q].get(), heights[t][q], nodes[t][q + 1].get(),
+                                                           heights[t][q + 1], n, bufs.back().get());
+        RK_LAUNCH_CHECK();
+        stacked.push_back({bufs.back().get(), h, h});
+        where.push_back({t, q / 2});
+      }
     }
-    qr_level(c, next, nh, n);
-    if (nodes.size() & 1) {
-      next.push_back(std::move(nodes.back()));
-      nh.push_back(heights.back());
+    if (stacked.empty()) break;
+    std::vector<DBuf<double>> out;
+    qr_level(c, stacked, out, n);
+    std::vector<std::vector<DBuf<double>>> next(T);
+    std::vector<std::vector<uint32_t>> nh(T);
+    size_t k = 0;
+    for (size_t t = 0; t < T; ++t) {
+      const size_t pairs = nodes[t].size() / 2;
+      for (size_t q = 0; q < pairs; ++q, ++k) {
+        next[t].push_back(std::move(out[k]));
+        nh[t].push_back(stacked[k].m);
+      }
+      if (nodes[t].size() & 1) {
+        next[t].push_back(std::move(nodes[t].back()));
+        nh[t].push_back(heights[t].back());
+      }
     }
     nodes = std::move(next);
     heights = std::move(nh);
   }
 }
 
-}  // namespace
+void tsqr_forest(Ctx& c, uint32_t n, std::vector<std::vector<LeafRef>>& leaves, std::vector<DBuf<double>>& roots) {
+  cudaStream_t s = c.stream;
+  const size_t T = leaves.size();
+  // level 0: every leaf of every tree in one batch
+  std::vector<LeafRef> flat;
+  std::vector<size_t> owner;
+  for (size_t t = 0; t < T; ++t)
+    for (const LeafRef& L : leaves[t]) {
+      flat.push_back(L);
+      owner.push_back(t);
+    }
+  std::vector<DBuf<double>> rs;
+  qr_level(c, flat, rs, n);
+  std::vector<std::vector<DBuf<double>>> nodes(T);
+  std::vector<std::vector<uint32_t>> heights(T);
+  for (size_t q = 0; q < flat.size(); ++q) {
+    nodes[owner[q]].push_back(std::move(rs[q]));
+    heights[owner[q]].push_back(flat[q].m);
+  }
+  forest_reduce(c, n, nodes, heights);
+  roots.clear();
+  for (size_t t = 0; t < T; ++t) roots.push_back(std::move(nodes[t][0]));
+}
 
 void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
                    const std::vector<uint32_t>& kept, uint32_t M, const std::vector<TreeLeaf>& leaves,
@@ -479,26 +527,33 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   DBuf<uint32_t> dkept(kept.size(), s);
   to_device(doff.get(), offset.data(), offset.size(), s);
   to_device(dkept.get(), kept.data(), kept.size(), s);
-  std::vector<DBuf<double>> nodes;
-  std::vector<uint32_t> heights;
+  std::vector<DBuf<double>> bufs;
+  std::vector<std::vector<LeafRef>> tree(1);
   for (size_t l = leaf_lo; l < leaf_hi; ++l) {
     const TreeLeaf& L = leaves[l];
-    nodes.emplace_back((uint64_t)L.height * M, s);
-    heights.push_back(L.height);
+    bufs.emplace_back((uint64_t)L.height * M, s);
     gather_leaf<<<grid_for((uint64_t)L.height * M), 256, 0, s>>>(payload, doff.get(), dkept.get(), L.r0, L.r1, M,
-                                                                 L.height, nodes.back().get());
+                                                                 L.height, bufs.back().get());
     RK_LAUNCH_CHECK();
+    tree[0].push_back({bufs.back().get(), L.height, L.height});
   }
-  qr_level(c, nodes, heights, M);
-  tree_reduce(c, nodes, heights, M);
-  r_out = std::move(nodes[0]);
+  std::vector<DBuf<double>> roots;
+  tsqr_forest(c, M, tree, roots);
+  r_out = std::move(roots[0]);
   sync(s);  // host vectors (offset copies) are released
 }
 
 void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut& out) {
   cudaStream_t s = c.stream;
-  std::vector<uint32_t> heights(roots.size(), M);
-  tree_reduce(c, roots, heights, M);
+  if (roots.size() > 1) {
+    // the roots are the R factors of complete subtrees: continue the same pairwise tree
+    std::vector<std::vector<DBuf<double>>> nodes(1);
+    std::vector<std::vector<uint32_t>> heights(1, std::vector<uint32_t>(roots.size(), M));
+    for (auto& r : roots) nodes[0].push_back(std::move(r));
+    forest_reduce(c, M, nodes, heights);
+    roots.clear();
+    roots.push_back(std::move(nodes[0][0]));
+  }
   const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
   DBuf<double> W((uint64_t)M * cp, s);
   W.zero();

@@ -33,6 +33,15 @@ struct MergeOut {
   uint64_t sweeps = 0, rotations = 0;
 };
 
+// TSQR over a forest: every tree's leaves (column-major, factored in place) are
+// reduced by a fixed pairwise tree to one R factor (n x n column-major, upper)
+struct LeafRef {
+  double* a;
+  uint64_t lda;
+  uint32_t m;
+};
+void tsqr_forest(Ctx& c, uint32_t n, std::vector<std::vector<LeafRef>>& leaves, std::vector<DBuf<double>>& roots);
+
 // leaves of the merge tree: consecutive records, each leaf at least M rows of P^T
 struct TreeLeaf {
   uint32_t r0, r1, height;

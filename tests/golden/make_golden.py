@@ -105,9 +105,13 @@ def main():
             arrays[key + "_sigma"], arrays[key + "_u"] = s.sigma, s.u
     # pipelines (sigma, U, records) on desk-scale instances
     pipes = {}
+    vrng = np.random.default_rng(99)
+    valued = (desk[0], desk[1], desk[2], desk[3], vrng.uniform(0.5, 1.5, len(desk[2])) * vrng.choice([-1, 1], len(desk[2])))
     for name, (m, D, meth, keep, seed) in {
         "desk_D8_neighbor": (desk, 8, "neighbor", 0, 3),
-        "desk_D16_random_keep3": (desk, 16, "random", 3, 5),
+        # keep < rank needs distinct singular values at the cut (value-1.0 blocks are
+        # degenerate there and the kept vectors would be an arbitrary basis choice)
+        "valued_D16_random_keep3": (valued, 16, "random", 3, 5),
         "synth16x96_D6_nr": (R.synth_bipartite(16, 96, 0.05, 8), 6, "neighbor-random", 0, 3),
     }.items():
         res = R.run_pipeline(m, D, meth, keep, seed, 4)
