@@ -177,15 +177,14 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
       const double aB = sAlpha[j];
       if (!(aA <= freeze || aB <= freeze)) {
         double b[E];
-        double g0 = 0.0, g1 = 0.0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int k = 0; k < E; ++k) {
           const uint32_t i = lq + Q * k;
           b[k] = i < rows ? pb[i] : 0.0;
-          if (k & 1) g1 += a[k] * b[k];
-          else g0 += a[k] * b[k];
+          acc[k & 3] += a[k] * b[k];
         }
-        double gamma = g0 + g1;
+        double gamma = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
         for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(gmask, gamma, o);
         const double prod = aA * aB;
@@ -228,7 +227,7 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
 }
 
 template <int Q, int E>
-__global__ void __launch_bounds__(kJThreads, 1) jacobi_cluster_kernel(JacobiParams P) {
+__global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
@@ -619,6 +618,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   auto launch = [&](auto kern) {
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     launch_cluster_kernel((const void*)kern, (unsigned)jobs.size() * cl, cl, kJThreads, smem, s, kargs);
   };
 #define RK_JAC_E(QQ)                                                  \

@@ -265,6 +265,7 @@ struct QrJob {        // one tall matrix, column-major, in place
   double* diag;       // n: R's diagonal
   double* beta;       // n: Householder betas (0 = identity)
   double* tmat;       // ceil(n/NB) * NB * NB: compact-WY T factors
+  uint32_t split = 0; // > 0: [R_a; R_b] stacked triangles, R_a = rows [0, split) (split == n)
 };
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms);  // rk_qr.cu
 uint32_t qr_max_rows();  // tallest matrix a panel can stage

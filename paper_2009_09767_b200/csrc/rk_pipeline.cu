@@ -324,7 +324,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     // tall blocks: TSQR of T_d over row leaves of at most kLeafRows rows (factored in
     // place), pairwise tree, then W = R^T into the block's Jacobi slot
     {
-      constexpr uint32_t kLeafRows = 1024;
+      constexpr uint32_t kLeafRows = 768;
       std::vector<std::vector<LeafRef>> trees;
       std::vector<size_t> tree_q;
       for (size_t q = 0; q < nb; ++q) {
@@ -334,7 +334,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         std::vector<LeafRef> leaves;
         for (uint32_t i = 0; i < L; ++i) {
           const uint64_t r0 = (uint64_t)nr * i / L, r1 = (uint64_t)nr * (i + 1) / L;
-          leaves.push_back({st.get() + plans[q].offset + r0, nr, (uint32_t)(r1 - r0)});
+          leaves.push_back({st.get() + plans[q].offset + r0, nr, (uint32_t)(r1 - r0), 0u});
         }
         trees.push_back(std::move(leaves));
         tree_q.push_back(q);
@@ -437,7 +437,7 @@ void qr_level(Ctx& c, std::vector<LeafRef>& mats, std::vector<DBuf<double>>& rs,
   rs.reserve(cnt);
   for (size_t q = 0; q < cnt; ++q) {
     QrJob j;
-    j.a = mats[q].a; j.lda = mats[q].lda; j.m = mats[q].m; j.n = n;
+    j.a = mats[q].a; j.lda = mats[q].lda; j.m = mats[q].m; j.n = n; j.split = mats[q].split;
     j.diag = aux.get() + q * aux_sz; j.beta = j.diag + n; j.tmat = j.diag + 2 * n;
     qj.push_back(j);
     rs.emplace_back((uint64_t)n * n, s);
@@ -469,7 +469,8 @@ void forest_reduce(Ctx& c, uint32_t n, std::vector<std::vector<DBuf<double>>>& n
         stack_r<<<grid_for((uint64_t)h * n), 256, 0, s>>>(nodes[t][q].get(), heights[t][q], nodes[t][q + 1].get(),
                                                            heights[t][q + 1], n, bufs.back().get());
         RK_LAUNCH_CHECK();
-        stacked.push_back({bufs.back().get(), h, h});
+        // a full n x n top triangle lets the combine skip the rows that stay zero
+        stacked.push_back({bufs.back().get(), h, h, heights[t][q] == n ? n : 0u});
         where.push_back({t, q / 2});
       }
     }
@@ -535,7 +536,7 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
     gather_leaf<<<grid_for((uint64_t)L.height * M), 256, 0, s>>>(payload, doff.get(), dkept.get(), L.r0, L.r1, M,
                                                                  L.height, bufs.back().get());
     RK_LAUNCH_CHECK();
-    tree[0].push_back({bufs.back().get(), L.height, L.height});
+    tree[0].push_back({bufs.back().get(), L.height, L.height, 0u});
   }
   std::vector<DBuf<double>> roots;
   tsqr_forest(c, M, tree, roots);

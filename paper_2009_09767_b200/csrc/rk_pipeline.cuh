@@ -39,6 +39,7 @@ struct LeafRef {
   double* a;
   uint64_t lda;
   uint32_t m;
+  uint32_t split;  // see QrJob::split
 };
 void tsqr_forest(Ctx& c, uint32_t n, std::vector<std::vector<LeafRef>>& leaves, std::vector<DBuf<double>>& roots);
 

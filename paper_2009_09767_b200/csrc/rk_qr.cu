@@ -1,20 +1,30 @@
 // rk_qr.cu -- batched blocked Householder QR of tall column-major FP64 matrices
 // (reference: householder_qr, proj/src/svd.cpp:77-107).
 //
-// One thread-block cluster per matrix (cluster size 1 when the batch alone
-// fills the GPU). For every panel of NB columns:
-//   * rank 0 stages the panel (rows k0..m-1) in shared memory, factors it with
-//     unblocked Householder steps (one CTA reduction for the norm, one for all
-//     dots of the step) and builds the compact-WY factor T (LAPACK dlarft,
-//     forward/columnwise), then writes the reflectors back in place (v0 on the
-//     diagonal, R's diagonal to job.diag);
-//   * every CTA of the cluster loads V and T into its own shared memory and
-//     updates its share of the trailing column tiles, C -= V (T^T (V^T C)), one
-//     warp per tile of 4 columns with register accumulators and V read from
-//     shared memory.
-// The reflector convention is the reference's: alpha = -sign(x0) ||x||,
-// v = x - alpha e1, beta = 2 / ||v||^2, beta = 0 for a zero column. NB is a
-// template parameter chosen from the matrix height so the panel fits in smem.
+// One CTA per matrix (a thread-block cluster per matrix when the batch is too
+// small to fill the GPU). For every panel of NB columns:
+//   * rank 0 stages the panel's active rows in shared memory and factors it with
+//     unblocked Householder steps. Each step needs ONE CTA reduction: the norm of
+//     x, the dots x^T a_j with the panel columns to the right and x^T V with the
+//     earlier reflectors are reduced together, and the v-dots follow from
+//     v^T y = x^T y - alpha y[0]. The compact-WY factor T (LAPACK dlarft,
+//     forward/columnwise) is built on the fly;
+//   * every CTA of the cluster updates its share of the trailing columns,
+//     C -= V (T^T (V^T C)), one warp per 8-column tile with FP64 tensor-core
+//     MMAs (mma.sync m8n8k4 f64 -> DMMA): V^T C accumulates in the MMA (no
+//     shuffle reductions), T^T W goes through a warp-private smem tile, and
+//     C - V W' is a second MMA pass with C as the accumulator.
+//
+// Row sets: a dense job factors rows k0..m-1 at panel k0. A "stacked" job
+// (split > 0) is [R_a; R_b] with R_a an n x n upper triangle in rows [0, split)
+// and R_b upper trapezoidal in rows [split, m): the reflector of column k only
+// involves top row k and bottom rows 0..k, so panel k0 works on the top rows
+// [k0, k0+nb) plus bottom rows [0, k0+nb) -- the TSQR combine costs ~2/3 n^3
+// instead of 10/3 n^3 flops, with the same arithmetic as the dense kernel on
+// the rows that are not identically zero.
+//
+// Reflector convention as the reference: alpha = -sign(x0) ||x||, v = x - alpha e1,
+// beta = 2/||v||^2 (= 1/(||x|| (||x|| + |x0|))), beta = 0 for a zero column.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -28,12 +38,19 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 4;
+constexpr int kTileN = 8;  // columns per warp tile (MMA n)
 
 __device__ __forceinline__ double wsum(double x) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
+}
+
+// d (8x8 f64 accumulator fragment: 2 per lane) += a (8x4, 1 per lane) * b (4x8, 1 per lane)
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
 }
 
 // CTA-wide sums of the first n of N per-thread values -> s_out[0..n)
@@ -57,8 +74,15 @@ __device__ __forceinline__ void block_sums(const double (&v)[N], int n, double* 
   __syncthreads();
 }
 
+struct Rows {  // local row i of the panel at k0 -> global row
+  uint32_t top_cnt, top_base, bot_base;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const {
+    return i < top_cnt ? top_base + i : bot_base + (i - top_cnt);
+  }
+};
+
 template <int NB>
-__global__ void __launch_bounds__(kThreads, 1) qr_kernel(const QrJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kThreads, 2) qr_kernel(const QrJob* __restrict__ jobs, uint32_t ldp) {
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
@@ -66,14 +90,16 @@ __global__ void __launch_bounds__(kThreads, 1) qr_kernel(const QrJob* __restrict
   double* __restrict__ A = job.a;
   const uint64_t lda = job.lda;
   const int m = (int)job.m, n = (int)job.n;
-  const int K = m < n ? m : n;
+  const int split = (int)job.split;
+  const int K = split ? n : (m < n ? m : n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  double* P = sm;                        // NB x m, column-major (ld m); local row i = global row k0+i
-  double* sT = P + (size_t)NB * m;       // NB x NB, T(r, c) at r * NB + c
+  double* P = sm;                        // NB x ldp, column-major: local row i of panel column q at q * ldp + i
+  double* sT = P + (size_t)NB * ldp;     // NB x NB, T(r, c) at r * NB + c
   double* s_part = sT + NB * NB;         // kWarps x NB
   double* s_red = s_part + kWarps * NB;  // NB
-  __shared__ double s_beta;
+  double* s_w = s_red + NB;              // kWarps x (NB x 8): per-warp W' tiles
+  __shared__ double s_alpha, s_beta;
 
   auto csync = [&]() {
     if (csize > 1) cluster.sync();
@@ -82,71 +108,84 @@ __global__ void __launch_bounds__(kThreads, 1) qr_kernel(const QrJob* __restrict
 
   for (int k0 = 0; k0 < K; k0 += NB) {
     const int nbk = min(NB, K - k0);
-    const int h = m - k0;
+    Rows R;
+    int h;
+    if (split) {
+      const int hb = min(k0 + nbk, m - split);
+      R = {(uint32_t)nbk, (uint32_t)k0, (uint32_t)split};
+      h = nbk + hb;
+    } else {
+      R = {(uint32_t)(m - k0), (uint32_t)k0, 0u};
+      h = m - k0;
+    }
     double* tglob = job.tmat + (uint64_t)(k0 / NB) * NB * NB;
     if (rank == 0) {
       for (int q = 0; q < nbk; ++q) {
-        const double* src = A + (uint64_t)(k0 + q) * lda + k0;
-        for (int i = tid; i < h; i += kThreads) P[q * m + i] = __ldcg(src + i);
+        const double* src = A + (uint64_t)(k0 + q) * lda;
+        for (int i = tid; i < h; i += kThreads) P[q * ldp + i] = __ldcg(src + R(i));
       }
       for (int t = tid; t < NB * NB; t += kThreads) sT[t] = 0.0;
       __syncthreads();
       for (int jj = 0; jj < nbk; ++jj) {
-        double* pj = P + jj * m;
-        double nrm[1] = {0.0};
-        for (int i = jj + tid; i < h; i += kThreads) nrm[0] += pj[i] * pj[i];
-        block_sums<1>(nrm, 1, s_part, s_red);
-        if (tid == 0) {
-          const double norm2 = s_red[0];
-          double beta = 0.0, alpha = 0.0;
-          if (norm2 > 0.0) {
-            const double norm = sqrt(norm2);
-            const double x0 = pj[jj];
-            alpha = x0 >= 0.0 ? -norm : norm;
-            beta = 2.0 / (2.0 * norm * (norm + fabs(x0)));  // ||x - alpha e1||^2 = 2 norm (norm + |x0|)
-            pj[jj] = x0 - alpha;
-          } else {
-            pj[jj] = 0.0;  // identity reflector
-          }
-          job.diag[k0 + jj] = alpha;
-          job.beta[k0 + jj] = beta;
-          s_beta = beta;
-        }
-        __syncthreads();
-        const double beta = s_beta;
-        if (beta == 0.0) continue;
-        // dots with the panel columns to the right and with the earlier reflectors (for T)
-        const int n_after = nbk - 1 - jj, n_vals = nbk - 1;
+        double* pj = P + jj * ldp;
+        const int n_after = nbk - 1 - jj;
+        // x^T x, x^T a_{jj+1..}, x^T v_{0..jj-1} over local rows >= jj
         double acc[NB];
 #pragma unroll
         for (int q = 0; q < NB; ++q) acc[q] = 0.0;
         for (int i = jj + tid; i < h; i += kThreads) {
-          const double vi = pj[i];
+          const double xi = pj[i];
+          acc[0] += xi * xi;
 #pragma unroll
-          for (int q = 0; q < NB; ++q) {
-            if (q < n_after) acc[q] += vi * P[(jj + 1 + q) * m + i];
-            else if (q < n_vals) acc[q] += vi * P[(q - n_after) * m + i];
+          for (int q = 1; q < NB; ++q) {
+            if (q <= n_after) acc[q] += xi * P[(jj + q) * ldp + i];
+            else if (q < nbk) acc[q] += xi * P[(q - 1 - n_after) * ldp + i];
           }
         }
-        block_sums<NB>(acc, n_vals, s_part, s_red);
+        block_sums<NB>(acc, nbk, s_part, s_red);
+        if (tid == 0) {
+          const double norm2 = s_red[0];
+          double beta = 0.0, alpha = 0.0;
+          const double x0 = pj[jj];
+          if (norm2 > 0.0) {
+            const double norm = sqrt(norm2);
+            alpha = x0 >= 0.0 ? -norm : norm;
+            beta = 1.0 / (norm * (norm + fabs(x0)));
+            pj[jj] = x0 - alpha;
+          }
+          job.diag[k0 + jj] = alpha;
+          job.beta[k0 + jj] = beta;
+          s_alpha = alpha;
+          s_beta = beta;
+        }
+        __syncthreads();
+        const double beta = s_beta, alpha = s_alpha;
+        if (beta == 0.0) continue;  // identity reflector, v = 0 (the column is zero from row jj)
+        // w_q = v^T a = x^T a - alpha a[jj]; z_r = v^T v_r = x^T v_r - alpha v_r[jj]
+        if (tid < n_after) s_part[tid] = s_red[1 + tid] - alpha * P[(jj + 1 + tid) * ldp + jj];
+        if (tid >= NB && tid < NB + jj) {
+          const int r = tid - NB;
+          s_part[NB + r] = s_red[1 + n_after + r] - alpha * P[r * ldp + jj];
+        }
+        __syncthreads();
         for (int i = jj + tid; i < h; i += kThreads) {
           const double vi = pj[i];
-          for (int q = 0; q < n_after; ++q) P[(jj + 1 + q) * m + i] -= beta * s_red[q] * vi;
+          for (int q = 0; q < n_after; ++q) P[(jj + 1 + q) * ldp + i] -= beta * s_part[q] * vi;
         }
         // T(0:jj, jj) = -beta T(0:jj, 0:jj) z, T(jj, jj) = beta
         if (tid < jj) {
           double t = 0.0;
-          for (int s = tid; s < jj; ++s) t += sT[tid * NB + s] * s_red[n_after + s];
-          s_part[tid] = -beta * t;
+          for (int s = tid; s < jj; ++s) t += sT[tid * NB + s] * s_part[NB + s];
+          s_red[tid] = -beta * t;
         }
         __syncthreads();
-        if (tid < jj) sT[tid * NB + jj] = s_part[tid];
+        if (tid < jj) sT[tid * NB + jj] = s_red[tid];
         if (tid == 0) sT[jj * NB + jj] = beta;
         __syncthreads();
       }
       for (int q = 0; q < nbk; ++q) {
-        double* dst = A + (uint64_t)(k0 + q) * lda + k0;
-        for (int i = tid; i < h; i += kThreads) dst[i] = P[q * m + i];
+        double* dst = A + (uint64_t)(k0 + q) * lda;
+        for (int i = tid; i < h; i += kThreads) dst[R(i)] = P[q * ldp + i];
       }
       if (csize > 1)
         for (int t = tid; t < NB * NB; t += kThreads) tglob[t] = sT[t];
@@ -154,98 +193,137 @@ __global__ void __launch_bounds__(kThreads, 1) qr_kernel(const QrJob* __restrict
     csync();
     if (rank != 0) {
       for (int q = 0; q < nbk; ++q) {
-        const double* src = A + (uint64_t)(k0 + q) * lda + k0;
-        for (int i = tid; i < h; i += kThreads) P[q * m + i] = __ldcg(src + i);
+        const double* src = A + (uint64_t)(k0 + q) * lda;
+        for (int i = tid; i < h; i += kThreads) P[q * ldp + i] = __ldcg(src + R(i));
       }
       for (int t = tid; t < NB * NB; t += kThreads) sT[t] = __ldcg(tglob + t);
       __syncthreads();
     }
-    // ---- trailing update: C = C - V (T^T (V^T C)) on columns >= k0 + nbk ----
+    // ---- trailing update on columns >= k0 + nbk, one warp per 8-column tile ----
     const int c0 = k0 + nbk;
-    const int ntiles = (n - c0 + kTile - 1) / kTile;
+    const int ntiles = (n - c0 + kTileN - 1) / kTileN;
+    double* wt = s_w + warp * (NB * 8);
+    const int lr = lane >> 2, lc = lane & 3;  // fragment coordinates
     for (int tile = rank * kWarps + warp; tile < ntiles; tile += csize * kWarps) {
-      const int j0 = c0 + tile * kTile;
-      double acc[NB][kTile];
+      const int j0 = c0 + tile * kTileN;
+      // pass 1: W = V^T C (NB x 8), k = rows
+      const int jb = j0 + lr;  // B fragment column
+      const bool jb_ok = jb < n;
+      const double* cb = A + (uint64_t)(jb_ok ? jb : n - 1) * lda;
+      double w[(NB + 7) / 8][2];
 #pragma unroll
-      for (int r = 0; r < NB; ++r)
+      for (int hh = 0; hh < (NB + 7) / 8; ++hh) w[hh][0] = w[hh][1] = 0.0;
+      for (int i0 = 0; i0 < h; i0 += 4) {
+        const int i = i0 + lc;
+        const double bv = (jb_ok && i < h) ? __ldcg(cb + R(i)) : 0.0;
 #pragma unroll
-        for (int q = 0; q < kTile; ++q) acc[r][q] = 0.0;
-      double* cb[kTile];
-#pragma unroll
-      for (int q = 0; q < kTile; ++q) cb[q] = A + (uint64_t)min(j0 + q, n - 1) * lda + k0;
-      for (int i = lane; i < h; i += 32) {
-        double c[kTile];
-#pragma unroll
-        for (int q = 0; q < kTile; ++q) c[q] = (j0 + q < n) ? __ldcg(cb[q] + i) : 0.0;
-#pragma unroll
-        for (int r = 0; r < NB; ++r) {
-          const double vr = (r < nbk && i >= r) ? P[r * m + i] : 0.0;
-#pragma unroll
-          for (int q = 0; q < kTile; ++q) acc[r][q] += vr * c[q];
+        for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
+          const int r = hh * 8 + lr;
+          const double av = (r < nbk && i >= r && i < h) ? P[r * ldp + i] : 0.0;
+          dmma(w[hh][0], w[hh][1], av, bv);
         }
       }
+      // W -> smem (row r = hh*8 + lr, cols 2lc, 2lc+1), then W' = -(T^T W) in place
 #pragma unroll
-      for (int r = 0; r < NB; ++r)
-#pragma unroll
-        for (int q = 0; q < kTile; ++q) acc[r][q] = wsum(acc[r][q]);
-#pragma unroll
-      for (int r = NB - 1; r >= 0; --r) {
-#pragma unroll
-        for (int q = 0; q < kTile; ++q) {
-          double t = 0.0;
-#pragma unroll
-          for (int s = 0; s <= r; ++s) t += sT[s * NB + r] * acc[s][q];
-          acc[r][q] = t;
+      for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
+        const int r = hh * 8 + lr;
+        if (r < NB) {
+          wt[r * 8 + 2 * lc] = w[hh][0];
+          wt[r * 8 + 2 * lc + 1] = w[hh][1];
         }
       }
-      for (int i = lane; i < h; i += 32) {
-        double c[kTile];
+      __syncwarp();
+      double wn[(NB * 8 + 31) / 32];
 #pragma unroll
-        for (int q = 0; q < kTile; ++q) c[q] = (j0 + q < n) ? __ldcg(cb[q] + i) : 0.0;
-#pragma unroll
-        for (int r = 0; r < NB; ++r) {
-          const double vr = (r < nbk && i >= r) ? P[r * m + i] : 0.0;
-#pragma unroll
-          for (int q = 0; q < kTile; ++q) c[q] -= vr * acc[r][q];
+      for (int e = 0; e < (NB * 8 + 31) / 32; ++e) {
+        const int idx = e * 32 + lane;
+        double t = 0.0;
+        if (idx < NB * 8) {
+          const int r = idx >> 3, q = idx & 7;
+          for (int s = 0; s <= r; ++s) t += sT[s * NB + r] * wt[s * 8 + q];
         }
-#pragma unroll
-        for (int q = 0; q < kTile; ++q)
-          if (j0 + q < n) cb[q][i] = c[q];
+        wn[e] = -t;
       }
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < (NB * 8 + 31) / 32; ++e) {
+        const int idx = e * 32 + lane;
+        if (idx < NB * 8) wt[idx] = wn[e];
+      }
+      __syncwarp();
+      // pass 2: C(8 rows x 8 cols) += V(8 x NB) * (-W'), accumulator = C
+      const int ja = j0 + 2 * lc;
+      double* ca0 = A + (uint64_t)min(ja, n - 1) * lda;
+      double* ca1 = A + (uint64_t)min(ja + 1, n - 1) * lda;
+      for (int i0 = 0; i0 < h; i0 += 8) {
+        const int i = i0 + lr;
+        const bool row_ok = i < h;
+        const uint32_t gi = row_ok ? R(i) : 0u;
+        double d0 = (row_ok && ja < n) ? __ldcg(ca0 + gi) : 0.0;
+        double d1 = (row_ok && ja + 1 < n) ? __ldcg(ca1 + gi) : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NB; kk += 4) {
+          const int r = kk + lc;
+          const double av = (r < nbk && row_ok && i >= r) ? P[r * ldp + i] : 0.0;
+          const double bv = wt[(kk + lc) * 8 + lr];
+          dmma(d0, d1, av, bv);
+        }
+        if (row_ok) {
+          if (ja < n) ca0[gi] = d0;
+          if (ja + 1 < n) ca1[gi] = d1;
+        }
+      }
+      __syncwarp();
     }
     csync();
   }
 }
 
-template <int NB>
-size_t qr_smem(uint32_t m) {
-  return ((size_t)NB * m + NB * NB + kWarps * NB + NB) * sizeof(double);
+uint32_t panel_ld(uint32_t h) {
+  // >= h, == 4 mod 16: the 8 reflectors x 4 rows of an MMA A fragment hit distinct bank pairs
+  uint32_t ld = (h + 15) / 16 * 16 + 4;
+  return ld;
 }
 
 template <int NB>
-void launch_qr(const std::vector<QrJob>& jobs, const QrJob* d_jobs, unsigned cl, uint32_t m_max, cudaStream_t s) {
-  const size_t smem = qr_smem<NB>(m_max);
+size_t qr_smem(uint32_t h_max) {
+  return ((size_t)NB * panel_ld(h_max) + NB * NB + kWarps * NB + NB + kWarps * NB * 8) * sizeof(double);
+}
+
+template <int NB>
+void launch_qr(const std::vector<QrJob>& jobs, const QrJob* d_jobs, unsigned cl, uint32_t h_max, cudaStream_t s) {
+  const size_t smem = qr_smem<NB>(h_max);
+  uint32_t ldp = panel_ld(h_max);
   RK_CUDA_CHECK(cudaFuncSetAttribute(qr_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   RK_CUDA_CHECK(cudaFuncSetAttribute(qr_kernel<NB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  const void* args[] = {&d_jobs};
-  launch_cluster_kernel((const void*)qr_kernel<NB>, (unsigned)jobs.size() * cl, cl, kThreads, smem, s,
-                        const_cast<void**>(args));
+  RK_CUDA_CHECK(cudaFuncSetAttribute(qr_kernel<NB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  void* args[] = {(void*)&d_jobs, (void*)&ldp};
+  launch_cluster_kernel((const void*)qr_kernel<NB>, (unsigned)jobs.size() * cl, cl, kThreads, smem, s, args);
 }
 
 }  // namespace
 
-uint32_t qr_max_rows() { return 5120; }
+uint32_t qr_max_rows() { return 6144; }
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   if (jobs.empty()) return;
-  uint32_t m_max = 0, widest = 0;
+  uint32_t h_max = 0, widest = 0;
   for (const QrJob& j : jobs) {
-    m_max = std::max(m_max, j.m);
+    // active panel rows: dense m - k0 <= m; stacked <= nb + (m - split)
+    const uint32_t h = j.split ? std::min<uint32_t>(j.m, (j.m - j.split) + 16) : j.m;
+    h_max = std::max(h_max, h);
     widest = std::max(widest, j.n);
   }
-  if (m_max > qr_max_rows()) fail(RK_RUNTIME, "qr_batched: matrix taller than a panel can stage");
-  unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)(2 * sms) / jobs.size());
-  const unsigned useful = std::max(1u, (widest / kTile + kWarps - 1) / kWarps);
+  if (h_max > qr_max_rows()) fail(RK_RUNTIME, "qr_batched: matrix taller than a panel can stage");
+  const size_t budget = 200 * 1024;
+  int nb = 16;
+  if (qr_smem<16>(h_max) > budget) nb = qr_smem<8>(h_max) <= budget ? 8 : 4;
+  const size_t smem = nb == 16 ? qr_smem<16>(h_max) : nb == 8 ? qr_smem<8>(h_max) : qr_smem<4>(h_max);
+  // one CTA per matrix while the batch fills the GPU (other CTAs on the SM hide the
+  // panel latency); clusters split the trailing update of small batches
+  const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 2048)));
+  unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)sms * per_sm / jobs.size());
+  const unsigned useful = std::max(1u, (widest / kTileN + kWarps - 1) / kWarps);
   cl = std::min({cl, 8u, useful});
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
@@ -253,10 +331,9 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   DBuf<QrJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   const QrJob* d = dj.get();
-  const size_t budget = 200 * 1024;
-  if (qr_smem<16>(m_max) <= budget) launch_qr<16>(jobs, d, cl, m_max, s);
-  else if (qr_smem<8>(m_max) <= budget) launch_qr<8>(jobs, d, cl, m_max, s);
-  else launch_qr<4>(jobs, d, cl, m_max, s);
+  if (nb == 16) launch_qr<16>(jobs, d, cl, h_max, s);
+  else if (nb == 8) launch_qr<8>(jobs, d, cl, h_max, s);
+  else launch_qr<4>(jobs, d, cl, h_max, s);
 }
 
 }  // namespace rk
