@@ -1,0 +1,329 @@
+// rk_gram.cu -- Gram + Cholesky route to the triangular factor R of a block.
+//
+// For A_d^T = Q R the factor R is, up to row signs, the Cholesky factor of the
+// Gram G_d = A_d A_d^T (exact arithmetic). The Jacobi stage needs W = R^T = L
+// (lower triangular), so the block factorization becomes
+//     G_d = A_d A_d^T   (sparse: entry (r, s) is the dot of CSR rows r and s
+//                        restricted to the block's columns, summed in ascending
+//                        column order -- deterministic)
+//     L = chol(G_d)     (blocked right-looking, DMMA SYRK trailing updates)
+// at O(M^3/3) flops instead of the 2 n_d M^2 of Householder on the densified
+// block. Cholesky squares the condition number, so the result is accepted only
+// when the block's kappa = sigma_max/sigma_min is small enough that the Gram's
+// rounding (~ M eps sigma_max^2) moves every singular value by less than
+// 1e-11 relative (kappa_max(M) = sqrt(2e-11 / (M eps))); otherwise -- and for a
+// non-positive pivot -- the block is redone on the Householder path. The same
+// kernels give the merge's R_P from P P^T (SYRK over the records).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "rk_internal.cuh"
+
+namespace rk {
+namespace {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// one thread per (block, r >= s) pair: G[r + s M] = G[s + r M] = sum_c A[r,c] A[s,c]
+__global__ void sparse_gram_kernel(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                                   const double* __restrict__ val, uint32_t M, Partition p, uint64_t d_lo,
+                                   uint64_t nblk, double* __restrict__ G, uint64_t stride) {
+  const uint64_t pairs = (uint64_t)M * (M + 1) / 2;
+  const uint64_t total = pairs * nblk;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t bi = t / pairs, pi = t % pairs;
+    // pi -> (r, s) with r >= s: r = floor((sqrt(8 pi + 1) - 1) / 2)
+    uint32_t r = (uint32_t)((sqrt(8.0 * (double)pi + 1.0) - 1.0) * 0.5);
+    while ((uint64_t)r * (r + 1) / 2 > pi) --r;
+    while ((uint64_t)(r + 1) * (r + 2) / 2 <= pi) ++r;
+    const uint32_t s = (uint32_t)(pi - (uint64_t)r * (r + 1) / 2);
+    const uint64_t d = d_lo + bi;
+    const uint32_t b = (uint32_t)p.begin(d), e = (uint32_t)p.end(d);
+    auto lower = [&](uint64_t lo, uint64_t hi) {
+      while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (col[mid] < b) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    uint64_t i = lower(row_ptr[r], row_ptr[r + 1]), iend = row_ptr[r + 1];
+    uint64_t j = (r == s) ? i : lower(row_ptr[s], row_ptr[s + 1]), jend = row_ptr[s + 1];
+    double acc = 0.0;
+    if (r == s) {
+      for (; i < iend && col[i] < e; ++i) acc += val[i] * val[i];
+    } else {
+      while (i < iend && j < jend) {
+        const uint32_t ci = col[i], cj = col[j];
+        if (ci >= e || cj >= e) break;
+        if (ci == cj) { acc += val[i] * val[j]; ++i; ++j; }
+        else if (ci < cj) ++i;
+        else ++j;
+      }
+    }
+    double* g = G + bi * stride;
+    g[r + (uint64_t)s * M] = acc;
+    g[s + (uint64_t)r * M] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// split-K SYRK over the records: partial[kc][r + s M] = sum_{j in chunk kc} P[r, j] P[s, j]
+// for 8x8 tiles with r-tile >= s-tile. The records are row-major M x k_d pieces.
+struct SyrkChunk {
+  const double* base;  // payload of one record (row-major M x k)
+  uint32_t k;          // columns of this record
+  uint32_t j0, j1;     // column range of this chunk inside the record
+};
+
+__global__ void syrk_records_kernel(const SyrkChunk* __restrict__ chunks, uint32_t n_chunks, uint32_t M,
+                                    double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  const uint32_t tiles = M / 8;
+  const uint64_t n_tile_pairs = (uint64_t)tiles * (tiles + 1) / 2;
+  const uint64_t total = n_tile_pairs * n_chunks;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < total;
+       w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t kc = (uint32_t)(w / n_tile_pairs);
+    const uint64_t tp = w % n_tile_pairs;
+    uint32_t ti = (uint32_t)((sqrt(8.0 * (double)tp + 1.0) - 1.0) * 0.5);
+    while ((uint64_t)ti * (ti + 1) / 2 > tp) --ti;
+    while ((uint64_t)(ti + 1) * (ti + 2) / 2 <= tp) ++ti;
+    const uint32_t tj = (uint32_t)(tp - (uint64_t)ti * (ti + 1) / 2);
+    const SyrkChunk c = chunks[kc];
+    double d0 = 0.0, d1 = 0.0;
+    // D(8x8) += A(8 rows of tile i x 4 k) * B(4 k x 8 rows of tile j)
+    const double* pa = c.base + (uint64_t)(ti * 8 + lr) * c.k;  // A[lr][lc] = P[ti*8+lr, j]
+    const double* pb = c.base + (uint64_t)(tj * 8 + lr) * c.k;  // B[lc][lr] = P[tj*8+lr, j]
+#pragma unroll 4
+    for (uint32_t j = c.j0; j < c.j1; j += 4) {
+      const uint32_t jj = j + lc;
+      const double a = jj < c.j1 ? pa[jj] : 0.0;
+      const double b = jj < c.j1 ? pb[jj] : 0.0;
+      dmma(d0, d1, a, b);
+    }
+    double* out = partial + (uint64_t)kc * M * M;
+    // D row = ti*8 + lr, cols tj*8 + 2lc + {0,1}; column-major G(r, s) at r + s M
+    const uint32_t r = ti * 8 + lr, s0 = tj * 8 + 2 * lc;
+    out[r + (uint64_t)s0 * M] = d0;
+    out[r + (uint64_t)(s0 + 1) * M] = d1;
+  }
+}
+
+// G = sum of the partials in chunk order, mirrored to the upper triangle
+__global__ void reduce_partials(const double* __restrict__ partial, uint32_t n_chunks, uint32_t M,
+                                double* __restrict__ G) {
+  const uint64_t total = (uint64_t)M * M;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(t % M), s = (uint32_t)(t / M);
+    if ((r / 8) < (s / 8)) continue;  // only tiles with r-tile >= s-tile were written
+    double acc = 0.0;
+    for (uint32_t k = 0; k < n_chunks; ++k) acc += partial[(uint64_t)k * total + t];
+    G[t] = acc;
+    G[s + (uint64_t)r * M] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// blocked right-looking Cholesky, one CTA per matrix, in place on the lower
+// triangle (column-major, ld M). On exit the strict upper triangle is zeroed so
+// the matrix is W = L. status[i]: 0 ok, 1 non-positive pivot.
+
+constexpr int kCT = 256;
+constexpr int kCB = 32;  // panel width
+
+__global__ void __launch_bounds__(kCT, 2) cholesky_kernel(double* const* __restrict__ mats, uint32_t M,
+                                                          uint32_t* __restrict__ status,
+                                                          double* __restrict__ diag_ratio) {
+  extern __shared__ __align__(16) double sm[];
+  double* D = sm;                   // kCB x kCB diagonal block (column-major)
+  double* Lp = D + kCB * kCB;       // (M) x kCB panel rows below the diagonal block (column-major, ld M)
+  __shared__ int s_bad;
+  __shared__ double s_dmin, s_dmax;
+  double* A = mats[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { s_bad = 0; s_dmin = INFINITY; s_dmax = 0.0; }
+  __syncthreads();
+  for (uint32_t k0 = 0; k0 < M; k0 += kCB) {
+    const uint32_t nb = min((uint32_t)kCB, M - k0);
+    // 1. factor the diagonal block (one warp, column by column)
+    for (uint32_t t = tid; t < nb * nb; t += kCT) {
+      const uint32_t i = t % nb, j = t / nb;
+      D[i + j * kCB] = (i >= j) ? __ldcg(A + (k0 + i) + (uint64_t)(k0 + j) * M) : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (uint32_t j = 0; j < nb; ++j) {
+        double piv = D[j + j * kCB];
+        if (!(piv > 0.0)) {
+          if (lane == 0) s_bad = 1;
+          piv = 1.0;
+        }
+        const double ljj = sqrt(piv);
+        __syncwarp();
+        if (lane == 0) {
+          D[j + j * kCB] = ljj;
+          s_dmin = fmin(s_dmin, ljj);
+          s_dmax = fmax(s_dmax, ljj);
+        }
+        __syncwarp();
+        const double inv = 1.0 / ljj;
+        for (uint32_t i = j + 1 + lane; i < nb; i += 32) D[i + j * kCB] *= inv;
+        __syncwarp();
+        // rank-1 update of the remaining lower part of D
+        for (uint32_t c = j + 1; c < nb; ++c) {
+          const double lcj = D[c + j * kCB];
+          for (uint32_t i = c + lane; i < nb; i += 32) D[i + c * kCB] -= D[i + j * kCB] * lcj;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+    // write the factored diagonal block back (zero above)
+    for (uint32_t t = tid; t < nb * nb; t += kCT) {
+      const uint32_t i = t % nb, j = t / nb;
+      A[(k0 + i) + (uint64_t)(k0 + j) * M] = (i >= j) ? D[i + j * kCB] : 0.0;
+    }
+    // 2. panel below: L21 = A21 L11^{-T}; row-wise forward substitution (thread per row)
+    const uint32_t below = M - k0 - nb;
+    for (uint32_t rr = tid; rr < below; rr += kCT) {
+      const uint32_t i = k0 + nb + rr;
+      double x[kCB];
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) x[j] = (j < (int)nb) ? __ldcg(A + i + (uint64_t)(k0 + j) * M) : 0.0;
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) {
+        if (j < (int)nb) {
+          double v = x[j];
+          for (int q = 0; q < j; ++q) v -= x[q] * D[j + q * kCB];
+          x[j] = v / D[j + j * kCB];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCB; ++j)
+        if (j < (int)nb) {
+          A[i + (uint64_t)(k0 + j) * M] = x[j];
+          Lp[rr + (uint64_t)j * M] = x[j];
+        }
+    }
+    __syncthreads();
+    // 3. trailing SYRK: A22 -= L21 L21^T on 8x8 tiles of the lower triangle (DMMA)
+    const uint32_t nt = (below + 7) / 8;
+    const uint64_t ntp = (uint64_t)nt * (nt + 1) / 2;
+    const int lr = lane >> 2, lc = lane & 3;
+    for (uint64_t tp = warp; tp < ntp; tp += kCT / 32) {
+      uint32_t ti = (uint32_t)((sqrt(8.0 * (double)tp + 1.0) - 1.0) * 0.5);
+      while ((uint64_t)ti * (ti + 1) / 2 > tp) --ti;
+      while ((uint64_t)(ti + 1) * (ti + 2) / 2 <= tp) ++ti;
+      const uint32_t tj = (uint32_t)(tp - (uint64_t)ti * (ti + 1) / 2);
+      const uint32_t ra = ti * 8 + lr;       // A fragment row (local)
+      const uint32_t sb = tj * 8 + lr;       // B fragment column (local)
+      const uint32_t r = ti * 8 + lr, s0 = tj * 8 + 2 * lc;  // D fragment
+      double* c0p = A + (k0 + nb + r) + (uint64_t)(k0 + nb + s0) * M;
+      const bool rok = r < below;
+      double d0 = (rok && s0 < below) ? -__ldcg(c0p) : 0.0;
+      double d1 = (rok && s0 + 1 < below) ? -__ldcg(c0p + M) : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < kCB; kk += 4) {
+        const int q = kk + lc;
+        const double a = (ra < below && q < (int)nb) ? Lp[ra + (uint64_t)q * M] : 0.0;
+        const double b = (sb < below && q < (int)nb) ? Lp[sb + (uint64_t)q * M] : 0.0;
+        dmma(d0, d1, a, b);  // accumulates -C + L L^T
+      }
+      if (rok && s0 < below) *c0p = -d0;
+      if (rok && s0 + 1 < below) c0p[M] = -d1;
+    }
+    __syncthreads();
+  }
+  // zero the strict upper triangle: W = L
+  if (!s_bad)
+    for (uint64_t t = tid; t < (uint64_t)M * M; t += kCT) {
+      const uint32_t i = (uint32_t)(t % M), j = (uint32_t)(t / M);
+      if (i < j) A[t] = 0.0;
+    }
+  if (tid == 0) {
+    status[blockIdx.x] = s_bad ? 1u : 0u;
+    diag_ratio[blockIdx.x] = s_bad ? INFINITY : s_dmax / s_dmin;
+  }
+}
+
+unsigned grid_for(uint64_t n, unsigned cap = 1u << 20) {
+  uint64_t g = ceil_div(n, 256);
+  if (g == 0) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+void sparse_gram(const DevCsr& a, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
+                 cudaStream_t s) {
+  const uint32_t M = (uint32_t)a.rows;
+  const uint64_t total = (uint64_t)M * (M + 1) / 2 * nblk;
+  if (!total) return;
+  sparse_gram_kernel<<<grid_for(total), 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), M, p, d_lo, nblk, G,
+                                                     stride);
+  RK_LAUNCH_CHECK();
+}
+
+void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
+                  uint32_t M, double* G, cudaStream_t s) {
+  if (M % 8) fail(RK_RUNTIME, "records_gram: M must be a multiple of 8");
+  std::vector<SyrkChunk> ch;
+  for (size_t d = 0; d < kept.size(); ++d) {
+    if (!kept[d]) continue;
+    for (uint32_t j0 = 0; j0 < kept[d]; j0 += 256)
+      ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + 256)});
+  }
+  if (ch.empty()) {
+    RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * M * M, s));
+    return;
+  }
+  DBuf<SyrkChunk> dch(ch.size(), s);
+  to_device(dch.get(), ch.data(), ch.size(), s);
+  DBuf<double> partial(ch.size() * (uint64_t)M * M, s);
+  const uint64_t tiles = M / 8;
+  const uint64_t warps = tiles * (tiles + 1) / 2 * ch.size();
+  syrk_records_kernel<<<grid_for(warps * 32), 256, 0, s>>>(dch.get(), (uint32_t)ch.size(), M, partial.get());
+  RK_LAUNCH_CHECK();
+  RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * M * M, s));
+  reduce_partials<<<grid_for((uint64_t)M * M), 256, 0, s>>>(partial.get(), (uint32_t)ch.size(), M, G);
+  RK_LAUNCH_CHECK();
+  sync(s);  // host chunk list
+}
+
+void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
+                      cudaStream_t s) {
+  if (!n_mats) return;
+  const size_t smem = ((size_t)kCB * kCB + (size_t)M * kCB) * sizeof(double);
+  if (smem > 200 * 1024) fail(RK_RUNTIME, "cholesky_batched: M too large for the panel buffer");
+  RK_CUDA_CHECK(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RK_CUDA_CHECK(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  cholesky_kernel<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
+  RK_LAUNCH_CHECK();
+}
+
+uint32_t cholesky_max_rows() { return 640; }  // the panel buffer (M x 32 doubles) must fit shared memory
+
+bool gram_route_enabled() {
+  const char* e = std::getenv("RK_BLOCK_ROUTE");
+  return !(e && std::string(e) == "householder");
+}
+
+double kappa_max(uint32_t M) {
+  // every sigma moves by < 1e-11 relative when M eps kappa^2 / 2 < 1e-11
+  const double eps = 1.1102230246251565e-16;
+  return sqrt(2e-11 / ((double)std::max<uint32_t>(M, 1) * eps));
+}
+
+}  // namespace rk

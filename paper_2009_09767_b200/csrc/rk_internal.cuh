@@ -211,7 +211,7 @@ struct Ctx {
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   uint64_t launches = 0;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[12] = {};  // [0..3] block stage, [3..7] pipeline stages, [8..11] spare
 };
 
 // RAII: activates the context's device and launch counter for one API call

@@ -258,28 +258,149 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   out.payload.alloc(total_payload ? total_payload : 1, s);
   if (M == 0) return;
 
-  // compaction plan
+  const uint32_t cols_pad_full = jacobi_cols_pad(M, M, false, c.smem_optin);
+  std::vector<char> done(nblk, 0);
+  for (uint64_t i = 0; i < nblk; ++i) done[i] = skip[i];
+
+  // Jacobi + finalize of a set of W slots; records stats and writes payloads
+  auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
+                             bool tall_flops_from_plans, double* sigma_all /* nullable: slots x cols_pad */) {
+    const size_t nb = slots.size();
+    DBuf<double> alpha((uint64_t)nb * cols_pad_full, s);
+    DBuf<uint64_t> stats(8 * nb, s);
+    DBuf<uint32_t> order((uint64_t)nb * cols_pad_full, s);
+    DBuf<double> fscratch((uint64_t)nb * cols_pad_full, s);
+    stats.zero();
+    std::vector<JacobiJob> jj(nb);
+    for (size_t q = 0; q < nb; ++q) {
+      jj[q].w = slots[q];
+      jj[q].v = nullptr;
+      jj[q].rows = M;
+      jj[q].cols = std::max<uint32_t>(cols[q], 1);
+      jj[q].cols_pad = cols_pad_full;
+      jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad_full;
+      jj[q].stats = stats.get() + 8 * q;
+    }
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
+    jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
+    std::vector<FinalJob> fj(nb);
+    for (size_t q = 0; q < nb; ++q) {
+      const uint64_t i = blocks[q];
+      FinalJob& f = fj[q];
+      std::memset(&f, 0, sizeof f);
+      f.w = slots[q];
+      f.rows = M;
+      f.cols = cols_pad_full;
+      f.k = out.kept[i];
+      f.payload = out.payload.get() + out.offset[i];
+      f.order = order.get() + (uint64_t)q * cols_pad_full;
+      f.scratch = fscratch.get() + (uint64_t)q * cols_pad_full;
+      f.sigma_all = sigma_all ? sigma_all + (uint64_t)q * cols_pad_full : nullptr;
+      if (api) {
+        f.u = api->u.get() + out.offset[i];
+        f.sigma = api->sigma.get() + i * (uint64_t)M;
+        f.deficient = api->deficient.get() + i * (uint64_t)M;
+      }
+    }
+    finalize_batched(fj, s);
+    std::vector<JacobiStats> js = read_stats(stats.get(), nb, s);  // synchronizes
+    float ms_j = 0;
+    cudaEventElapsedTime(&ms_j, c.ev[9], c.ev[10]);
+    out.jacobi_ms += ms_j;
+    (void)tall_flops_from_plans;
+    for (size_t q = 0; q < nb; ++q) {
+      out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
+      out.sweeps_sum += js[q].sweeps;
+      out.rotations += js[q].rotations;
+      const double cA = cols[q], Md = M;
+      out.jacobi_flops += (double)js[q].sweeps * (cA * (cA - 1) / 2 * 2 * Md + 2 * Md * cA) +
+                          (double)js[q].rotations * 6 * Md;
+      if (js[q].failed) {
+        out.failures[blocks[q]] = "one-sided Jacobi did not converge (residual " + residual_text(js[q].residual) + ")";
+        out.conv_residual = js[q].residual;
+      }
+    }
+    return js;
+  };
+
+  size_t free_b = 0, total_b = 0;
+  RK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t budget = std::max<uint64_t>((uint64_t)(free_b * 0.4), 256ull << 20);
+
+  // ---- route 1: W = chol(A_d A_d^T), accepted when kappa <= kappa_max(M) ----
+  if (gram_route_enabled() && M <= cholesky_max_rows()) {
+    const double kmax = kappa_max(M);
+    const uint64_t per_block = (uint64_t)M * cols_pad_full * 8 * 2;
+    const uint64_t chunk = std::max<uint64_t>(1, budget / per_block);
+    for (uint64_t i0 = 0; i0 < nblk; i0 += chunk) {
+      const uint64_t i1 = std::min(nblk, i0 + chunk), nb = i1 - i0;
+      DBuf<double> W(nb * M * cols_pad_full, s);
+      W.zero();
+      RK_CUDA_CHECK(cudaEventRecord(c.ev[8], s));
+      sparse_gram(a.csr, p, d_lo + i0, nb, W.get(), (uint64_t)M * cols_pad_full, s);
+      std::vector<double*> ptrs(nb);
+      for (uint64_t q = 0; q < nb; ++q) ptrs[q] = W.get() + q * M * cols_pad_full;
+      DBuf<double*> dptrs(nb, s);
+      DBuf<uint32_t> status(nb, s);
+      DBuf<double> ratio(nb, s);
+      to_device(dptrs.get(), ptrs.data(), nb, s);
+      cholesky_batched(dptrs.get(), (uint32_t)nb, M, status.get(), ratio.get(), s);
+      RK_CUDA_CHECK(cudaEventRecord(c.ev[11], s));
+      std::vector<uint32_t> hst;
+      std::vector<double> hrat;
+      to_host(hst, status.get(), nb, s);
+      to_host(hrat, ratio.get(), nb, s);
+      sync(s);
+      float ms_g = 0;
+      cudaEventElapsedTime(&ms_g, c.ev[8], c.ev[11]);
+      out.qr_ms += ms_g;
+      out.qr_flops += (double)nb * M * (double)M * M / 3.0;
+      std::vector<double*> slots;
+      std::vector<uint32_t> cols;
+      std::vector<uint64_t> blocks;
+      for (uint64_t q = 0; q < nb; ++q) {
+        const uint64_t i = i0 + q;
+        if (skip[i] || hst[q] != 0 || !(hrat[q] <= kmax)) continue;
+        slots.push_back(ptrs[q]);
+        cols.push_back(M);
+        blocks.push_back(i);
+      }
+      if (slots.empty()) continue;
+      DBuf<double> sig((uint64_t)slots.size() * cols_pad_full, s);
+      jacobi_finalize(slots, cols, blocks, false, sig.get());
+      std::vector<double> hs;
+      to_host(hs, sig.get(), sig.n, s);
+      sync(s);
+      for (size_t q = 0; q < slots.size(); ++q) {
+        const double smax = hs[q * cols_pad_full], smin = hs[q * cols_pad_full + M - 1];
+        const uint64_t i = blocks[q];
+        if (!out.failures[i].empty()) { done[i] = 1; continue; }  // a Jacobi failure is final
+        if (smin > 0.0 && smax / smin <= kmax) done[i] = 1;
+      }
+    }
+  }
+
+  // ---- route 2: Householder (compaction -> TSQR -> W = R^T), as the reference ----
+  std::vector<uint64_t> todo;
+  for (uint64_t i = 0; i < nblk; ++i)
+    if (!done[i]) todo.push_back(i);
+  if (todo.empty()) return;
   DBuf<uint32_t> counts(2 * nblk, s);
   DBuf<double> single(nblk * (uint64_t)M, s);
   compaction_counts(a, p, d_lo, d_hi, counts.get(), single.get(), s);
   std::vector<uint32_t> hc;
   to_host(hc, counts.get(), 2 * nblk, s);
   sync(s);
-
-  size_t free_b = 0, total_b = 0;
-  RK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-  const uint64_t budget = std::max<uint64_t>((uint64_t)(free_b * 0.4), 256ull << 20);
-  const uint32_t cols_pad_full = jacobi_cols_pad(M, M, false, c.smem_optin);
   const uint64_t aux_sz = 2 * (uint64_t)M + (ceil_div(M, 16) + 1) * 256;
 
-  uint64_t i0 = 0;
-  while (i0 < nblk) {
+  size_t t0 = 0;
+  while (t0 < todo.size()) {
     std::vector<BlockPlan> plans;
     uint64_t staging = 0, wdoubles = 0;
-    uint32_t max_cols = 1;
-    uint64_t i1 = i0;
-    for (; i1 < nblk; ++i1) {
-      if (skip[i1]) continue;
+    size_t t1 = t0;
+    for (; t1 < todo.size(); ++t1) {
+      const uint64_t i1 = todo[t1];
       BlockPlan pl;
       pl.block = d_lo + i1;
       pl.n_multi = hc[2 * i1];
@@ -291,23 +412,16 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       pl.offset = staging;
       staging += pl.tall ? (uint64_t)pl.n_rows * M : 0;
       wdoubles += (uint64_t)M * cols_pad_full + aux_sz;
-      max_cols = std::max(max_cols, std::min<uint32_t>(pl.n_rows, M));
       plans.push_back(pl);
     }
-    if (plans.empty()) { i0 = i1; continue; }
     const size_t nb = plans.size();
     // one padded width per M (not per chunk): the Jacobi group layout, and with it
     // the rotation order and rounding, depends only on the block's own data
     const uint32_t cols_pad = cols_pad_full;
     DBuf<double> st(staging ? staging : 1, s);
     DBuf<double> W((uint64_t)nb * M * cols_pad, s);
-    DBuf<double> alpha((uint64_t)nb * cols_pad, s);
-    DBuf<uint64_t> stats(8 * nb, s);
-    DBuf<uint32_t> order((uint64_t)nb * cols_pad, s);
-    DBuf<double> fscratch((uint64_t)nb * cols_pad, s);
     if (staging) st.zero();
     W.zero();
-    stats.zero();
     std::vector<BlockPlan> fill_tall, fill_wide;
     for (size_t q = 0; q < nb; ++q) {
       if (plans[q].tall) {
@@ -318,7 +432,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         fill_wide.push_back(w);
       }
     }
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[0], s));
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[8], s));
     compaction_fill(a, p, fill_tall, d_lo, single.get(), st.get(), s);
     compaction_fill(a, p, fill_wide, d_lo, single.get(), W.get(), s);
     // tall blocks: TSQR of T_d over row leaves of at most kLeafRows rows (factored in
@@ -338,6 +452,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         }
         trees.push_back(std::move(leaves));
         tree_q.push_back(q);
+        out.qr_flops += 2.0 * nr * (double)M * M - 2.0 / 3.0 * (double)M * M * M;
       }
       if (!trees.empty()) {
         std::vector<DBuf<double>> roots;
@@ -349,60 +464,20 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         }
       }
     }
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[1], s));
-    std::vector<JacobiJob> jj(nb);
+    RK_CUDA_CHECK(cudaEventRecord(c.ev[11], s));
+    std::vector<double*> slots(nb);
+    std::vector<uint32_t> cols(nb);
+    std::vector<uint64_t> blocks(nb);
     for (size_t q = 0; q < nb; ++q) {
-      jj[q].w = W.get() + (uint64_t)q * M * cols_pad;
-      jj[q].v = nullptr;
-      jj[q].rows = M;
-      jj[q].cols = std::max<uint32_t>(std::min<uint32_t>(plans[q].n_rows, M), 1);
-      jj[q].cols_pad = cols_pad;
-      jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad;
-      jj[q].stats = stats.get() + 8 * q;
+      slots[q] = W.get() + (uint64_t)q * M * cols_pad;
+      cols[q] = std::min<uint32_t>(plans[q].n_rows, M);
+      blocks[q] = plans[q].block - d_lo;
     }
-    jacobi_batched(jj, s, c.num_sms, c.smem_optin);
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[2], s));
-    std::vector<FinalJob> fj(nb);
-    for (size_t q = 0; q < nb; ++q) {
-      const uint64_t i = plans[q].block - d_lo;
-      FinalJob& f = fj[q];
-      std::memset(&f, 0, sizeof f);
-      f.w = jj[q].w;
-      f.rows = M;
-      f.cols = cols_pad;
-      f.k = out.kept[i];
-      f.payload = out.payload.get() + out.offset[i];
-      f.order = order.get() + (uint64_t)q * cols_pad;
-      f.scratch = fscratch.get() + (uint64_t)q * cols_pad;
-      if (api) {
-        f.u = api->u.get() + out.offset[i];
-        f.sigma = api->sigma.get() + i * (uint64_t)M;
-        f.deficient = api->deficient.get() + i * (uint64_t)M;
-      }
-    }
-    finalize_batched(fj, s);
-    std::vector<JacobiStats> js = read_stats(stats.get(), nb, s);  // synchronizes
-    float ms_qr = 0, ms_j = 0;
-    cudaEventElapsedTime(&ms_qr, c.ev[0], c.ev[1]);
-    cudaEventElapsedTime(&ms_j, c.ev[1], c.ev[2]);
+    jacobi_finalize(slots, cols, blocks, true, nullptr);
+    float ms_qr = 0;
+    cudaEventElapsedTime(&ms_qr, c.ev[8], c.ev[11]);
     out.qr_ms += ms_qr;
-    out.jacobi_ms += ms_j;
-    for (size_t q = 0; q < nb; ++q) {
-      out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
-      out.sweeps_sum += js[q].sweeps;
-      out.rotations += js[q].rotations;
-      const double cA = std::min<uint32_t>(plans[q].n_rows, M), Md = M;
-      out.jacobi_flops += (double)js[q].sweeps * (cA * (cA - 1) / 2 * 2 * Md + 2 * Md * cA) +
-                          (double)js[q].rotations * 6 * Md;
-      if (plans[q].tall)
-        out.qr_flops += 2.0 * plans[q].n_rows * Md * Md - 2.0 / 3.0 * Md * Md * Md;
-      if (js[q].failed) {
-        const uint64_t i = plans[q].block - d_lo;
-        out.failures[i] = "one-sided Jacobi did not converge (residual " + residual_text(js[q].residual) + ")";
-        out.conv_residual = js[q].residual;
-      }
-    }
-    i0 = i1;
+    t0 = t1;
   }
 }
 
@@ -544,6 +619,45 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   sync(s);  // host vectors (offset copies) are released
 }
 
+namespace {
+
+// Jacobi on W (M x cp, ld M, `cols` real columns) and finalize into out (sigma, U);
+// returns kappa = sigma_max / sigma_min over the `cols` columns
+double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t cp, MergeOut& out) {
+  cudaStream_t s = c.stream;
+  const uint32_t k = std::min(M, cols);
+  out.k = k;
+  out.sigma.alloc(k ? k : 1, s);
+  out.u.alloc((uint64_t)M * (k ? k : 1), s);
+  DBuf<double> alpha(cp, s);
+  DBuf<uint64_t> stats(8, s);
+  stats.zero();
+  std::vector<JacobiJob> jj(1);
+  jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = cols; jj[0].cols_pad = cp;
+  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
+  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+  JacobiStats js = read_stats(stats.get(), 1, s)[0];
+  out.sweeps = js.sweeps;
+  out.rotations = js.rotations;
+  if (js.failed) throw_convergence(js.residual);
+  DBuf<uint32_t> order(cp, s);
+  DBuf<double> scratch(cp, s), sig_all(cp, s);
+  DBuf<uint8_t> def(k ? k : 1, s);
+  FinalJob f;
+  std::memset(&f, 0, sizeof f);
+  f.w = W.get(); f.rows = M; f.cols = cp; f.k = k;
+  f.u = out.u.get(); f.sigma = out.sigma.get(); f.sigma_all = sig_all.get();
+  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
+  finalize_batched({f}, s);
+  std::vector<double> hs;
+  to_host(hs, sig_all.get(), cols, s);
+  if (any_flag(def.get(), k, s)) complete_and_sign(c, out.u.get(), M, k, def.get(), nullptr, 0);
+  const double smin = cols ? hs[cols - 1] : 0.0;
+  return smin > 0.0 ? hs[0] / smin : INFINITY;
+}
+
+}  // namespace
+
 void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut& out) {
   cudaStream_t s = c.stream;
   if (roots.size() > 1) {
@@ -560,30 +674,7 @@ void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut
   W.zero();
   transpose_sq<<<grid_for((uint64_t)M * M), 256, 0, s>>>(roots[0].get(), M, W.get());
   RK_LAUNCH_CHECK();
-  out.k = M;
-  out.sigma.alloc(M, s);
-  out.u.alloc((uint64_t)M * M, s);
-  DBuf<double> alpha(cp, s);
-  DBuf<uint64_t> stats(8, s);
-  stats.zero();
-  std::vector<JacobiJob> jj(1);
-  jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = M; jj[0].cols_pad = cp;
-  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
-  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
-  JacobiStats js = read_stats(stats.get(), 1, s)[0];
-  out.sweeps = js.sweeps;
-  out.rotations = js.rotations;
-  if (js.failed) throw_convergence(js.residual);
-  DBuf<uint32_t> order(cp, s);
-  DBuf<double> scratch(cp, s);
-  DBuf<uint8_t> def(M, s);
-  FinalJob f;
-  std::memset(&f, 0, sizeof f);
-  f.w = W.get(); f.rows = M; f.cols = cp; f.k = M;
-  f.u = out.u.get(); f.sigma = out.sigma.get();
-  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
-  finalize_batched({f}, s);
-  if (any_flag(def.get(), M, s)) complete_and_sign(c, out.u.get(), M, M, def.get(), nullptr, 0);
+  merge_jacobi(c, W, M, M, cp, out);
 }
 
 void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
@@ -598,6 +689,33 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
     return;
   }
   if (total > M) {
+    // Gram route: R_P^T = chol(P P^T), accepted when kappa(P) <= kappa_max(M)
+    if (gram_route_enabled() && M <= cholesky_max_rows() && M % 8 == 0) {
+      const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
+      DBuf<double> W((uint64_t)M * cp, s);
+      W.zero();
+      records_gram(payload, offset, kept, M, W.get(), s);
+      double* ptr = W.get();
+      DBuf<double*> dptr(1, s);
+      DBuf<uint32_t> status(1, s);
+      DBuf<double> ratio(1, s);
+      to_device(dptr.get(), &ptr, 1, s);
+      cholesky_batched(dptr.get(), 1, M, status.get(), ratio.get(), s);
+      uint32_t hst = 1;
+      double hr = INFINITY;
+      RK_CUDA_CHECK(cudaMemcpyAsync(&hst, status.get(), sizeof hst, cudaMemcpyDeviceToHost, s));
+      RK_CUDA_CHECK(cudaMemcpyAsync(&hr, ratio.get(), sizeof hr, cudaMemcpyDeviceToHost, s));
+      sync(s);
+      const double kmax = kappa_max(M);
+      if (hst == 0 && hr <= kmax) {
+        MergeOut tmp;
+        const double kappa = merge_jacobi(c, W, M, M, cp, tmp);
+        if (kappa <= kmax) {
+          out = std::move(tmp);
+          return;
+        }
+      }
+    }
     std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
     std::vector<DBuf<double>> roots(1);
     merge_subtree(c, payload, offset, kept, M, leaves, 0, leaves.size(), roots[0]);
@@ -617,30 +735,7 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
     RK_LAUNCH_CHECK();
     col += kept[r];
   }
-  out.k = tc;
-  out.sigma.alloc(tc, s);
-  out.u.alloc((uint64_t)M * tc, s);
-  DBuf<double> alpha(cp, s);
-  DBuf<uint64_t> stats(8, s);
-  stats.zero();
-  std::vector<JacobiJob> jj(1);
-  jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = tc; jj[0].cols_pad = cp;
-  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
-  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
-  JacobiStats js = read_stats(stats.get(), 1, s)[0];
-  out.sweeps = js.sweeps;
-  out.rotations = js.rotations;
-  if (js.failed) throw_convergence(js.residual);
-  DBuf<uint32_t> order(cp, s);
-  DBuf<double> scratch(cp, s);
-  DBuf<uint8_t> def(tc, s);
-  FinalJob f;
-  std::memset(&f, 0, sizeof f);
-  f.w = W.get(); f.rows = M; f.cols = cp; f.k = tc;
-  f.u = out.u.get(); f.sigma = out.sigma.get();
-  f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
-  finalize_batched({f}, s);
-  if (any_flag(def.get(), tc, s)) complete_and_sign(c, out.u.get(), M, tc, def.get(), nullptr, 0);
+  merge_jacobi(c, W, M, tc, cp, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -66,6 +66,17 @@ struct DenseSvdOut {
 };
 void dense_svd_dev(Ctx& c, const double* a, uint32_t rows, uint32_t cols, DenseSvdOut& out);
 
+// rk_gram.cu: Gram + Cholesky route (see the file header)
+void sparse_gram(const DevCsr& a, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
+                 cudaStream_t s);
+void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
+                  uint32_t M, double* G, cudaStream_t s);
+void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
+                      cudaStream_t s);
+double kappa_max(uint32_t M);
+uint32_t cholesky_max_rows();
+bool gram_route_enabled();
+
 // small launch helpers
 void sign_rows(double* u, uint32_t rows, uint32_t k, double* v, uint32_t vrows, cudaStream_t s);
 void check_finite_or_throw(const double* x, uint64_t n, const char* what, cudaStream_t s);

@@ -157,3 +157,19 @@ def test_baseline_config_end_to_end(name, ref):
     # bit-exact V given identical U, sigma and repaired matrix
     vr = ref.recover_right_vectors((a.rows(), a.cols(), *res.repaired.coo()), res.svd.u, res.svd.sigma, 1e-10)
     assert np.array_equal(res.svd.v, vr)
+
+
+@pytest.mark.parametrize("route", ["auto", "householder"])
+def test_block_routes_agree(route, monkeypatch, ref):
+    """The Gram/Cholesky route (accepted only when kappa <= kappa_max(M)) and the
+    Householder route both reproduce the reference on c1 (ill-conditioned blocks:
+    mostly Householder) and a c2 slice (well-conditioned: Gram)."""
+    monkeypatch.setenv("RK_BLOCK_ROUTE", route)
+    for name, scale in (("c1", None), ("c2", 262144 // 8)):
+        cfg = configs.CONFIGS[name]
+        a = cfg.generate(scale)
+        r, c, v = a.coo()
+        blocks = cfg.blocks if scale is None else cfg.blocks // 8
+        res = rk.run_pipeline(a, blocks, cfg.method, cfg.keep, cfg.seed, 1)
+        o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), blocks, cfg.method, cfg.keep, cfg.seed)
+        compare(res.svd, o.sigma, o.u, f"{name} {route}")
