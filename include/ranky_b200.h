@@ -144,6 +144,9 @@ RK_API rk_status rk_ctx_synchronize(rk_ctx* ctx);
 /* kernels launched through this context since creation */
 RK_API uint64_t rk_ctx_kernel_launches(const rk_ctx* ctx);
 
+/* release one library-allocated host buffer (e.g. a field taken over from a result
+ * record, which must then be set to NULL before the record is freed) */
+RK_API void rk_host_free(void* p);
 RK_API void rk_svd_free(rk_svd* s);
 RK_API void rk_repair_report_free(rk_repair_report* r);
 RK_API void rk_sparse_free(rk_sparse* s);

@@ -4,7 +4,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
-#include <unordered_set>
+#include <unordered_map>
 
 #include "rk_pipeline.cuh"
 
@@ -73,18 +73,31 @@ rk_status guarded(F&& body) {
 }
 
 // Output buffers above 1 MiB are page-locked so device->host copies of V run at
-// full PCIe rate; the registry lets rk_*_free release either kind.
+// full PCIe rate. Page-locking is expensive (the OS pins every page), so freed
+// pinned buffers go to a small cache keyed by size and are reused by the next
+// call of the same shape; the registry lets rk_*_free release either kind.
 std::mutex g_pinned_mu;
-std::unordered_set<void*> g_pinned;
+std::unordered_map<void*, size_t> g_pinned;          // live pinned buffers -> bytes
+std::unordered_multimap<size_t, void*> g_pinned_free;  // cached for reuse
+size_t g_pinned_cached = 0;
+constexpr size_t kPinnedCacheMax = size_t(8) << 30;
 
 template <class T>
 T* host_alloc(size_t n) {
   const size_t bytes = (n ? n : 1) * sizeof(T);
   if (bytes >= (1u << 20)) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    auto it = g_pinned_free.find(bytes);
+    if (it != g_pinned_free.end()) {
+      void* p = it->second;
+      g_pinned_free.erase(it);
+      g_pinned_cached -= bytes;
+      g_pinned[p] = bytes;
+      return static_cast<T*>(p);
+    }
     void* p = nullptr;
     if (cudaMallocHost(&p, bytes) == cudaSuccess) {
-      std::lock_guard<std::mutex> lk(g_pinned_mu);
-      g_pinned.insert(p);
+      g_pinned[p] = bytes;
       return static_cast<T*>(p);
     }
     cudaGetLastError();
@@ -100,8 +113,14 @@ void host_free(void* p) {
     std::lock_guard<std::mutex> lk(g_pinned_mu);
     auto it = g_pinned.find(p);
     if (it != g_pinned.end()) {
+      const size_t bytes = it->second;
       g_pinned.erase(it);
-      cudaFreeHost(p);
+      if (g_pinned_cached + bytes <= kPinnedCacheMax) {
+        g_pinned_free.emplace(bytes, p);
+        g_pinned_cached += bytes;
+      } else {
+        cudaFreeHost(p);
+      }
       return;
     }
   }
@@ -320,6 +339,8 @@ rk_status rk_ctx_synchronize(rk_ctx* ctx) {
 }
 
 uint64_t rk_ctx_kernel_launches(const rk_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+void rk_host_free(void* p) { host_free(p); }
 
 void rk_svd_free(rk_svd* s) {
   if (!s) return;

@@ -76,6 +76,34 @@ __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_
   return pos == 0 ? 0 : 1 + (pos - 1 + step) % (n - 1);
 }
 
+// Rotation (c, s) for a pair with norms^2 ap, aq and inner product gamma, the
+// reference's zeta/t formulas (svd.cpp:238-242) evaluated cheaply:
+//   * d = aq - ap and e = 2 gamma are scaled by an exact power of two so that
+//     max(|d|, |e|) is in [1, 2), then t = sign(zeta)|e| / (|d| + sqrt(d^2+e^2))
+//     is computed in FP32 (MUFU) -- the angle only steers convergence;
+//   * (c, s) = (1, t)/sqrt(1+t^2) is rounded to FP64 and renormalized with two
+//     Newton steps for 1/sqrt(c^2+s^2), so the applied rotation is orthogonal to
+//     FP64 precision whatever the angle's accuracy. The convergence test itself
+//     uses the FP64 gamma, so the stopping rule is the reference's.
+__device__ __forceinline__ void rotation_cs(double ap, double aq, double gamma, double& c, double& s) {
+  const double d = aq - ap, e = 2.0 * gamma;
+  const double m = fmax(fabs(d), fabs(e));
+  // 2^-floor(log2 m) built from the exponent bits (exact scaling, m > 0 here)
+  const int ex = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;
+  const double f = __hiloint2double((1023 - ex) << 20, 0);
+  const float df = (float)(d * f), ef = (float)(e * f);
+  const float r = sqrtf(fmaf(df, df, ef * ef));
+  const float sgn = (df == 0.0f || ((df > 0.0f) == (ef > 0.0f))) ? 1.0f : -1.0f;
+  const float t = sgn * fabsf(ef) / (fabsf(df) + r);
+  const float c32 = rsqrtf(fmaf(t, t, 1.0f));
+  double cc = (double)c32, ss = (double)(c32 * t);
+  const double n = cc * cc + ss * ss;
+  double r1 = 1.5 - 0.5 * n;
+  r1 = r1 * (1.5 - 0.5 * n * r1 * r1);
+  c = cc * r1;
+  s = ss * r1;
+}
+
 // Rotate one pair (p, q) of staged columns with a group of Q lanes (Q | 32);
 // returns 1 when rotated. Same decision rule as the reference (svd.cpp:232-260):
 // frozen columns are skipped before the dot; the pair rotates when
@@ -113,15 +141,11 @@ __device__ __forceinline__ int rotate_pair_q(double* __restrict__ wp, double* __
   double gamma = g0 + g1;
 #pragma unroll
   for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(gmask, gamma, o);
-  const double prod = ap * aq;
-  const double r2 = gamma * gamma / prod;
-  max_r2 = fmax(max_r2, r2);
-  if (!(gamma * gamma > kJacobiTol * kJacobiTol * prod)) return 0;
-  const double d = aq - ap, e = 2.0 * gamma;
-  const double sgn = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? 1.0 : -1.0;
-  const double t = sgn * fabs(e) / (fabs(d) + sqrt(fma(d, d, e * e)));
-  const double c = rsqrt(fma(t, t, 1.0));
-  const double s = c * t;
+  const double prod = ap * aq, g2 = gamma * gamma;
+  if (g2 > max_r2 * prod) max_r2 = g2 / prod;
+  if (!(g2 > kJacobiTol * kJacobiTol * prod)) return 0;
+  double c, s;
+  rotation_cs(ap, aq, gamma, c, s);
   i = lq + off;
   for (k = lq; k < rows; k += Q) {
     const uint32_t ii = i >= rows ? i - rows : i;
@@ -151,82 +175,82 @@ __device__ __forceinline__ int rotate_pair_q(double* __restrict__ wp, double* __
 // Cross round r pairs A_t with B_{(t+r) mod g}. Group t keeps A_t (and its alpha)
 // in registers for all g rounds of the step and streams the B columns through
 // shared memory: per element-pair one 8-byte shared load and one store (the
-// B value), instead of re-reading and re-writing both columns.
-template <int Q, int E>
-__device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint32_t rows, uint32_t g, double* sAlpha,
-                                                 double freeze, double& max_r2, unsigned long long& my_rot) {
+// B value), instead of re-reading and re-writing both columns. Control flow is
+// warp-uniform (the two or four lane groups of a warp may disagree on whether
+// their pair is frozen or rotates; that is handled with predication), so the
+// group reductions use full-warp shuffles that stay inside the group (xor < Q).
+template <int Q, int E, bool EXACT>
+__device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint32_t rows_rt, uint32_t g,
+                                                 double* sAlpha, double freeze, double& max_r2,
+                                                 unsigned long long& my_rot) {
+  const uint32_t rows = EXACT ? (uint32_t)(Q * E) : rows_rt;
   const int tid = threadIdx.x;
   const int grp = tid / Q, lq = tid & (Q - 1);
-  const unsigned gmask = (Q == 32) ? 0xffffffffu : (((1u << Q) - 1u) << ((tid & 31) & ~(Q - 1)));
   const bool active = (uint32_t)grp < g;
   double a[E];
   double aA = 0.0;
-  if (active) {
-    const double* pa = sW + (uint64_t)grp * ldS;
+  {
+    const double* pa = sW + (uint64_t)(active ? grp : 0) * ldS + lq;
+#pragma unroll
+    for (int k = 0; k < E; ++k) a[k] = (active && (EXACT || lq + Q * k < (int)rows)) ? pa[Q * k] : 0.0;
+    aA = active ? sAlpha[grp] : 0.0;
+  }
+  uint32_t jl = active ? (uint32_t)grp : 0u;  // (grp + r) mod g, advanced incrementally
+  double* const bbase = sW + (uint64_t)g * ldS + lq;
+  for (uint32_t r = 0; r < g; ++r) {
+    double* pb = bbase + (uint64_t)jl * ldS;
+    const double aB = sAlpha[g + jl];
+    const bool live = active && !(aA <= freeze || aB <= freeze);
+    double b[E];
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const uint32_t i = lq + Q * k;
-      a[k] = i < rows ? pa[i] : 0.0;
+      b[k] = (live && (EXACT || lq + Q * k < (int)rows)) ? pb[Q * k] : 0.0;
+      const double pr = a[k] * b[k];
+      if ((k & 3) == 0) acc0 += pr;
+      else if ((k & 3) == 1) acc1 += pr;
+      else if ((k & 3) == 2) acc2 += pr;
+      else acc3 += pr;
     }
-    aA = sAlpha[grp];
-  }
-  for (uint32_t r = 0; r < g; ++r) {
-    if (active) {
-      const uint32_t j = g + ((uint32_t)grp + r) % g;
-      double* pb = sW + (uint64_t)j * ldS;
-      const double aB = sAlpha[j];
-      if (!(aA <= freeze || aB <= freeze)) {
-        double b[E];
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double gamma = (acc0 + acc1) + (acc2 + acc3);
 #pragma unroll
-        for (int k = 0; k < E; ++k) {
-          const uint32_t i = lq + Q * k;
-          b[k] = i < rows ? pb[i] : 0.0;
-          acc[k & 3] += a[k] * b[k];
-        }
-        double gamma = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(0xffffffffu, gamma, o);
+    const double prod = aA * aB, g2 = gamma * gamma;
+    if (live && g2 > max_r2 * prod) max_r2 = g2 / prod;
+    const bool rot = live && (g2 > kJacobiTol * kJacobiTol * prod);
+    if (__any_sync(0xffffffffu, rot)) {
+      double c = 1.0, sn = 0.0;
+      if (rot) rotation_cs(aA, aB, gamma, c, sn);
 #pragma unroll
-        for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(gmask, gamma, o);
-        const double prod = aA * aB;
-        max_r2 = fmax(max_r2, gamma * gamma / prod);
-        if (gamma * gamma > kJacobiTol * kJacobiTol * prod) {
-          const double d = aB - aA, e = 2.0 * gamma;
-          const double sgn = (d == 0.0 || ((d > 0.0) == (e > 0.0))) ? 1.0 : -1.0;
-          const double t = sgn * fabs(e) / (fabs(d) + sqrt(fma(d, d, e * e)));
-          const double c = rsqrt(fma(t, t, 1.0));
-          const double sn = c * t;
-#pragma unroll
-          for (int k = 0; k < E; ++k) {
-            const uint32_t i = lq + Q * k;
-            const double xp = a[k], xq = b[k];
-            a[k] = c * xp - sn * xq;
-            if (i < rows) pb[i] = sn * xp + c * xq;
-          }
-          const double na = c * c * aA - 2.0 * c * sn * gamma + sn * sn * aB;
-          const double nq = sn * sn * aA + 2.0 * c * sn * gamma + c * c * aB;
-          aA = na > 0.0 ? na : 0.0;
-          if (lq == 0) {
-            sAlpha[j] = nq > 0.0 ? nq : 0.0;
-            ++my_rot;
-          }
+      for (int k = 0; k < E; ++k) {
+        const double xp = a[k], xq = b[k];
+        a[k] = c * xp - sn * xq;
+        if (rot && (EXACT || lq + Q * k < (int)rows)) pb[Q * k] = sn * xp + c * xq;
+      }
+      if (rot) {
+        const double na = c * c * aA - 2.0 * c * sn * gamma + sn * sn * aB;
+        const double nq = sn * sn * aA + 2.0 * c * sn * gamma + c * c * aB;
+        aA = na > 0.0 ? na : 0.0;
+        if (lq == 0) {
+          sAlpha[g + jl] = nq > 0.0 ? nq : 0.0;
+          ++my_rot;
         }
       }
     }
+    jl = (jl + 1 == g) ? 0u : jl + 1;
     __syncthreads();
   }
   if (active) {
-    double* pa = sW + (uint64_t)grp * ldS;
+    double* pa = sW + (uint64_t)grp * ldS + lq;
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const uint32_t i = lq + Q * k;
-      if (i < rows) pa[i] = a[k];
-    }
+    for (int k = 0; k < E; ++k)
+      if (EXACT || lq + Q * k < (int)rows) pa[Q * k] = a[k];
     if (lq == 0) sAlpha[grp] = aA;
   }
   __syncthreads();
 }
 
-template <int Q, int E>
+template <int Q, int E, bool EXACT>
 __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -322,7 +346,7 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
         }
         // cross rounds: (A_i, B_{(i + r) mod g})
         if constexpr (E > 0) {
-          cross_rounds_reg<Q, E>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
+          cross_rounds_reg<Q, E, EXACT>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
         } else {
           for (uint32_t r = 0; r < g; ++r) {
             for (uint32_t t = grp_id; t < g; t += kGroups) {
@@ -560,7 +584,7 @@ size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
 void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, uint32_t& g, uint32_t& G) {
   // largest even group size (<= gcap) whose two staged groups fit the budget; a
   // smaller cap trades longer tournaments for more CTAs per SM (latency hiding)
-  static const uint32_t gcap = [] {
+  const uint32_t gcap = [] {
     const char* e = std::getenv("RK_JACOBI_GMAX");
     const long v = e ? std::strtol(e, nullptr, 10) : 16;
     return (uint32_t)std::max<long>(2, std::min<long>(32, v & ~1L));
@@ -611,23 +635,28 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // elements per lane held in registers by the cross rounds (0: shared-memory path)
   int Q = 32;
   while (Q > 8 && (kJThreads / Q) < (int)g) Q /= 2;
+  if (const char* qe = std::getenv("RK_JACOBI_Q")) {  // tuning override (must give >= g lane groups)
+    const int qv = (int)std::strtol(qe, nullptr, 10);
+    if ((qv == 8 || qv == 16 || qv == 32) && kJThreads / qv >= (int)g) Q = qv;
+  }
   int E = 1;
   while (E * Q < (int)rows) E *= 2;
   if (E < 4) E = 4;
   if (E > 32 || with_v) E = 0;  // a[E] + b[E] must stay in registers
+  const bool exact = E > 0 && (int)rows == Q * E;
   auto launch = [&](auto kern) {
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     launch_cluster_kernel((const void*)kern, (unsigned)jobs.size() * cl, cl, kJThreads, smem, s, kargs);
   };
-#define RK_JAC_E(QQ)                                                  \
-  switch (E) {                                                        \
-    case 4: launch(jacobi_cluster_kernel<QQ, 4>); break;              \
-    case 8: launch(jacobi_cluster_kernel<QQ, 8>); break;              \
-    case 16: launch(jacobi_cluster_kernel<QQ, 16>); break;            \
-    case 32: launch(jacobi_cluster_kernel<QQ, 32>); break;            \
-    default: launch(jacobi_cluster_kernel<QQ, 0>); break;             \
+#define RK_JAC_E(QQ)                                                                   \
+  switch (E) {                                                                         \
+    case 4: exact ? launch(jacobi_cluster_kernel<QQ, 4, true>) : launch(jacobi_cluster_kernel<QQ, 4, false>); break;   \
+    case 8: exact ? launch(jacobi_cluster_kernel<QQ, 8, true>) : launch(jacobi_cluster_kernel<QQ, 8, false>); break;   \
+    case 16: exact ? launch(jacobi_cluster_kernel<QQ, 16, true>) : launch(jacobi_cluster_kernel<QQ, 16, false>); break; \
+    case 32: exact ? launch(jacobi_cluster_kernel<QQ, 32, true>) : launch(jacobi_cluster_kernel<QQ, 32, false>); break; \
+    default: launch(jacobi_cluster_kernel<QQ, 0, false>); break;                       \
   }
   if (Q == 8) { RK_JAC_E(8) }
   else if (Q == 16) { RK_JAC_E(16) }

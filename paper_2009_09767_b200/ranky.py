@@ -173,7 +173,7 @@ def lib():
             "rk_ctx_create": ([i32, C.POINTER(vp)], i32), "rk_ctx_destroy": ([vp], i32),
             "rk_ctx_set_stream": ([vp, vp], i32), "rk_ctx_synchronize": ([vp], i32),
             "rk_ctx_kernel_launches": ([vp], u64),
-            "rk_svd_free": ([C.POINTER(_Svd)], None), "rk_repair_report_free": ([C.POINTER(_Report)], None),
+            "rk_svd_free": ([C.POINTER(_Svd)], None), "rk_host_free": ([C.c_void_p], None), "rk_repair_report_free": ([C.POINTER(_Report)], None),
             "rk_sparse_free": ([C.POINTER(_Sparse)], None), "rk_records_free": ([C.POINTER(_Records)], None),
             "rk_pipeline_result_free": ([C.POINTER(_Pipeline)], None),
             "rk_keyed_rng_next": ([vp, u64, u64, pu64, pu64, u64, pu64], i32),
@@ -580,12 +580,45 @@ class SvdResult:
     v: np.ndarray | None = None
 
 
+class _HostBuffer:
+    """Owns one library-allocated host buffer; numpy arrays view it without a copy."""
+
+    def __init__(self, addr):
+        self.addr = addr
+
+    def __del__(self):
+        try:
+            lib().rk_host_free(C.c_void_p(self.addr))
+        except Exception:
+            pass
+
+
+def _take_array(struct, field: str, n: int, shape) -> np.ndarray:
+    """Zero-copy numpy view of a large result buffer; ownership moves to the array
+    (the struct field is cleared so the record's free does not release it)."""
+    ptr = getattr(struct, field)
+    addr = C.cast(ptr, C.c_void_p).value
+    if n < (1 << 17) or not addr:
+        return _arr(ptr, n, np.float64).reshape(shape)
+    buf = (C.c_double * n).from_address(addr)
+    arr = np.frombuffer(buf, dtype=np.float64).reshape(shape)
+    keeper = _HostBuffer(addr)
+    setattr(struct, field, C.cast(C.c_void_p(0), type(ptr)))
+    holder = np.ndarray.__new__(_Owned, arr.shape, dtype=arr.dtype, buffer=buf)
+    holder._keeper = keeper
+    return holder
+
+
+class _Owned(np.ndarray):
+    """ndarray subclass that keeps the library buffer alive."""
+
+
 def _svd_of(s: _Svd) -> SvdResult:
-    u = _arr(s.u, s.u_rows * s.u_cols, np.float64).reshape(int(s.u_rows), int(s.u_cols))
+    u = _take_array(s, "u", int(s.u_rows * s.u_cols), (int(s.u_rows), int(s.u_cols)))
     sig = _arr(s.sigma, s.n_sigma, np.float64)
     v = None
     if s.has_v:
-        v = _arr(s.v, s.v_rows * s.v_cols, np.float64).reshape(int(s.v_rows), int(s.v_cols))
+        v = _take_array(s, "v", int(s.v_rows * s.v_cols), (int(s.v_rows), int(s.v_cols)))
     return SvdResult(u, sig, v)
 
 
