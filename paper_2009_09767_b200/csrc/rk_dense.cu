@@ -580,6 +580,8 @@ void r_extract_batched(const std::vector<RJob>& jobs, bool transpose, cudaStream
 }
 
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
+bool jacobi_gram_supported(uint32_t rows, uint32_t g, size_t smem_optin);
+void jacobi_gram_batched(std::vector<JacobiJob>& jobs, uint32_t g, uint32_t G, cudaStream_t s, int sms);
 
 void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, uint32_t& g, uint32_t& G) {
   // largest even group size (<= gcap) whose two staged groups fit the budget; a
@@ -619,6 +621,18 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     if (j.cols > cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols > cols_pad");
   }
   if (g * G != cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols_pad is not a planned width");
+  // Gram-assisted kernel: only where the direct kernel cannot keep the A column in
+  // registers (rows > 32 lanes-per-pair x 32), i.e. long columns relative to 2g;
+  // RK_JACOBI_GRAM=1 / RK_JACOBI_DIRECT=1 force either kernel (tuning)
+  bool all_gram = !with_v && !std::getenv("RK_JACOBI_DIRECT");
+  for (const JacobiJob& j : jobs) all_gram = all_gram && j.gram_ok;
+  int q_direct = 32;
+  while (q_direct > 8 && (kJThreads / q_direct) < (int)g) q_direct /= 2;
+  const bool long_columns = rows > (uint32_t)(32 * q_direct) || std::getenv("RK_JACOBI_GRAM");
+  if (all_gram && long_columns && jacobi_gram_supported(rows, g, smem_optin)) {
+    jacobi_gram_batched(jobs, g, G, s, sms);
+    return;
+  }
   const size_t smem = jacobi_smem(rows, g, g * G, with_v);
   // cluster size: enough CTAs for the SMs at the occupancy the shared memory allows
   const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (smem + 2048)));

@@ -284,6 +284,7 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
   uint32_t rows, cols, cols_pad;
   double* alpha;      // cols_pad scratch
   uint64_t* stats;    // [0] sweeps, [1] rotations, [2] status (0 ok, 1 not converged), [3] residual bits, [4..7] scratch
+  uint32_t gram_ok = 0;  // well-conditioned (kappa <= kappa_max): the Gram-assisted kernel may run it
 };
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin);
 

@@ -264,7 +264,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
 
   // Jacobi + finalize of a set of W slots; records stats and writes payloads
   auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
-                             bool tall_flops_from_plans, double* sigma_all /* nullable: slots x cols_pad */) {
+                             bool gram_ok, double* sigma_all /* nullable: slots x cols_pad */) {
     const size_t nb = slots.size();
     DBuf<double> alpha((uint64_t)nb * cols_pad_full, s);
     DBuf<uint64_t> stats(8 * nb, s);
@@ -280,6 +280,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       jj[q].cols_pad = cols_pad_full;
       jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad_full;
       jj[q].stats = stats.get() + 8 * q;
+      jj[q].gram_ok = gram_ok ? 1u : 0u;
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
     jacobi_batched(jj, s, c.num_sms, c.smem_optin);
@@ -308,7 +309,6 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     float ms_j = 0;
     cudaEventElapsedTime(&ms_j, c.ev[9], c.ev[10]);
     out.jacobi_ms += ms_j;
-    (void)tall_flops_from_plans;
     for (size_t q = 0; q < nb; ++q) {
       out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
       out.sweeps_sum += js[q].sweeps;
@@ -368,14 +368,17 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       }
       if (slots.empty()) continue;
       DBuf<double> sig((uint64_t)slots.size() * cols_pad_full, s);
-      jacobi_finalize(slots, cols, blocks, false, sig.get());
+      jacobi_finalize(slots, cols, blocks, true, sig.get());
       std::vector<double> hs;
       to_host(hs, sig.get(), sig.n, s);
       sync(s);
       for (size_t q = 0; q < slots.size(); ++q) {
         const double smax = hs[q * cols_pad_full], smin = hs[q * cols_pad_full + M - 1];
         const uint64_t i = blocks[q];
-        if (!out.failures[i].empty()) { done[i] = 1; continue; }  // a Jacobi failure is final
+        if (!out.failures[i].empty()) {  // redo on the Householder route
+          out.failures[i].clear();
+          continue;
+        }
         if (smin > 0.0 && smax / smin <= kmax) done[i] = 1;
       }
     }
@@ -473,7 +476,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       cols[q] = std::min<uint32_t>(plans[q].n_rows, M);
       blocks[q] = plans[q].block - d_lo;
     }
-    jacobi_finalize(slots, cols, blocks, true, nullptr);
+    jacobi_finalize(slots, cols, blocks, false, nullptr);
     float ms_qr = 0;
     cudaEventElapsedTime(&ms_qr, c.ev[8], c.ev[11]);
     out.qr_ms += ms_qr;
@@ -623,7 +626,8 @@ namespace {
 
 // Jacobi on W (M x cp, ld M, `cols` real columns) and finalize into out (sigma, U);
 // returns kappa = sigma_max / sigma_min over the `cols` columns
-double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t cp, MergeOut& out) {
+double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t cp, MergeOut& out,
+                    bool gram_ok = false) {
   cudaStream_t s = c.stream;
   const uint32_t k = std::min(M, cols);
   out.k = k;
@@ -634,12 +638,15 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   stats.zero();
   std::vector<JacobiJob> jj(1);
   jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = cols; jj[0].cols_pad = cp;
-  jj[0].alpha = alpha.get(); jj[0].stats = stats.get();
+  jj[0].alpha = alpha.get(); jj[0].stats = stats.get(); jj[0].gram_ok = gram_ok ? 1u : 0u;
   jacobi_batched(jj, s, c.num_sms, c.smem_optin);
   JacobiStats js = read_stats(stats.get(), 1, s)[0];
   out.sweeps = js.sweeps;
   out.rotations = js.rotations;
-  if (js.failed) throw_convergence(js.residual);
+  if (js.failed) {
+    if (gram_ok) return INFINITY;  // the caller falls back to the TSQR route
+    throw_convergence(js.residual);
+  }
   DBuf<uint32_t> order(cp, s);
   DBuf<double> scratch(cp, s), sig_all(cp, s);
   DBuf<uint8_t> def(k ? k : 1, s);
@@ -709,7 +716,7 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
       const double kmax = kappa_max(M);
       if (hst == 0 && hr <= kmax) {
         MergeOut tmp;
-        const double kappa = merge_jacobi(c, W, M, M, cp, tmp);
+        const double kappa = merge_jacobi(c, W, M, M, cp, tmp, true);
         if (kappa <= kmax) {
           out = std::move(tmp);
           return;
