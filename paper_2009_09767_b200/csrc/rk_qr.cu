@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2) qr_kernel(const QrJob* __restrict
         for (int kk = 0; kk < NB; kk += 4) {
           const int r = kk + lc;
           const double av = (r < nbk && row_ok && i >= r) ? P[r * ldp + i] : 0.0;
-          const double bv = wt[(kk + lc) * 8 + lr];
+          const double bv = (kk + lc < NB) ? wt[(kk + lc) * 8 + lr] : 0.0;
           dmma(d0, d1, av, bv);
         }
         if (row_ok) {
@@ -303,7 +303,7 @@ void launch_qr(const std::vector<QrJob>& jobs, const QrJob* d_jobs, unsigned cl,
 
 }  // namespace
 
-uint32_t qr_max_rows() { return 6144; }
+uint32_t qr_max_rows() { return 24000; }
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   if (jobs.empty()) return;
@@ -317,8 +317,15 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   if (h_max > qr_max_rows()) fail(RK_RUNTIME, "qr_batched: matrix taller than a panel can stage");
   const size_t budget = 200 * 1024;
   int nb = 16;
-  if (qr_smem<16>(h_max) > budget) nb = qr_smem<8>(h_max) <= budget ? 8 : 4;
-  const size_t smem = nb == 16 ? qr_smem<16>(h_max) : nb == 8 ? qr_smem<8>(h_max) : qr_smem<4>(h_max);
+  while (nb > 1 && (nb == 16 ? qr_smem<16>(h_max) : nb == 8 ? qr_smem<8>(h_max) : nb == 4 ? qr_smem<4>(h_max)
+                                                                                          : qr_smem<2>(h_max)) > budget)
+    nb /= 2;
+  const size_t smem = nb == 16 ? qr_smem<16>(h_max)
+                      : nb == 8 ? qr_smem<8>(h_max)
+                      : nb == 4 ? qr_smem<4>(h_max)
+                      : nb == 2 ? qr_smem<2>(h_max)
+                                : qr_smem<1>(h_max);
+  if (smem > budget) fail(RK_RUNTIME, "qr_batched: matrix taller than a panel can stage");
   // one CTA per matrix while the batch fills the GPU (other CTAs on the SM hide the
   // panel latency); clusters split the trailing update of small batches
   const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 2048)));
@@ -333,7 +340,9 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   const QrJob* d = dj.get();
   if (nb == 16) launch_qr<16>(jobs, d, cl, h_max, s);
   else if (nb == 8) launch_qr<8>(jobs, d, cl, h_max, s);
-  else launch_qr<4>(jobs, d, cl, h_max, s);
+  else if (nb == 4) launch_qr<4>(jobs, d, cl, h_max, s);
+  else if (nb == 2) launch_qr<2>(jobs, d, cl, h_max, s);
+  else launch_qr<1>(jobs, d, cl, h_max, s);
 }
 
 }  // namespace rk

@@ -1,0 +1,27 @@
+"""The reference's own acceptance suite (proj/tests/acceptance_main.cpp), relinked
+with its hot-path objects (repair, svd, proxy, pipeline) replaced by the B200
+drop-in (paper_2009_09767_b200/dropin/ranky_dropin.cpp -> libranky_b200.so).
+The binary is built by oracle/Makefile (target dropin) where the reference
+sources exist and travels prebuilt in oracle/_ref."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "ranky_acceptance_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_acceptance_suite_on_b200_dropin():
+    if not os.path.exists(BIN):
+        pytest.skip("relinked acceptance binary not built (needs the reference sources)")
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
+    text = out.stdout + out.stderr
+    print(text)
+    passed = [l for l in text.splitlines() if l.startswith("PASS")]
+    failed = [l for l in text.splitlines() if l.startswith("FAIL")]
+    assert not failed, failed
+    assert len(passed) == 8, text
+    assert out.returncode == 0
