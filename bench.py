@@ -234,10 +234,9 @@ def main():
             R.dev_outputs_free(out)
             return t
     else:
-        leaves = int(L.rk_merge_tree_leaves(M, cfg.cols, cfg.blocks, cfg.keep))
-        per = leaves // ws
-        lo, hi = rank * per, (rank + 1) * per if rank + 1 < ws else leaves
-        width = cfg.cols // cfg.blocks
+        from paper_2009_09767_b200 import shard as SH
+        sp = SH.plan(M, cfg.cols, cfg.blocks, cfg.keep, ws, rank)
+        lo, hi, c_lo, c_hi = sp.leaf_lo, sp.leaf_hi, sp.col_lo, sp.col_hi
         roots = torch.empty((ws, M, M), dtype=torch.float64, device="cuda")
         mine = torch.empty((M, M), dtype=torch.float64, device="cuda")
 
@@ -248,9 +247,6 @@ def main():
                                            cfg.seed, lo, hi, C.c_void_p(mine.data_ptr()), C.byref(shard),
                                            C.byref(t)))
             torch.distributed.all_gather_into_tensor(roots, mine)
-            # columns owned by this rank: its leaves' blocks (uniform kept -> blocks per leaf)
-            bpl = cfg.blocks // leaves
-            c_lo, c_hi = lo * bpl * width, (hi * bpl * width if rank + 1 < ws else cfg.cols)
             out = C.POINTER(R.DevOutputs)()
             t2 = R.Timing()
             R._check(L.rk_dev_shard_finish(ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V,
