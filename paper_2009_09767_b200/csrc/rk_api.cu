@@ -1,5 +1,7 @@
 // rk_api.cu -- the C ABI (include/ranky_b200.h): argument checks with the
 // reference's messages, exception -> status mapping, host <-> device marshaling.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -10,6 +12,27 @@
 
 namespace rk {
 thread_local uint64_t* g_launch_counter = nullptr;
+
+void trim_pool(cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+}
+
+void trace_launch(const char* file, int line) {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaDeviceSynchronize();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, "[rk trace] %s:%d %.3f ms %s\n", file, line, ms, cudaGetErrorString(e));
+}
 void* host_alloc_bytes(size_t bytes);
 
 CallScope::CallScope(Ctx* c) {
@@ -230,6 +253,7 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   RK_CUDA_CHECK(cudaEventRecord(ev2, s));
   merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
   RK_CUDA_CHECK(cudaEventRecord(ev3, s));
+  if (!(flags & RK_WANT_RECORDS)) fr.blocks.payload.release();  // P is not an output: make room for V
   if (flags & RK_WANT_V) {
     const uint32_t k = fr.merge.k;
     const uint32_t kk = (top_k && top_k < k) ? (uint32_t)top_k : k;

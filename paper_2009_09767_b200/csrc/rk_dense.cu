@@ -479,63 +479,124 @@ __global__ void __launch_bounds__(kFThreads) finalize_kernel(const FinalJob* job
 }
 
 // ===========================================================================
-// orthonormal completion (single warp, deterministic) -- svd.cpp:150-201
+// orthonormal completion (one CTA, deterministic) -- svd.cpp:150-201
 // u is row-major rows x cols
 // ===========================================================================
 
-__global__ void complete_kernel(double* u, uint32_t rows, uint32_t cols, const uint8_t* deficient, int* fail) {
+// One CTA. Same candidate rule as the reference (e_0, e_1, ... ; the first whose
+// residual after two orthogonalization passes against the placed columns exceeds
+// 0.5, else the best one, then one touch-up pass) with two changes that keep the
+// choice: the passes are classical Gram-Schmidt over the whole CTA (projections
+// of w onto all placed columns at once, twice -- CGS2 -- instead of the
+// reference's column-by-column MGS; the completion basis of an exactly
+// degenerate cluster is not unique anyway), and the scan resumes after the
+// leading candidates already known to be dead -- rejected with a clear margin
+// (residual < 0.5 - 1e-6) or taken -- for an earlier column: the placed span only
+// grows, so their residual can only shrink and the reference would reject them
+// again. This removes the O(deficient^2) rescans that made rank-deficient
+// 512-row blocks take minutes. If no candidate passes, the dead ones are scanned
+// too (the reference's best-residual fallback over all candidates).
+constexpr int kCThreads = 1024;
+
+__device__ double block_sum(double x, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  x = warp_sum(x);
+  __syncthreads();
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(kCThreads) complete_kernel(double* u, uint32_t rows, uint32_t cols,
+                                                             const uint8_t* deficient, int* fail) {
   extern __shared__ double cw[];
   double* w = cw;
   double* best = cw + rows;
-  const int lane = threadIdx.x;
+  double* proj = best + rows;
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  uint32_t start = 0;
+  // w <- (I - U_p U_p^T)^2 e_cand over the placed columns p (not deficient, or < j)
+  auto orth_candidate = [&](uint32_t cand, uint32_t j) -> double {
+    for (uint32_t i = tid; i < rows; i += blockDim.x) w[i] = (i == cand) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (uint32_t c = tid; c < cols; c += blockDim.x) {
+        double acc = 0.0;
+        if (!deficient[c] || c < j)
+          for (uint32_t i = 0; i < rows; ++i) acc += u[(uint64_t)i * cols + c] * w[i];
+        proj[c] = acc;
+      }
+      __syncthreads();
+      for (uint32_t i = warp; i < rows; i += nw) {
+        double acc = 0.0;
+        for (uint32_t c = lane; c < cols; c += 32) acc += u[(uint64_t)i * cols + c] * proj[c];
+        acc = warp_sum(acc);
+        if (lane == 0) w[i] -= acc;
+      }
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (uint32_t i = tid; i < rows; i += blockDim.x) nn += w[i] * w[i];
+    return sqrt(block_sum(nn, red));
+  };
   for (uint32_t j = 0; j < cols; ++j) {
     if (!deficient[j]) continue;
     double best_norm = -1.0;
-    for (uint32_t cand = 0; cand < rows; ++cand) {
-      for (uint32_t i = lane; i < rows; i += 32) w[i] = (i == cand) ? 1.0 : 0.0;
-      __syncwarp();
-      for (int pass = 0; pass < 2; ++pass) {
-        for (uint32_t c = 0; c < cols; ++c) {
-          if (deficient[c] && c >= j) continue;
-          double d = 0.0;
-          for (uint32_t i = lane; i < rows; i += 32) d += u[(uint64_t)i * cols + c] * w[i];
-          d = warp_sum(d);
-          for (uint32_t i = lane; i < rows; i += 32) w[i] -= d * u[(uint64_t)i * cols + c];
-          __syncwarp();
+    bool found = false, leading = true;
+    uint32_t next_start = start;
+    for (int phase = 0; phase < 2 && !found; ++phase) {
+      const uint32_t c0 = phase == 0 ? start : 0, c1 = phase == 0 ? rows : start;
+      for (uint32_t cand = c0; cand < c1; ++cand) {
+        const double wn = orth_candidate(cand, j);
+        const bool take = wn > 0.5;
+        if (take || wn > best_norm) {
+          best_norm = wn;
+          for (uint32_t i = tid; i < rows; i += blockDim.x) best[i] = w[i];
+        }
+        if (phase == 0 && leading) {
+          if (take || wn < 0.5 - 1e-6) next_start = cand + 1;
+          else leading = false;
+        }
+        __syncthreads();
+        if (take) {
+          found = true;
+          break;
         }
       }
-      double nn = 0.0;
-      for (uint32_t i = lane; i < rows; i += 32) nn += w[i] * w[i];
-      const double wn = sqrt(warp_sum(nn));
-      const bool take = wn > 0.5;
-      if (take || wn > best_norm) {
-        best_norm = wn;
-        for (uint32_t i = lane; i < rows; i += 32) best[i] = w[i];
-        __syncwarp();
-      }
-      if (take) break;
     }
+    start = next_start;
     if (!(best_norm > 0.0)) {
       // no independent direction (svd.cpp:183-186)
-      if (lane == 0) *fail = 1;
+      if (tid == 0) *fail = 1;
       return;
     }
-    for (uint32_t i = lane; i < rows; i += 32) u[(uint64_t)i * cols + j] = best[i] / best_norm;
-    __syncwarp();
+    for (uint32_t i = tid; i < rows; i += blockDim.x) u[(uint64_t)i * cols + j] = best[i] / best_norm;
+    __syncthreads();
     if (best_norm <= 0.5) {
-      for (uint32_t c = 0; c < cols; ++c) {
-        if (deficient[c] && c >= j) continue;
-        double d = 0.0;
-        for (uint32_t i = lane; i < rows; i += 32) d += u[(uint64_t)i * cols + c] * u[(uint64_t)i * cols + j];
-        d = warp_sum(d);
-        for (uint32_t i = lane; i < rows; i += 32) u[(uint64_t)i * cols + j] -= d * u[(uint64_t)i * cols + c];
-        __syncwarp();
+      for (uint32_t i = tid; i < rows; i += blockDim.x) w[i] = u[(uint64_t)i * cols + j];
+      __syncthreads();
+      for (uint32_t c = tid; c < cols; c += blockDim.x) {
+        double acc = 0.0;
+        if (!deficient[c] || c < j)
+          for (uint32_t i = 0; i < rows; ++i) acc += u[(uint64_t)i * cols + c] * w[i];
+        proj[c] = acc;
       }
+      __syncthreads();
+      for (uint32_t i = warp; i < rows; i += nw) {
+        double acc = 0.0;
+        for (uint32_t c = lane; c < cols; c += 32) acc += u[(uint64_t)i * cols + c] * proj[c];
+        acc = warp_sum(acc);
+        if (lane == 0) w[i] -= acc;
+      }
+      __syncthreads();
       double nn = 0.0;
-      for (uint32_t i = lane; i < rows; i += 32) nn += u[(uint64_t)i * cols + j] * u[(uint64_t)i * cols + j];
-      const double wn = sqrt(warp_sum(nn));
-      for (uint32_t i = lane; i < rows; i += 32) u[(uint64_t)i * cols + j] /= wn;
-      __syncwarp();
+      for (uint32_t i = tid; i < rows; i += blockDim.x) nn += w[i] * w[i];
+      const double wn = sqrt(block_sum(nn, red));
+      for (uint32_t i = tid; i < rows; i += blockDim.x) u[(uint64_t)i * cols + j] = w[i] / wn;
+      __syncthreads();
     }
   }
 }
@@ -699,10 +760,10 @@ void finalize_batched(const std::vector<FinalJob>& jobs, cudaStream_t s) {
 
 void complete_columns_device(double* u, uint32_t rows, uint32_t cols, const uint8_t* deficient, int* d_fail,
                              cudaStream_t s) {
-  const size_t smem = (size_t)2 * rows * 8;
-  if (smem > 48 * 1024)
-    RK_CUDA_CHECK(cudaFuncSetAttribute(complete_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  complete_kernel<<<1, 32, smem, s>>>(u, rows, cols, deficient, d_fail);
+  const size_t smem = ((size_t)2 * rows + cols) * 8;
+  if (smem > 200 * 1024) fail(RK_RUNTIME, "orthonormal completion: matrix too large");
+  RK_CUDA_CHECK(cudaFuncSetAttribute(complete_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  complete_kernel<<<1, kCThreads, smem, s>>>(u, rows, cols, deficient, d_fail);
   RK_LAUNCH_CHECK();
 }
 

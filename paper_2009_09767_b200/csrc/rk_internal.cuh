@@ -36,16 +36,22 @@ struct Error : std::runtime_error {
 // launch bookkeeping: every kernel launch goes through RK_LAUNCH so the context
 // can report how many of its kernels ran (bench.py "gpu_launches")
 extern thread_local uint64_t* g_launch_counter;
+// RK_TRACE=1: synchronize after every launch and log it to stderr (debugging hangs)
+void trace_launch(const char* file, int line);
 #define RK_LAUNCH_CHECK()                                                                    \
   do {                                                                                      \
     if (::rk::g_launch_counter) ++*::rk::g_launch_counter;                                   \
     cudaError_t rk_e_ = cudaGetLastError();                                                 \
     if (rk_e_ != cudaSuccess)                                                               \
       ::rk::fail(RK_CUDA, std::string("kernel launch: ") + cudaGetErrorString(rk_e_));     \
+    ::rk::trace_launch(__FILE__, __LINE__);                                                 \
   } while (0)
 
 // ---------------------------------------------------------------------------
 // stream-ordered device buffer
+
+// synchronize `s` and release the device's pool memory that is not in use
+void trim_pool(cudaStream_t s);
 
 template <class T>
 struct DBuf {
@@ -60,12 +66,23 @@ struct DBuf {
     n = count;
     if (count) {
       cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st);
+      if (e == cudaErrorMemoryAllocation) {
+        // the stream-ordered pool keeps freed blocks (release threshold = max); give
+        // them back to the driver and retry once before reporting out-of-memory
+        cudaGetLastError();
+        trim_pool(st);
+        e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st);
+      }
       if (e != cudaSuccess) {
         p = nullptr;
         n = 0;
         cudaGetLastError();
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        cudaGetLastError();
         fail(RK_NOMEM, std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
-                           " bytes failed: " + cudaGetErrorString(e));
+                           " bytes failed: " + cudaGetErrorString(e) + " (device free " +
+                           std::to_string(fr >> 20) + " of " + std::to_string(tot >> 20) + " MiB)");
       }
     }
   }

@@ -396,11 +396,12 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   to_host(hc, counts.get(), 2 * nblk, s);
   sync(s);
   const uint64_t aux_sz = 2 * (uint64_t)M + (ceil_div(M, 16) + 1) * 256;
+  constexpr uint32_t kLeafRows = 768;  // TSQR leaf height of the tall blocks
 
   size_t t0 = 0;
   while (t0 < todo.size()) {
     std::vector<BlockPlan> plans;
-    uint64_t staging = 0, wdoubles = 0;
+    uint64_t staging = 0, wdoubles = 0, planned = 0;
     size_t t1 = t0;
     for (; t1 < todo.size(); ++t1) {
       const uint64_t i1 = todo[t1];
@@ -410,8 +411,13 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       pl.n_single = hc[2 * i1 + 1];
       pl.n_rows = pl.n_multi + pl.n_single;
       pl.tall = pl.n_rows > M;
-      const uint64_t need = (pl.tall ? (uint64_t)pl.n_rows * M : 0) + (uint64_t)M * cols_pad_full + aux_sz;
-      if (!plans.empty() && (staging + wdoubles + need) * 8 > budget) break;
+      // staging + the TSQR forest (leaf R factors, then stacked pairs and their R
+      // factors alive together: <= 3 M x M per leaf) + the Jacobi slot
+      const uint64_t n_leaves = pl.tall ? ceil_div(pl.n_rows, kLeafRows) : 0;
+      const uint64_t need = (pl.tall ? (uint64_t)pl.n_rows * M + 3 * n_leaves * ((uint64_t)M * M + aux_sz) : 0) +
+                            (uint64_t)M * cols_pad_full + aux_sz;
+      if (!plans.empty() && (planned + need) * 8 > budget) break;
+      planned += need;
       pl.offset = staging;
       staging += pl.tall ? (uint64_t)pl.n_rows * M : 0;
       wdoubles += (uint64_t)M * cols_pad_full + aux_sz;
@@ -441,7 +447,6 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     // tall blocks: TSQR of T_d over row leaves of at most kLeafRows rows (factored in
     // place), pairwise tree, then W = R^T into the block's Jacobi slot
     {
-      constexpr uint32_t kLeafRows = 768;
       std::vector<std::vector<LeafRef>> trees;
       std::vector<size_t> tree_q;
       for (size_t q = 0; q < nb; ++q) {

@@ -865,3 +865,23 @@ def dev_full_svd(m: DeviceMatrix, block_count: int, method, keep: int = 0, seed:
 
 def dev_outputs_free(out):
     lib().rk_dev_outputs_free(out)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over library-owned device memory (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def dev_outputs_tensors(out):
+    """(sigma, U, V) of rk_dev_outputs as torch views of the library's HBM buffers
+    (valid until dev_outputs_free); V is None without RK_WANT_V."""
+    import torch
+    o = out.contents
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sig = torch.as_tensor(_CudaArray(o.d_sigma, (o.k_sigma,)), device=dev) if o.k_sigma else None
+    u = torch.as_tensor(_CudaArray(o.d_u, (o.rows, o.k_sigma)), device=dev) if o.k_sigma else None
+    v = torch.as_tensor(_CudaArray(o.d_v, (o.cols, o.k_v)), device=dev) if o.d_v else None
+    return sig, u, v
