@@ -69,6 +69,7 @@ struct JacobiParams {
   uint32_t g;       // columns per group (even)
   uint32_t G;       // groups (even), G * g = cols_pad
   int with_v;
+  double check_ratio;  // Gram convergence check after a sweep whose max ratio is below this (0: off)
 };
 
 __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_t n) {
@@ -94,7 +95,7 @@ __device__ __forceinline__ void rotation_cs(double ap, double aq, double gamma, 
   const float df = (float)(d * f), ef = (float)(e * f);
   const float r = sqrtf(fmaf(df, df, ef * ef));
   const float sgn = (df == 0.0f || ((df > 0.0f) == (ef > 0.0f))) ? 1.0f : -1.0f;
-  const float t = sgn * fabsf(ef) / (fabsf(df) + r);
+  const float t = sgn * __fdividef(fabsf(ef), fabsf(df) + r);  // |df| + r >= 1: no range issue
   const float c32 = rsqrtf(fmaf(t, t, 1.0f));
   double cc = (double)c32, ss = (double)(c32 * t);
   const double n = cc * cc + ss * ss;
@@ -205,7 +206,7 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      b[k] = (live && (EXACT || lq + Q * k < (int)rows)) ? pb[Q * k] : 0.0;
+      b[k] = (EXACT || lq + Q * k < (int)rows) ? pb[Q * k] : 0.0;  // frozen pairs: gamma unused
       const double pr = a[k] * b[k];
       if ((k & 3) == 0) acc0 += pr;
       else if ((k & 3) == 1) acc1 += pr;
@@ -250,6 +251,219 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
   __syncthreads();
 }
 
+// ---- convergence tail -------------------------------------------------------
+// Once the sweeps are in the quadratic regime, what is left is the rounding-noise
+// floor: a handful of pairs whose |gamma| / sqrt(alpha_p alpha_q) sits at the
+// 1e-14 threshold, rotated by tiny angles sweep after sweep until, by chance, none
+// exceeds it (the reference stops after a sweep with no rotation, svd.cpp:265). A
+// full sweep re-tests all n(n-1)/2 pairs in n-1 latency-bound rounds to rotate
+// those few. The tail instead
+//   1. tests every pair at once: W^T W by DMMA (one 32x32 block per warp across
+//      the cluster), with fresh norms and the reference's freeze and rotation
+//      rule; the violating pairs go to a list in CTA 0's shared memory (DSMEM);
+//   2. no violation: the check IS the reference's rotation-free last sweep -> done;
+//   3. a few violations: CTA 0 sorts them (deterministic order) and rotates
+//      exactly those pairs, sequentially, with fresh dots -- a sweep in which
+//      every other pair was tested and left alone -- then checks again;
+//   4. many violations: back to full sweeps.
+// Each check computes all the sweep's dot products, so it counts as a sweep.
+constexpr int kViolCap = 64;
+constexpr int kTailIters = 8;  // then back to full sweeps
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct TailShared {
+  uint32_t count;
+  uint32_t list[kViolCap];  // (q << 16) | p, p < q
+};
+
+// Step 1; returns the number of violating pairs (may exceed kViolCap). All
+// threads of the cluster call it; *freeze_out gets the fresh freeze level.
+__device__ uint32_t tail_check(cg::cluster_group& cluster, const JacobiJob& job, unsigned rank, unsigned csize,
+                               double* s_red, double* s_amax, TailShared* ts, double* worst_out) {
+  const uint32_t rows = job.rows, n = job.cols_pad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* W = job.w;
+  double* alpha_g = job.alpha;
+  for (uint32_t j = rank * kJWarps + warp; j < n; j += csize * kJWarps) {
+    const double* wj = W + (uint64_t)j * rows;
+    double a = 0.0;
+    for (uint32_t i = lane; i < rows; i += 32) {
+      const double x = __ldcg(wj + i);
+      a += x * x;
+    }
+    a = warp_sum(a);
+    if (lane == 0) alpha_g[j] = a;
+  }
+  if (rank == 0 && tid == 0) {
+    ts->count = 0;
+    job.stats[7] = 0ull;
+  }
+  cluster.sync();
+  double amax = 0.0;
+  for (uint32_t j = tid; j < n; j += kJThreads) amax = fmax(amax, __ldcg(alpha_g + j));
+  for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) s_red[warp] = amax;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kJWarps; ++w) t = fmax(t, s_red[w]);
+    *s_amax = t;
+  }
+  __syncthreads();
+  const double freeze = kJacobiTol * kJacobiTol * (*s_amax);
+  TailShared* ts0 = cluster.map_shared_rank(ts, 0);
+  const uint32_t nb = (n + 31) / 32;
+  const uint32_t T = nb * (nb + 1) / 2;
+  const int lr = lane >> 2, lc = lane & 3;
+  double worst = 0.0;
+  for (uint32_t t = rank * kJWarps + warp; t < T; t += csize * kJWarps) {
+    uint32_t bi = 0;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const uint32_t bj = t - bi * (bi + 1) / 2;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* pa[4];
+    const double* pb[4];
+    bool va[4], vb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t ca = bi * 32 + i * 8 + lr, cb = bj * 32 + i * 8 + lr;
+      va[i] = ca < n;
+      vb[i] = cb < n;
+      pa[i] = W + (uint64_t)(va[i] ? ca : 0) * rows + lc;
+      pb[i] = W + (uint64_t)(vb[i] ? cb : 0) * rows + lc;
+    }
+    for (uint32_t k0 = 0; k0 < rows; k0 += 4) {
+      const bool ok = k0 + lc < rows;
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = (ok && va[i]) ? __ldcg(pa[i] + k0) : 0.0;
+        b[i] = (ok && vb[i]) ? __ldcg(pb[i] + k0) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t r = bi * 32 + i * 8 + lr, c = bj * 32 + j * 8 + 2 * lc + e;
+          if (r < n && c < n && r > c) {
+            const double h = acc[i][j][e];
+            const double ar = __ldcg(alpha_g + r), ac = __ldcg(alpha_g + c);
+            if (ar > freeze && ac > freeze) {
+              const double q = h * h / (ar * ac);
+              worst = fmax(worst, q);
+              if (h * h > kJacobiTol * kJacobiTol * (ar * ac)) {
+                const uint32_t slot = atomicAdd(&ts0->count, 1u);
+                if (slot < (uint32_t)kViolCap) ts0->list[slot] = (r << 16) | c;
+              }
+            }
+          }
+        }
+  }
+  for (int o = 16; o; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if (lane == 0 && worst > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long*>(job.stats + 7), __double_as_longlong(worst));
+  cluster.sync();
+  const uint32_t nv = ts0->count;
+  *worst_out = sqrt(__longlong_as_double(__ldcg(reinterpret_cast<const long long*>(job.stats + 7))));
+  cluster.sync();  // every CTA has read CTA 0's count before anyone moves on
+  return nv;
+}
+
+// Step 3 (CTA 0, warp 0): rotate the listed pairs in sorted order, fresh dots.
+__device__ uint32_t tail_rotate(const JacobiJob& job, TailShared* ts, uint32_t nv, double freeze, bool with_v) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t rows = job.rows, vrows = job.cols_pad;
+  double* W = job.w;
+  double* V = job.v;
+  // rank sort of the (distinct) keys: deterministic whatever the atomic order was
+  uint32_t keys[(kViolCap + 31) / 32];
+#pragma unroll
+  for (int u = 0; u < (kViolCap + 31) / 32; ++u) {
+    const uint32_t i = u * 32 + lane;
+    keys[u] = i < nv ? ts->list[i] : 0u;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < (kViolCap + 31) / 32; ++u) {
+    const uint32_t i = u * 32 + lane;
+    if (i < nv) {
+      uint32_t rnk = 0;
+      for (uint32_t j = 0; j < nv; ++j) rnk += ts->list[j] < keys[u];
+      keys[u] = rnk;  // reuse: rank of my key
+    }
+  }
+  __syncwarp();
+  uint32_t mine[(kViolCap + 31) / 32];
+#pragma unroll
+  for (int u = 0; u < (kViolCap + 31) / 32; ++u) {
+    const uint32_t i = u * 32 + lane;
+    mine[u] = i < nv ? ts->list[i] : 0u;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < (kViolCap + 31) / 32; ++u) {
+    const uint32_t i = u * 32 + lane;
+    if (i < nv) ts->list[keys[u]] = mine[u];
+  }
+  __syncwarp();
+  uint32_t rotated = 0;
+  for (uint32_t t = 0; t < nv; ++t) {
+    const uint32_t key = ts->list[t];
+    const uint32_t q = key >> 16, p = key & 0xffffu;  // p < q
+    double* wp = W + (uint64_t)p * rows;
+    double* wq = W + (uint64_t)q * rows;
+    double ap = 0.0, aq = 0.0, gm = 0.0;
+    for (uint32_t i = lane; i < rows; i += 32) {
+      const double x = wp[i], y = wq[i];
+      ap += x * x;
+      aq += y * y;
+      gm += x * y;
+    }
+    ap = warp_sum(ap);
+    aq = warp_sum(aq);
+    gm = warp_sum(gm);
+    // the DMMA check flagged this pair; at the noise floor a sequential dot may land
+    // just under the threshold -- rotate anyway (an angle of ~1e-14) so the pass
+    // always makes progress
+    if (ap <= freeze || aq <= freeze || gm == 0.0) continue;
+    double c, sn;
+    rotation_cs(ap, aq, gm, c, sn);
+    for (uint32_t i = lane; i < rows; i += 32) {
+      const double x = wp[i], y = wq[i];
+      wp[i] = c * x - sn * y;
+      wq[i] = sn * x + c * y;
+    }
+    if (with_v) {
+      double* vp = V + (uint64_t)p * vrows;
+      double* vq = V + (uint64_t)q * vrows;
+      for (uint32_t i = lane; i < vrows; i += 32) {
+        const double x = vp[i], y = vq[i];
+        vp[i] = c * x - sn * y;
+        vq[i] = sn * x + c * y;
+      }
+    }
+    __syncwarp();
+    ++rotated;
+  }
+  return rotated;
+}
+
 template <int Q, int E, bool EXACT>
 __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
@@ -269,6 +483,7 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
   __shared__ double s_red[kJWarps];
   __shared__ double s_amax;
   __shared__ unsigned long long s_rot;
+  __shared__ TailShared s_tail;
 
   unsigned long long* counters = reinterpret_cast<unsigned long long*>(job.stats + 4);  // rotations per sweep, mod 3
   double* W = job.w;
@@ -399,6 +614,26 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
     if (rank == 0 && tid == 0) job.stats[3] = 0ull;
     if (rot == 0) converged = 1;
     cluster.sync();
+    // quadratic regime: the convergence tail (see tail_check)
+    if (!converged && last_max_ratio < P.check_ratio) {
+      for (int it = 0; it < kTailIters && sweep + 1 < kMaxSweeps; ++it) {
+        double worst = 0.0;
+        const uint32_t nv = tail_check(cluster, job, rank, csize, s_red, &s_amax, &s_tail, &worst);
+        last_max_ratio = worst;
+        if (nv == 0) {  // the rotation-free sweep: converged
+          converged = 1;
+          ++sweep;
+          break;
+        }
+        if (nv > (uint32_t)kViolCap) break;  // back to full sweeps
+        if (rank == 0 && warp == 0) {
+          const uint32_t r = tail_rotate(job, &s_tail, nv, kJacobiTol * kJacobiTol * s_amax, with_v);
+          total_rot += r;
+        }
+        ++sweep;
+        cluster.sync();
+      }
+    }
   }
   if (rank == 0 && tid == 0) {
     job.stats[0] = (uint64_t)sweep;
@@ -652,7 +887,11 @@ void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, 
     const long v = e ? std::strtol(e, nullptr, 10) : 16;
     return (uint32_t)std::max<long>(2, std::min<long>(32, v & ~1L));
   }();
-  for (uint32_t gmax = gcap; gmax >= 2; gmax -= 2) {
+  // columns longer than 16 lanes x 32 registers: 8 groups of 32 lanes keep the A
+  // column in registers (E <= 32); without the cap the plan falls back to the
+  // shared-memory rounds (E = 0), several times slower
+  const uint32_t gtop = (rows > 16 * 32 && rows <= 32 * 32 && !with_v) ? std::min<uint32_t>(gcap, 8) : gcap;
+  for (uint32_t gmax = gtop; gmax >= 2; gmax -= 2) {
     G = (uint32_t)ceil_div(cols ? cols : 1, gmax);
     if (G < 2) G = 2;
     if (G & 1) ++G;
@@ -704,7 +943,8 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   cl = p2;
   DBuf<JacobiJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
-  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0};
+  const char* ce = std::getenv("RK_JACOBI_CHECK");
+  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : 1e-7};
   void* kargs[] = {&P};
   // lanes per pair: enough lane groups for the g pairs of a round; E = column
   // elements per lane held in registers by the cross rounds (0: shared-memory path)
