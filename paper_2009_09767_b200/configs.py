@@ -24,7 +24,7 @@ VAL_ONE, VAL_UNIFORM_PM1, VAL_NORMAL, VAL_UNIFORM_01 = 0, 1, 2, 3
 
 def build_gen() -> str:
     if not os.path.exists(GEN_SO) or os.path.getmtime(GEN_SO) < os.path.getmtime(GEN_SRC):
-        subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-o", GEN_SO, GEN_SRC, "-lm"], check=True)
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", GEN_SO, GEN_SRC, "-lm"], check=True)
     return GEN_SO
 
 
@@ -44,6 +44,8 @@ def _lib():
         L.rkg_zipf_mean.restype = dbl
         L.rkg_synth_bipartite.argtypes = [u64, u64, dbl, u64, C.POINTER(u64)]
         L.rkg_synth_bipartite.restype = C.c_void_p
+        L.rkg_planted.argtypes = [u64, u64, dbl, u64, dbl, dbl, u64, C.POINTER(u64)]
+        L.rkg_planted.restype = C.c_void_p
         L.rkg_free.argtypes = [C.c_void_p]
         _gen = L
     return _gen
@@ -83,6 +85,16 @@ def synth_bipartite(rows, cols, density, seed) -> SparseMatrix:
     return SparseMatrix._trusted(rows, cols, _take(p, n.value))
 
 
+def planted(rows, cols, density, k, decay, noise, seed) -> SparseMatrix:
+    """c5's planted spectrum: mask(density) o (P diag(decay^j) Q^T) + noise N(0,1) on
+    the nonzeros, P (rows x k) and Q (cols x k) orthonormal from seeded Gaussians."""
+    n = C.c_uint64()
+    p = _lib().rkg_planted(rows, cols, density, k, decay, noise, seed, C.byref(n))
+    if not p:
+        raise MemoryError("planted generator failed")
+    return SparseMatrix._trusted(rows, cols, _take(p, n.value))
+
+
 @dataclass(frozen=True)
 class Config:
     name: str
@@ -106,7 +118,9 @@ class Config:
             return zipf(self.rows, n, 0.002 * self.rows, 1.1, VAL_UNIFORM_01, self.seed)
         if self.name == "c4":
             return uniform(self.rows, n, 0.001, VAL_NORMAL, self.seed)
-        raise NotImplementedError(f"generator for {self.name} is not built yet")
+        if self.name == "c5":
+            return planted(self.rows, n, 0.0005, 64, 0.9, 1e-6, self.seed)
+        raise ValueError(f"unknown config {self.name}")
 
 
 CONFIGS = {
@@ -121,5 +135,6 @@ CONFIGS = {
     "c4": Config("c4", 1024, 16777216, 1024, "neighbor-random", 3, 0, 0,
                  "M=1024 N=16777216 0.1% uniform N(0,1) seed 3, 1024 blocks, NeighborRandomChecker"),
     "c5": Config("c5", 2048, 67108864, 4096, "neighbor-random", 4, 64, 64,
-                 "planted spectrum M=2048 N=67108864, 4096 blocks, NeighborRandomChecker, top-64"),
+                 "planted spectrum M=2048 N=67108864: mask(0.05% uniform, seed 4) o (P diag(0.9^k) Q^T) + 1e-6 N(0,1), "
+                 "P, Q orthonormal (k=64) from seeded Gaussians; 4096 blocks, NeighborRandomChecker, keep 64, top-64"),
 }

@@ -190,3 +190,177 @@ rkg_entry* rkg_synth_bipartite(uint64_t rows, uint64_t cols, double density, uin
   *n_out = v.n;
   return v.e;
 }
+
+/* ---------------------------------------------------------------------------
+ * c5: planted spectrum. P (rows x k) and Q (cols x k) have orthonormal columns,
+ * obtained from seeded Gaussians by Cholesky QR (Q = G R^-1 with R = chol(G^T G);
+ * P the same, twice); sigma_j = decay^j. A = mask o (P diag(sigma) Q^T) + noise *
+ * N(0,1) on the nonzeros, the mask being uniform positions of the given density.
+ * Since Q_c = G_c R^-1, A_ic = G_c . H_i with H = P diag(sigma) R^-T, so Q is
+ * never stored: row c of G is regenerated from KeyedRng(seed, 'Q', c) for every
+ * nonzero of column c. G^T G is accumulated over fixed chunks of rows and summed
+ * in chunk order, so the result does not depend on the number of threads.
+ * ------------------------------------------------------------------------- */
+enum { TAG_P = 0x50, TAG_Q = 0x51, TAG_NOISE = 0x4e4f4953 };
+
+static void gauss_row(uint64_t seed, uint64_t tag, uint64_t idx, uint64_t k, double* out) {
+  rng_t g = rng_make(seed, tag, idx);
+  for (uint64_t j = 0; j < k; j += 2) {
+    double u1, u2;
+    do { u1 = rng_unit(&g); } while (u1 <= 0.0);
+    u2 = rng_unit(&g);
+    const double r = sqrt(-2.0 * log(u1));
+    out[j] = r * cos(6.283185307179586 * u2);
+    if (j + 1 < k) out[j + 1] = r * sin(6.283185307179586 * u2);
+  }
+}
+
+/* in place: S (k x k, row-major, symmetric positive definite) -> upper R, S = R^T R */
+static int chol_upper(double* S, uint64_t k) {
+  for (uint64_t i = 0; i < k; ++i) {
+    double d = S[i * k + i];
+    for (uint64_t p = 0; p < i; ++p) d -= S[p * k + i] * S[p * k + i];
+    if (!(d > 0.0)) return -1;
+    d = sqrt(d);
+    S[i * k + i] = d;
+    for (uint64_t j = i + 1; j < k; ++j) {
+      double x = S[i * k + j];
+      for (uint64_t p = 0; p < i; ++p) x -= S[p * k + i] * S[p * k + j];
+      S[i * k + j] = x / d;
+    }
+    for (uint64_t j = 0; j < i; ++j) S[i * k + j] = 0.0;
+  }
+  return 0;
+}
+
+/* inverse of an upper-triangular R (row-major), in place */
+static void inv_upper(double* R, uint64_t k) {
+  double* X = (double*)calloc(k * k, sizeof(double));
+  for (uint64_t j = 0; j < k; ++j) {  /* column j of R^-1: solve R x = e_j */
+    for (int64_t i = (int64_t)j; i >= 0; --i) {
+      double s = (i == (int64_t)j) ? 1.0 : 0.0;
+      for (uint64_t p = (uint64_t)i + 1; p <= j; ++p) s -= R[i * k + p] * X[p * k + j];
+      X[i * k + j] = s / R[i * k + i];
+    }
+  }
+  memcpy(R, X, k * k * sizeof(double));
+  free(X);
+}
+
+/* Gram of the Gaussian rows [0, n) of stream `tag`: chunked, deterministic */
+static void gauss_gram(uint64_t seed, uint64_t tag, uint64_t n, uint64_t k, double* S) {
+  const uint64_t chunk = 1ull << 15;
+  const uint64_t nc = (n + chunk - 1) / chunk;
+  double* part = (double*)calloc(nc * k * k, sizeof(double));
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t c = 0; c < (int64_t)nc; ++c) {
+    double* row = (double*)malloc(k * sizeof(double));
+    double* acc = part + (uint64_t)c * k * k;
+    const uint64_t r1 = ((uint64_t)c + 1) * chunk < n ? ((uint64_t)c + 1) * chunk : n;
+    for (uint64_t r = (uint64_t)c * chunk; r < r1; ++r) {
+      gauss_row(seed, tag, r, k, row);
+      for (uint64_t i = 0; i < k; ++i) {
+        const double x = row[i];
+        for (uint64_t j = i; j < k; ++j) acc[i * k + j] += x * row[j];
+      }
+    }
+    free(row);
+  }
+  memset(S, 0, k * k * sizeof(double));
+  for (uint64_t c = 0; c < nc; ++c)
+    for (uint64_t i = 0; i < k; ++i)
+      for (uint64_t j = i; j < k; ++j) S[i * k + j] += part[c * k * k + i * k + j];
+  for (uint64_t i = 0; i < k; ++i)
+    for (uint64_t j = 0; j < i; ++j) S[i * k + j] = S[j * k + i];
+  free(part);
+}
+
+rkg_entry* rkg_planted(uint64_t rows, uint64_t cols, double density, uint64_t k, double decay, double noise,
+                       uint64_t seed, uint64_t* n_out) {
+  *n_out = 0;
+  if (k == 0 || k > rows || k > cols) return NULL;
+  /* P: rows x k, orthonormal columns (Cholesky QR applied twice) */
+  double* P = (double*)malloc(rows * k * sizeof(double));
+  for (uint64_t r = 0; r < rows; ++r) gauss_row(seed, TAG_P, r, k, P + r * k);
+  double* S = (double*)malloc(k * k * sizeof(double));
+  double* T = (double*)malloc(rows * k * sizeof(double));
+  for (int pass = 0; pass < 2; ++pass) {
+    memset(S, 0, k * k * sizeof(double));
+    for (uint64_t r = 0; r < rows; ++r)
+      for (uint64_t i = 0; i < k; ++i)
+        for (uint64_t j = 0; j < k; ++j) S[i * k + j] += P[r * k + i] * P[r * k + j];
+    if (chol_upper(S, k)) { free(P); free(S); free(T); return NULL; }
+    inv_upper(S, k);
+    for (uint64_t r = 0; r < rows; ++r)
+      for (uint64_t j = 0; j < k; ++j) {
+        double x = 0.0;
+        for (uint64_t i = 0; i <= j; ++i) x += P[r * k + i] * S[i * k + j];
+        T[r * k + j] = x;
+      }
+    memcpy(P, T, rows * k * sizeof(double));
+  }
+  free(T);
+  /* Q = G R^-1 with G^T G = R^T R */
+  gauss_gram(seed, TAG_Q, cols, k, S);
+  if (chol_upper(S, k)) { free(P); free(S); return NULL; }
+  inv_upper(S, k); /* S = R^-1 (upper) */
+  /* H = P diag(sigma) R^-T : H[i][l] = sum_j Rinv[l][j] sigma_j P[i][j] */
+  double* H = (double*)calloc(rows * k, sizeof(double));
+  double sig = 1.0;
+  double* sigma = (double*)malloc(k * sizeof(double));
+  for (uint64_t j = 0; j < k; ++j) { sigma[j] = sig; sig *= decay; }
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t l = 0; l < k; ++l) {
+      double x = 0.0;
+      for (uint64_t j = l; j < k; ++j) x += S[l * k + j] * sigma[j] * P[i * k + j];
+      H[i * k + l] = x;
+    }
+  free(P); free(S); free(sigma);
+  /* mask positions per row (geometric skipping); counts first, then values */
+  const double lq = log1p(-density);
+  uint64_t* cnt = (uint64_t*)calloc(rows + 1, sizeof(uint64_t));
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < (int64_t)rows; ++r) {
+    rng_t g = rng_make(seed, TAG_POS, (uint64_t)r);
+    int64_t c = -1;
+    uint64_t n = 0;
+    for (;;) {
+      const double gap = floor(log1p(-rng_unit(&g)) / lq);
+      if (!(gap < (double)cols)) break;
+      c += (int64_t)gap + 1;
+      if ((uint64_t)c >= cols) break;
+      ++n;
+    }
+    cnt[r + 1] = n;
+  }
+  for (uint64_t r = 0; r < rows; ++r) cnt[r + 1] += cnt[r];
+  const uint64_t nnz = cnt[rows];
+  rkg_entry* out = (rkg_entry*)malloc((nnz ? nnz : 1) * sizeof(rkg_entry));
+  if (!out) { free(H); free(cnt); return NULL; }
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < (int64_t)rows; ++r) {
+    rng_t g = rng_make(seed, TAG_POS, (uint64_t)r);
+    rng_t gn = rng_make(seed, TAG_NOISE, (uint64_t)r);
+    double* grow = (double*)malloc(k * sizeof(double));
+    const double* h = H + (uint64_t)r * k;
+    int64_t c = -1;
+    uint64_t o = cnt[r];
+    for (;;) {
+      const double gap = floor(log1p(-rng_unit(&g)) / lq);
+      if (!(gap < (double)cols)) break;
+      c += (int64_t)gap + 1;
+      if ((uint64_t)c >= cols) break;
+      gauss_row(seed, TAG_Q, (uint64_t)c, k, grow);
+      double x = 0.0;
+      for (uint64_t l = 0; l < k; ++l) x += h[l] * grow[l];
+      x += noise * draw_value(&gn, VAL_NORMAL);
+      if (x == 0.0) x = noise;  /* keep the mask exact (probability ~0) */
+      out[o].row = (uint64_t)r; out[o].col = (uint64_t)c; out[o].value = x;
+      ++o;
+    }
+    free(grow);
+  }
+  free(H); free(cnt);
+  *n_out = nnz;
+  return out;
+}

@@ -112,3 +112,24 @@ def test_c2_shape_and_planted_rows():
     e = a.entries()
     v = e["value"]
     assert abs(v.mean()) < 0.01 and abs(v.std() - 1) < 0.01  # N(0,1)
+
+
+def test_planted_generator_spectrum():
+    """c5 generator: with a full mask and no noise A = P diag(0.9^k) Q^T exactly,
+    so its singular values are 0.9^k (k < 64) and ~0 after; deterministic; the
+    mask density and the noise level follow the spec."""
+    a = configs.planted(128, 4096, 1.0, 64, 0.9, 0.0, 7)
+    assert a.nnz() == 128 * 4096
+    s = np.linalg.svd(a.to_dense(), compute_uv=False)
+    assert np.abs(s[:64] - 0.9 ** np.arange(64)).max() < 1e-13
+    assert s[64] < 1e-13
+    b = configs.planted(256, 65536, 0.0005, 64, 0.9, 1e-6, 4)
+    assert np.array_equal(b.entries(), configs.planted(256, 65536, 0.0005, 64, 0.9, 1e-6, 4).entries())
+    assert abs(b.nnz() / (256 * 65536) - 0.0005) < 0.00005
+    r, c, v = b.coo()
+    assert np.all(v != 0) and np.all(np.diff(r.astype(np.int64)) >= 0)
+    # the noise is additive on the same mask: the difference of two noise levels is noise
+    z0 = configs.planted(64, 8192, 0.01, 64, 0.9, 0.0, 3)
+    z1 = configs.planted(64, 8192, 0.01, 64, 0.9, 1e-6, 3)
+    assert np.array_equal(z0.coo()[1], z1.coo()[1])
+    assert 0.5e-6 < np.std(z1.coo()[2] - z0.coo()[2]) < 2e-6
