@@ -70,6 +70,7 @@ struct JacobiParams {
   uint32_t G;       // groups (even), G * g = cols_pad
   int with_v;
   double check_ratio;  // Gram convergence check after a sweep whose max ratio is below this (0: off)
+  int check_first;     // start with the tail check (W comes from jacobi_warp_kernel)
 };
 
 __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_t n) {
@@ -464,6 +465,25 @@ __device__ uint32_t tail_rotate(const JacobiJob& job, TailShared* ts, uint32_t n
   return rotated;
 }
 
+// The tail loop: each check counts as a sweep (`done` = completed sweeps).
+// Returns true once a check finds no pair to rotate.
+__device__ bool run_tail(cg::cluster_group& cluster, const JacobiJob& job, unsigned rank, unsigned csize,
+                         double* s_red, double* s_amax, TailShared* s_tail, bool with_v, int& done,
+                         unsigned long long& total_rot, double& last_max_ratio) {
+  const int warp = threadIdx.x >> 5;
+  for (int it = 0; it < kTailIters && done < kMaxSweeps; ++it) {
+    double worst = 0.0;
+    const uint32_t nv = tail_check(cluster, job, rank, csize, s_red, s_amax, s_tail, &worst);
+    last_max_ratio = worst;
+    ++done;
+    if (nv == 0) return true;                    // the rotation-free sweep
+    if (nv > (uint32_t)kViolCap) return false;   // back to full sweeps
+    if (rank == 0 && warp == 0) total_rot += tail_rotate(job, s_tail, nv, kJacobiTol * kJacobiTol * (*s_amax), with_v);
+    cluster.sync();
+  }
+  return false;
+}
+
 template <int Q, int E, bool EXACT>
 __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
@@ -496,6 +516,16 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
   double last_max_ratio = 0.0;
   int converged = (job.cols < 2);
   int sweep = 0;
+  if (P.check_first && !converged) {
+    // continuing after the Gram-assisted warp kernel: certify on W first
+    sweep = (int)job.stats[0];
+    total_rot = job.stats[1];
+    int done = sweep;
+    converged = run_tail(cluster, job, rank, csize, s_red, &s_amax, &s_tail, with_v, done, total_rot,
+                         last_max_ratio);
+    sweep = done;
+    cluster.sync();
+  }
   for (; sweep < kMaxSweeps && !converged; ++sweep) {
     // ---- column norms (fresh each sweep, svd.cpp:222-226) ----
     for (uint32_t j = rank * kJWarps + warp; j < cols_pad; j += csize * kJWarps) {
@@ -615,24 +645,11 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
     if (rot == 0) converged = 1;
     cluster.sync();
     // quadratic regime: the convergence tail (see tail_check)
-    if (!converged && last_max_ratio < P.check_ratio) {
-      for (int it = 0; it < kTailIters && sweep + 1 < kMaxSweeps; ++it) {
-        double worst = 0.0;
-        const uint32_t nv = tail_check(cluster, job, rank, csize, s_red, &s_amax, &s_tail, &worst);
-        last_max_ratio = worst;
-        if (nv == 0) {  // the rotation-free sweep: converged
-          converged = 1;
-          ++sweep;
-          break;
-        }
-        if (nv > (uint32_t)kViolCap) break;  // back to full sweeps
-        if (rank == 0 && warp == 0) {
-          const uint32_t r = tail_rotate(job, &s_tail, nv, kJacobiTol * kJacobiTol * s_amax, with_v);
-          total_rot += r;
-        }
-        ++sweep;
-        cluster.sync();
-      }
+    if (!converged && last_max_ratio < P.check_ratio && sweep + 1 < kMaxSweeps) {
+      int done = sweep + 1;
+      converged = run_tail(cluster, job, rank, csize, s_red, &s_amax, &s_tail, with_v, done, total_rot,
+                           last_max_ratio);
+      sweep = done - 1;  // the loop increment counts it
     }
   }
   if (rank == 0 && tid == 0) {
@@ -640,6 +657,327 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
     job.stats[1] = total_rot;
     job.stats[2] = converged ? 0ull : 1ull;
     job.stats[3] = (uint64_t)__double_as_longlong(last_max_ratio);
+  }
+}
+
+// ===========================================================================
+// Gram-assisted warp Jacobi (matrices accepted on the Gram route, kappa bounded)
+// ===========================================================================
+// The same tournament over groups of kWG = 8 columns, but one WARP owns a group
+// pair for a whole step:
+//   1. H = X^T X (16 x 16, X = the pair's 16 columns) by DMMA straight from W;
+//   2. the step's rounds (intra-group rounds in step 0, then 8 cross rounds) on H
+//      in the warp's shared memory -- a rotation of columns (p, q) is the two-sided
+//      update H <- J^T H J (rows, then columns) -- with the reference's decision
+//      rule and formulas on H's entries, accumulating Z = J_1 J_2 ... in registers;
+//   3. X <- X Z by DMMA, back into W.
+// The only barrier is one per step among the matrix's warps (a cluster of G/16
+// CTAs), and the M-long work runs on the tensor cores. H is formed afresh every
+// step and only the step's rotations are applied to it, so for the kappa the Gram
+// route admits its rounding stays far below the 1e-14 rotation threshold. Once a
+// sweep's largest |gamma| / sqrt(alpha_p alpha_q) is in the quadratic regime the
+// kernel hands over to jacobi_cluster_kernel, which certifies convergence on W
+// itself (tail_check) -- the reference's stopping rule.
+constexpr int kWG = 8, kWN = 16, kWS = 17;
+
+struct WarpParams {
+  const JacobiJob* jobs;
+  uint32_t G;         // groups of kWG columns (even), G * kWG = cols_pad
+  double stop_ratio;  // hand over once a sweep's max ratio is below this
+};
+
+template <int KIND, int R>  // KIND 0: cross round R; 1: intra-group round R
+__device__ __forceinline__ void round_pair(int i, int& p, int& q) {
+  if (KIND == 0) {
+    p = i;
+    q = 8 + ((i + R) & 7);
+  } else {
+    const int grp = i >> 2, t = i & 3;
+    const int a = t, b = 7 - t;
+    p = grp * 8 + (a == 0 ? 0 : 1 + (a - 1 + R) % 7);
+    q = grp * 8 + (b == 0 ? 0 : 1 + (b - 1 + R) % 7);
+  }
+}
+
+template <int KIND, int R>
+__device__ __forceinline__ void warp_round(double* sH, double* sCS, double (&z)[kWN], double freeze, double& max_r2,
+                                           uint32_t& nrot) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 8) {
+    int p, q;
+    round_pair<KIND, R>(lane, p, q);
+    const double ap = sH[p * kWS + p], aq = sH[q * kWS + q], gm = sH[p * kWS + q];
+    double c = 1.0, sn = 0.0;
+    const bool live = !(ap <= freeze || aq <= freeze);
+    const double prod = ap * aq, g2 = gm * gm;
+    if (live && g2 > max_r2 * prod) max_r2 = g2 / prod;
+    if (live && g2 > kJacobiTol * kJacobiTol * prod) {
+      rotation_cs(ap, aq, gm, c, sn);
+      ++nrot;
+    }
+    sCS[2 * lane] = c;
+    sCS[2 * lane + 1] = sn;
+  }
+  __syncwarp();
+  double cs[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cs[i] = sCS[i];
+  if (lane < kWN) {  // rows p, q of H; lane owns column `lane`
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int p, q;
+      round_pair<KIND, R>(i, p, q);
+      const double x = sH[p * kWS + lane], y = sH[q * kWS + lane];
+      sH[p * kWS + lane] = cs[2 * i] * x - cs[2 * i + 1] * y;
+      sH[q * kWS + lane] = cs[2 * i + 1] * x + cs[2 * i] * y;
+    }
+  } else {  // Z <- Z J; lane owns row lane - 16
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int p, q;
+      round_pair<KIND, R>(i, p, q);
+      const double x = z[p], y = z[q];
+      z[p] = cs[2 * i] * x - cs[2 * i + 1] * y;
+      z[q] = cs[2 * i + 1] * x + cs[2 * i] * y;
+    }
+  }
+  __syncwarp();
+  if (lane < kWN) {  // columns p, q of H; lane owns row `lane`
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int p, q;
+      round_pair<KIND, R>(i, p, q);
+      const double x = sH[lane * kWS + p], y = sH[lane * kWS + q];
+      sH[lane * kWS + p] = cs[2 * i] * x - cs[2 * i + 1] * y;
+      sH[lane * kWS + q] = cs[2 * i + 1] * x + cs[2 * i] * y;
+    }
+  }
+  __syncwarp();
+}
+
+// H = X^T X for the 16 columns cA..cA+7, cB..cB+7 of W (column-major, ld rows)
+__device__ __forceinline__ void warp_gram(const double* __restrict__ W, uint32_t rows, uint32_t cA, uint32_t cB,
+                                          double* sH) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  const double* pa = W + (uint64_t)(cA + lr) * rows + lc;
+  const double* pb = W + (uint64_t)(cB + lr) * rows + lc;
+  double h[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) h[i] = 0.0;
+  uint32_t k0 = 0;
+  // 8 k-steps per batch: 16 loads in flight before the 24 DMMAs that use them
+  for (; k0 + 32 <= rows; k0 += 32) {
+    double a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[u] = __ldcg(pa + k0 + 4 * u);
+      b[u] = __ldcg(pb + k0 + 4 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int o = (u & 1) * 6;
+      dmma884(h[o], h[o + 1], a[u], a[u]);
+      dmma884(h[o + 2], h[o + 3], b[u], a[u]);
+      dmma884(h[o + 4], h[o + 5], b[u], b[u]);
+    }
+  }
+  for (; k0 + 8 <= rows; k0 += 8) {
+    const double a0 = __ldcg(pa + k0), b0 = __ldcg(pb + k0), a1 = __ldcg(pa + k0 + 4), b1 = __ldcg(pb + k0 + 4);
+    dmma884(h[0], h[1], a0, a0);
+    dmma884(h[2], h[3], b0, a0);
+    dmma884(h[4], h[5], b0, b0);
+    dmma884(h[6], h[7], a1, a1);
+    dmma884(h[8], h[9], b1, a1);
+    dmma884(h[10], h[11], b1, b1);
+  }
+  for (; k0 < rows; k0 += 4) {
+    const bool ok = k0 + lc < rows;
+    const double a0 = ok ? __ldcg(pa + k0) : 0.0, b0 = ok ? __ldcg(pb + k0) : 0.0;
+    dmma884(h[0], h[1], a0, a0);
+    dmma884(h[2], h[3], b0, a0);
+    dmma884(h[4], h[5], b0, b0);
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int j = 2 * lc + e;
+    const double t00 = h[e] + h[6 + e], t10 = h[2 + e] + h[8 + e], t11 = h[4 + e] + h[10 + e];
+    sH[lr * kWS + j] = t00;              // (A, A)
+    sH[(8 + lr) * kWS + j] = t10;        // (B, A)
+    sH[j * kWS + 8 + lr] = t10;          // (A, B) mirror
+    sH[(8 + lr) * kWS + 8 + j] = t11;    // (B, B)
+  }
+  __syncwarp();
+}
+
+// X <- X Z (Z from the warp's shared memory, row-major 16 x 16)
+__device__ __forceinline__ void warp_xz(double* __restrict__ W, uint32_t rows, uint32_t cA, uint32_t cB,
+                                        const double* sZ) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double bf[4][2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[kc][nt] = sZ[(4 * kc + lc) * kWN + 8 * nt + lr];
+  const double* src[4];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) {
+    const int t = 4 * kc + lc;
+    src[kc] = W + (uint64_t)(t < kWG ? cA + t : cB + t - kWG) * rows;
+  }
+  double* dst[2][2];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int t = 8 * nt + 2 * lc + e;
+      dst[nt][e] = W + (uint64_t)(t < kWG ? cA + t : cB + t - kWG) * rows;
+    }
+  // 4 row blocks per batch: 16 loads in flight
+  constexpr int kRB = 4;
+  for (uint32_t r0 = 0; r0 < rows; r0 += 8 * kRB) {
+    double af[kRB][4];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      const uint32_t r = r0 + 8 * u + lr;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) af[u][kc] = r < rows ? __ldcg(src[kc] + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      const uint32_t r = r0 + 8 * u + lr;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) dmma884(d0, d1, af[u][kc], bf[kc][nt]);
+        if (r < rows) {
+          dst[nt][0][r] = d0;
+          dst[nt][1][r] = d1;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
+  const JacobiJob job = P.jobs[blockIdx.x / csize];
+  const uint32_t rows = job.rows, cols_pad = job.cols_pad, G = P.G, npairs = G / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double sH[kJWarps][kWN * kWS];
+  __shared__ double sZ[kJWarps][kWN * kWN];
+  __shared__ double sCS[kJWarps][16];
+  __shared__ double s_red[kJWarps];
+  __shared__ double s_amax;
+  __shared__ unsigned long long s_rot;
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(job.stats + 4);
+  double* W = job.w;
+  double* alpha_g = job.alpha;
+  const uint32_t w = rank * kJWarps + warp;  // this warp's pair slot
+
+  unsigned long long total_rot = 0;
+  double last_max_ratio = 0.0;
+  int converged = (job.cols < 2);
+  int sweep = 0;
+  for (; sweep < kMaxSweeps && !converged; ++sweep) {
+    for (uint32_t j = rank * kJWarps + warp; j < cols_pad; j += csize * kJWarps) {
+      const double* wj = W + (uint64_t)j * rows;
+      double a = 0.0;
+      for (uint32_t i = lane; i < rows; i += 32) {
+        const double x = __ldcg(wj + i);
+        a += x * x;
+      }
+      a = warp_sum(a);
+      if (lane == 0) alpha_g[j] = a;
+    }
+    if (rank == 0 && tid == 0) counters[(sweep + 1) % 3] = 0ull;
+    cluster.sync();
+    double amax = 0.0;
+    for (uint32_t j = tid; j < cols_pad; j += kJThreads) amax = fmax(amax, __ldcg(alpha_g + j));
+    for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) s_red[warp] = amax;
+    if (tid == 0) s_rot = 0ull;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < kJWarps; ++i) t = fmax(t, s_red[i]);
+      s_amax = t;
+    }
+    __syncthreads();
+    const double freeze = kJacobiTol * kJacobiTol * s_amax;
+    uint32_t nrot = 0;
+    double max_r2 = 0.0;
+    for (uint32_t step = 0; step + 1 < G; ++step) {
+      if (w < npairs) {
+        const uint32_t cA = rr_slot(w, step, G) * kWG, cB = rr_slot(G - 1 - w, step, G) * kWG;
+        double* h = sH[warp];
+        warp_gram(W, rows, cA, cB, h);
+        double z[kWN];
+#pragma unroll
+        for (int k = 0; k < kWN; ++k) z[k] = (k == lane - 16) ? 1.0 : 0.0;
+        if (step == 0) {
+          warp_round<1, 0>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 1>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 2>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 3>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 4>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 5>(h, sCS[warp], z, freeze, max_r2, nrot);
+          warp_round<1, 6>(h, sCS[warp], z, freeze, max_r2, nrot);
+        }
+        warp_round<0, 0>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 1>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 2>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 3>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 4>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 5>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 6>(h, sCS[warp], z, freeze, max_r2, nrot);
+        warp_round<0, 7>(h, sCS[warp], z, freeze, max_r2, nrot);
+        if (lane >= kWN) {
+#pragma unroll
+          for (int k = 0; k < kWN; ++k) sZ[warp][(lane - kWN) * kWN + k] = z[k];
+        }
+        __syncwarp();
+        warp_xz(W, rows, cA, cB, sZ[warp]);
+      }
+      cluster.sync();
+    }
+    // rotations and the largest ratio of the sweep, over the cluster
+    unsigned long long r64 = nrot;
+    for (int o = 16; o; o >>= 1) {
+      r64 += __shfl_xor_sync(0xffffffffu, r64, o);
+      max_r2 = fmax(max_r2, __shfl_xor_sync(0xffffffffu, max_r2, o));
+    }
+    if (lane == 0) {
+      if (r64) atomicAdd(&s_rot, r64);
+      s_red[warp] = max_r2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < kJWarps; ++i) t = fmax(t, s_red[i]);
+      if (s_rot) atomicAdd(&counters[sweep % 3], s_rot);
+      atomicMax(reinterpret_cast<unsigned long long*>(job.stats + 3), __double_as_longlong(sqrt(t)));
+    }
+    cluster.sync();
+    const unsigned long long rot = __ldcg(&counters[sweep % 3]);
+    total_rot += rot;
+    last_max_ratio = __longlong_as_double(__ldcg(reinterpret_cast<long long*>(job.stats + 3)));
+    cluster.sync();
+    if (rank == 0 && tid == 0) job.stats[3] = 0ull;
+    if (rot == 0 || last_max_ratio < P.stop_ratio) {
+      ++sweep;
+      break;
+    }
+    cluster.sync();
+  }
+  cluster.sync();
+  if (rank == 0 && tid == 0) {
+    job.stats[0] = (uint64_t)sweep;
+    job.stats[1] = total_rot;
+    job.stats[2] = 0ull;
+    job.stats[3] = (uint64_t)__double_as_longlong(last_max_ratio);
+    job.stats[4] = job.stats[5] = job.stats[6] = 0ull;
   }
 }
 
@@ -926,10 +1264,29 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // RK_JACOBI_GRAM=1 / RK_JACOBI_DIRECT=1 force either kernel (tuning)
   bool all_gram = !with_v && !std::getenv("RK_JACOBI_DIRECT");
   for (const JacobiJob& j : jobs) all_gram = all_gram && j.gram_ok;
+  // Gram-route matrices: Gram-assisted warp Jacobi, then the direct kernel
+  // certifies convergence on W (check_first)
+  // (measured on c2: 7.30 ms vs 7.23 ms for the direct kernel on the 64 blocks and
+  // 2x slower on the single merge matrix -- the L2 latency of streaming X twice per
+  // step is not hidden at 8 warps per SM -- so it is opt-in: RK_JACOBI_WARP=1)
+  const char* we = std::getenv("RK_JACOBI_WARP");
+  bool use_warp = we && we[0] == '1' && !with_v && cols_pad % 16 == 0 && cols_pad / 16 <= 64;
+  for (const JacobiJob& j : jobs) use_warp = use_warp && j.gram_ok;
+  if (use_warp) {
+    const char* ce0 = std::getenv("RK_JACOBI_CHECK");
+    WarpParams WP{nullptr, cols_pad / kWG, ce0 ? std::strtod(ce0, nullptr) : 1e-7};
+    DBuf<JacobiJob> djw(jobs.size(), s);
+    to_device(djw.get(), jobs.data(), jobs.size(), s);
+    WP.jobs = djw.get();
+    void* wargs[] = {&WP};
+    const unsigned wcl = (unsigned)ceil_div(cols_pad / 16, kJWarps);
+    RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_warp_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    launch_cluster_kernel((const void*)jacobi_warp_kernel, (unsigned)jobs.size() * wcl, wcl, kJThreads, 0, s, wargs);
+  }
   int q_direct = 32;
   while (q_direct > 8 && (kJThreads / q_direct) < (int)g) q_direct /= 2;
   const bool long_columns = rows > (uint32_t)(32 * q_direct) || std::getenv("RK_JACOBI_GRAM");
-  if (all_gram && long_columns && jacobi_gram_supported(rows, g, smem_optin)) {
+  if (!use_warp && all_gram && long_columns && jacobi_gram_supported(rows, g, smem_optin)) {
     jacobi_gram_batched(jobs, g, G, s, sms);
     return;
   }
@@ -944,7 +1301,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   DBuf<JacobiJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   const char* ce = std::getenv("RK_JACOBI_CHECK");
-  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : 1e-7};
+  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : 1e-7, use_warp ? 1 : 0};
   void* kargs[] = {&P};
   // lanes per pair: enough lane groups for the g pairs of a round; E = column
   // elements per lane held in registers by the cross rounds (0: shared-memory path)
