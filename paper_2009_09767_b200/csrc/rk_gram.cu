@@ -141,7 +141,7 @@ __global__ void reduce_partials(const double* __restrict__ partial, uint32_t n_c
 constexpr int kCT = 256;
 constexpr int kCB = 32;  // panel width
 
-__global__ void __launch_bounds__(kCT, 2) cholesky_kernel(double* const* __restrict__ mats, uint32_t M,
+__global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restrict__ mats, uint32_t M,
                                                           uint32_t* __restrict__ status,
                                                           double* __restrict__ diag_ratio) {
   extern __shared__ __align__(16) double sm[];
@@ -162,29 +162,43 @@ __global__ void __launch_bounds__(kCT, 2) cholesky_kernel(double* const* __restr
     }
     __syncthreads();
     if (warp == 0) {
-      for (uint32_t j = 0; j < nb; ++j) {
-        double piv = D[j + j * kCB];
-        if (!(piv > 0.0)) {
-          if (lane == 0) s_bad = 1;
-          piv = 1.0;
+      // lane i holds row i of the diagonal block in registers; column j: pivot by
+      // shuffle, scale, rank-1 update of the rows below (no shared-memory round trips)
+      double r[kCB];
+#pragma unroll
+      for (int c = 0; c < kCB; ++c) r[c] = (lane < (int)nb && c < (int)nb) ? D[lane + c * kCB] : 0.0;
+      bool bad = false;
+      double dmin = INFINITY, dmax = 0.0;
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) {
+        if (j < (int)nb) {
+          double piv = __shfl_sync(0xffffffffu, r[j], j);
+          if (!(piv > 0.0)) {
+            bad = true;
+            piv = 1.0;
+          }
+          const double ljj = sqrt(piv);
+          const double inv = 1.0 / ljj;
+          dmin = fmin(dmin, ljj);
+          dmax = fmax(dmax, ljj);
+          const double l = lane > j ? r[j] * inv : (lane == j ? ljj : 0.0);
+          if (lane >= j) r[j] = l;
+#pragma unroll
+          for (int c = j + 1; c < kCB; ++c) {
+            const double lcj = __shfl_sync(0xffffffffu, l, c);
+            if (lane >= c) r[c] -= l * lcj;
+          }
         }
-        const double ljj = sqrt(piv);
-        __syncwarp();
-        if (lane == 0) {
-          D[j + j * kCB] = ljj;
-          s_dmin = fmin(s_dmin, ljj);
-          s_dmax = fmax(s_dmax, ljj);
-        }
-        __syncwarp();
-        const double inv = 1.0 / ljj;
-        for (uint32_t i = j + 1 + lane; i < nb; i += 32) D[i + j * kCB] *= inv;
-        __syncwarp();
-        // rank-1 update of the remaining lower part of D
-        for (uint32_t c = j + 1; c < nb; ++c) {
-          const double lcj = D[c + j * kCB];
-          for (uint32_t i = c + lane; i < nb; i += 32) D[i + c * kCB] -= D[i + j * kCB] * lcj;
-        }
-        __syncwarp();
+      }
+      if (lane < (int)nb) {
+#pragma unroll
+        for (int c = 0; c < kCB; ++c)
+          if (c < (int)nb) D[lane + c * kCB] = lane >= c ? r[c] : 0.0;
+      }
+      if (lane == 0) {
+        if (bad) s_bad = 1;
+        s_dmin = fmin(s_dmin, dmin);
+        s_dmax = fmax(s_dmax, dmax);
       }
     }
     __syncthreads();
@@ -219,29 +233,48 @@ __global__ void __launch_bounds__(kCT, 2) cholesky_kernel(double* const* __restr
     __syncthreads();
     // 3. trailing SYRK: A22 -= L21 L21^T on 8x8 tiles of the lower triangle (DMMA)
     const uint32_t nt = (below + 7) / 8;
-    const uint64_t ntp = (uint64_t)nt * (nt + 1) / 2;
     const int lr = lane >> 2, lc = lane & 3;
-    for (uint64_t tp = warp; tp < ntp; tp += kCT / 32) {
-      uint32_t ti = (uint32_t)((sqrt(8.0 * (double)tp + 1.0) - 1.0) * 0.5);
-      while ((uint64_t)ti * (ti + 1) / 2 > tp) --ti;
-      while ((uint64_t)(ti + 1) * (ti + 2) / 2 <= tp) ++ti;
-      const uint32_t tj = (uint32_t)(tp - (uint64_t)ti * (ti + 1) / 2);
-      const uint32_t ra = ti * 8 + lr;       // A fragment row (local)
-      const uint32_t sb = tj * 8 + lr;       // B fragment column (local)
-      const uint32_t r = ti * 8 + lr, s0 = tj * 8 + 2 * lc;  // D fragment
-      double* c0p = A + (k0 + nb + r) + (uint64_t)(k0 + nb + s0) * M;
-      const bool rok = r < below;
-      double d0 = (rok && s0 < below) ? -__ldcg(c0p) : 0.0;
-      double d1 = (rok && s0 + 1 < below) ? -__ldcg(c0p + M) : 0.0;
+    // a warp owns tile rows ti = warp, warp + 8, ...: its A fragments (L21 rows of
+    // the tile row) are loaded once and reused across the row's tiles tj <= ti,
+    // two tiles at a time so their C loads are in flight together
+    for (uint32_t ti = warp; ti < nt; ti += kCT / 32) {
+      const uint32_t r = ti * 8 + lr;
+      double af[kCB / 4];
 #pragma unroll
-      for (int kk = 0; kk < kCB; kk += 4) {
-        const int q = kk + lc;
-        const double a = (ra < below && q < (int)nb) ? Lp[ra + (uint64_t)q * M] : 0.0;
-        const double b = (sb < below && q < (int)nb) ? Lp[sb + (uint64_t)q * M] : 0.0;
-        dmma(d0, d1, a, b);  // accumulates -C + L L^T
+      for (int kk = 0; kk < kCB / 4; ++kk) {
+        const int q = 4 * kk + lc;
+        af[kk] = (r < below && q < (int)nb) ? Lp[r + (uint64_t)q * M] : 0.0;
       }
-      if (rok && s0 < below) *c0p = -d0;
-      if (rok && s0 + 1 < below) c0p[M] = -d1;
+      for (uint32_t tj = 0; tj <= ti; tj += 2) {
+        double d0[2], d1[2];
+        double* cp[2];
+        bool ok0[2], ok1[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t t = tj + u, s0 = t * 8 + 2 * lc;
+          cp[u] = A + (k0 + nb + r) + (uint64_t)(k0 + nb + s0) * M;
+          const bool live = t <= ti && r < below;
+          ok0[u] = live && s0 < below;
+          ok1[u] = live && s0 + 1 < below;
+          d0[u] = ok0[u] ? -__ldcg(cp[u]) : 0.0;
+          d1[u] = ok1[u] ? -__ldcg(cp[u] + M) : 0.0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < kCB / 4; ++kk) {
+          const int q = 4 * kk + lc;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t sb = (tj + u) * 8 + lr;
+            const double bv = (sb < below && q < (int)nb) ? Lp[sb + (uint64_t)q * M] : 0.0;
+            dmma(d0[u], d1[u], af[kk], bv);  // accumulates -C + L L^T
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (ok0[u]) *cp[u] = -d0[u];
+          if (ok1[u]) cp[u][M] = -d1[u];
+        }
+      }
     }
     __syncthreads();
   }
