@@ -1253,6 +1253,18 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   uint32_t g, G;
   const size_t budget = std::min<size_t>(smem_optin, 200 * 1024);
   jacobi_plan(rows, cols_pad, with_v, budget, g, G);
+  // a single matrix (the merge) is latency-bound: smaller groups, 32 lanes per
+  // pair (shorter dot and update chains per round) and up to 16 CTAs in the cluster
+  unsigned max_cluster = 8;
+  if (jobs.size() == 1 && !with_v) {
+    const char* ge = std::getenv("RK_JACOBI_SINGLE_G");
+    const uint32_t g1 = ge ? (uint32_t)std::strtoul(ge, nullptr, 10) : 8u;
+    if (g1 >= 2 && g1 % 2 == 0 && g1 < g && cols_pad % g1 == 0 && (cols_pad / g1) % 2 == 0 && rows <= 32u * 32u) {
+      g = g1;
+      G = cols_pad / g1;
+      max_cluster = 16;
+    }
+  }
   for (JacobiJob& j : jobs) {
     if (j.rows != rows || j.cols_pad != cols_pad || (j.v != nullptr) != with_v)
       fail(RK_RUNTIME, "jacobi_batched: heterogeneous batch");
@@ -1294,7 +1306,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // cluster size: enough CTAs for the SMs at the occupancy the shared memory allows
   const unsigned per_sm = (unsigned)std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (smem + 2048)));
   unsigned cl = (unsigned)std::max<uint64_t>(1, (uint64_t)sms * per_sm / jobs.size());
-  cl = std::min<unsigned>({cl, G / 2, 8u});
+  cl = std::min<unsigned>({cl, G / 2, max_cluster});
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
   cl = p2;
