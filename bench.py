@@ -136,6 +136,24 @@ def fp64_peak_tflops(torch):
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def profiled_traffic(dominant):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the newest
+    committed `ncu --set full` summary (profiles/*_kernels.json, written by
+    profiles/summarize.py); None when there is none."""
+    import glob
+    names = {"block_jacobi": "jacobi_cluster_kernel<16, 16, 1>", "block_qr": "qr_kernel"}
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
+    for f in reversed(files):
+        try:
+            kern = json.load(open(f))
+        except Exception:
+            continue
+        for k, launches in kern.items():
+            if names.get(dominant, "?") in k and launches and "traffic_bytes" in launches[0]:
+                return launches[0]["traffic_bytes"], os.path.relpath(f, ROOT) + " :: " + k
+    return None, None
+
+
 # --------------------------------------------------------------------------- reference arm
 
 def reference_arm(args, cfg):
@@ -295,8 +313,10 @@ def main():
     dom = max(cand, key=lambda k: cand[k][0])
     d_ms, d_flops = cand[dom]
     achieved = d_flops / (d_ms * 1e-3) / 1e12 if d_ms > 0 else 0.0
-    roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-                "frac": achieved / fp64 if fp64 else None, "traffic": None,
+    traffic, traffic_src = profiled_traffic(dom)
+    roofline = {"bound": "tensor", "pipe": "fp64 (DFMA rounds + DMMA)", "kernel": dom, "achieved": achieved,
+                "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64 if fp64 else None, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": "measured in bench.py: cuBLAS DGEMM burst (torch.matmul f64 8192^3, best of 5); "
                                "FP64 is not in MEASURED_PEAKS.json",
                 "flops_per_launch": d_flops, "ms_per_launch": d_ms,

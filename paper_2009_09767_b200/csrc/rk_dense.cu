@@ -1253,10 +1253,11 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   uint32_t g, G;
   const size_t budget = std::min<size_t>(smem_optin, 200 * 1024);
   jacobi_plan(rows, cols_pad, with_v, budget, g, G);
-  // a single matrix (the merge) is latency-bound: smaller groups, 32 lanes per
-  // pair (shorter dot and update chains per round) and up to 16 CTAs in the cluster
+  // few matrices (the merge; a rank's share of the blocks on many GPUs) are
+  // latency-bound: smaller groups, 32 lanes per pair (shorter dot and update
+  // chains per round) and up to 16 CTAs per matrix when the SMs have room
   unsigned max_cluster = 8;
-  if (jobs.size() == 1 && !with_v) {
+  if ((uint64_t)jobs.size() * 16 <= (uint64_t)sms && !with_v) {
     const char* ge = std::getenv("RK_JACOBI_SINGLE_G");
     const uint32_t g1 = ge ? (uint32_t)std::strtoul(ge, nullptr, 10) : 8u;
     if (g1 >= 2 && g1 % 2 == 0 && g1 < g && cols_pad % g1 == 0 && (cols_pad / g1) % 2 == 0 && rows <= 32u * 32u) {

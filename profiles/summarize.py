@@ -57,6 +57,8 @@ def launches(tag, src):
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
+        if "rk::" not in r["Kernel Name"]:  # torch fill/RNG kernels, the cuBLAS DGEMM of the peak probe
+            continue
         k = short(r["Kernel Name"])
         ns = float(r["Metric Value"]) * (1e3 if r["Metric Unit"] == "us" else 1e6 if r["Metric Unit"] == "ms" else 1)
         a = agg.setdefault(k, [0, 0.0])
@@ -99,7 +101,7 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(HERE), "gpurun_out")
     agg = launches(tag, src)
-    mine = {k: v for k, v in agg.items() if not any(t in k for t in ("gemm", "Kernel", "elementwise", "fill"))}
+    mine = {k: v for k, v in agg.items() if k.startswith("<unnamed>::") or k.startswith("rk::")}
     steps = 5  # capture.sh: --steps 2 --warmup 3, every step launches the same kernels
     total = sum(v[1] for v in mine.values()) / steps
     md = [f"# {tag}: ncu launch list of `bench.py --steps 2 --warmup 3` (c2), per step",
@@ -111,6 +113,19 @@ def main():
     open(os.path.join(HERE, f"{tag}_launches.md"), "w").write("\n".join(md) + "\n")
     kern = full(tag, src)
     json.dump(kern, open(os.path.join(HERE, f"{tag}_kernels.json"), "w"), indent=1)
+    km = [f"# {tag}: `ncu --set full` of one bench step (first launch of each kernel)", "",
+          "| kernel | ms | DRAM MB (r+w) | FP64 pipe % active | FP64 tensor % | issue active % | warps active % | "
+          "grid x block | regs |", "|---|---:|---:|---:|---:|---:|---:|---|---:|"]
+    for k, ds in kern.items():
+        d = ds[0]
+        km.append(f"| `{k}` | {d.get('duration_ms', 0):.3f} | {d.get('traffic_bytes', 0) / 1e6:.1f} | "
+                  f"{d.get('fp64_pipe_pct_active', 0):.1f} | {d.get('fp64_tensor_pct_elapsed', 0):.1f} | "
+                  f"{d.get('issue_active_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} | "
+                  f"{d.get('grid', 0):.0f} x {d.get('block', 0):.0f} | {d.get('regs', 0):.0f} |")
+    open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(km) + "\n")
+    bj = os.path.join(src, f"{tag}_bench.jsonl")
+    if os.path.exists(bj):
+        shutil.copy(bj, os.path.join(HERE, f"{tag}_bench.jsonl"))
     print("\n".join(md))
     for k, ds in kern.items():
         d = ds[0]
