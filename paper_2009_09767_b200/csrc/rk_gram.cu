@@ -139,8 +139,9 @@ __global__ void reduce_partials(const double* __restrict__ partial, uint32_t n_c
 // the matrix is W = L. status[i]: 0 ok, 1 non-positive pivot.
 
 constexpr int kCT = 256;
-constexpr int kCB = 32;  // panel width
 
+// kCB: panel width (32; 16 for tall matrices, so the M x kCB panel fits shared memory)
+template <int kCB>
 __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restrict__ mats, uint32_t M,
                                                           uint32_t* __restrict__ status,
                                                           double* __restrict__ diag_ratio) {
@@ -338,15 +339,19 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
                       cudaStream_t s) {
   if (!n_mats) return;
-  const size_t smem = ((size_t)kCB * kCB + (size_t)M * kCB) * sizeof(double);
-  if (smem > 200 * 1024) fail(RK_RUNTIME, "cholesky_batched: M too large for the panel buffer");
-  RK_CUDA_CHECK(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  RK_CUDA_CHECK(cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  cholesky_kernel<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
-  RK_LAUNCH_CHECK();
+  auto launch = [&](auto kern, int cb) {
+    const size_t smem = ((size_t)cb * cb + (size_t)M * cb) * sizeof(double);
+    if (smem > 200 * 1024) fail(RK_RUNTIME, "cholesky_batched: M too large for the panel buffer");
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    kern<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
+    RK_LAUNCH_CHECK();
+  };
+  if (M <= 640) launch(cholesky_kernel<32>, 32);
+  else launch(cholesky_kernel<16>, 16);
 }
 
-uint32_t cholesky_max_rows() { return 640; }  // the panel buffer (M x 32 doubles) must fit shared memory
+uint32_t cholesky_max_rows() { return 1280; }  // the panel buffer (M x 16 doubles) must fit shared memory
 
 bool gram_route_enabled() {
   const char* e = std::getenv("RK_BLOCK_ROUTE");
