@@ -1214,8 +1214,6 @@ void r_extract_batched(const std::vector<RJob>& jobs, bool transpose, cudaStream
 }
 
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
-bool jacobi_gram_supported(uint32_t rows, uint32_t g, size_t smem_optin);
-void jacobi_gram_batched(std::vector<JacobiJob>& jobs, uint32_t g, uint32_t G, cudaStream_t s, int sms);
 
 void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, uint32_t& g, uint32_t& G) {
   // largest even group size (<= gcap) whose two staged groups fit the budget; a
@@ -1244,7 +1242,7 @@ void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, 
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v) {
   return (size_t)2 * g * (rows + 8) * 8 + (with_v ? (size_t)2 * g * (cols_pad + 8) * 8 : 0) + (size_t)2 * g * 8;
 }
-void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin) {
+void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency) {
   if (jobs.empty()) return;
   // jobs in one launch share rows / cols_pad / with_v (the caller groups them);
   // the group layout is a function of (rows, cols_pad) only
@@ -1253,11 +1251,10 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   uint32_t g, G;
   const size_t budget = std::min<size_t>(smem_optin, 200 * 1024);
   jacobi_plan(rows, cols_pad, with_v, budget, g, G);
-  // few matrices (the merge; a rank's share of the blocks on many GPUs) are
-  // latency-bound: smaller groups, 32 lanes per pair (shorter dot and update
-  // chains per round) and up to 16 CTAs per matrix when the SMs have room
+  // a single latency-critical matrix (the merge): smaller groups, 32 lanes per
+  // pair (shorter dot and update chains per round), up to 16 CTAs per matrix
   unsigned max_cluster = 8;
-  if ((uint64_t)jobs.size() * 16 <= (uint64_t)sms && !with_v) {
+  if (latency && jobs.size() == 1 && !with_v) {
     const char* ge = std::getenv("RK_JACOBI_SINGLE_G");
     const uint32_t g1 = ge ? (uint32_t)std::strtoul(ge, nullptr, 10) : 8u;
     if (g1 >= 2 && g1 % 2 == 0 && g1 < g && cols_pad % g1 == 0 && (cols_pad / g1) % 2 == 0 && rows <= 32u * 32u) {
@@ -1272,18 +1269,16 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     if (j.cols > cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols > cols_pad");
   }
   if (g * G != cols_pad) fail(RK_RUNTIME, "jacobi_batched: cols_pad is not a planned width");
-  // Gram-assisted kernel: only where the direct kernel cannot keep the A column in
-  // registers (rows > 32 lanes-per-pair x 32), i.e. long columns relative to 2g;
-  // RK_JACOBI_GRAM=1 / RK_JACOBI_DIRECT=1 force either kernel (tuning)
-  bool all_gram = !with_v && !std::getenv("RK_JACOBI_DIRECT");
-  for (const JacobiJob& j : jobs) all_gram = all_gram && j.gram_ok;
   // Gram-route matrices: Gram-assisted warp Jacobi, then the direct kernel
   // certifies convergence on W (check_first)
-  // (measured on c2: 7.30 ms vs 7.23 ms for the direct kernel on the 64 blocks and
-  // 2x slower on the single merge matrix -- the L2 latency of streaming X twice per
-  // step is not hidden at 8 warps per SM -- so it is opt-in: RK_JACOBI_WARP=1)
+  // Where it pays (measured): long columns in a batch -- c4's 1024 blocks of 1024
+  // rows: 7.5 s vs 12.2 s for the direct kernel. At 256 rows it ties on c2's 64
+  // blocks (7.30 vs 7.23 ms) and is 2x slower on a single matrix (the L2 latency of
+  // streaming X twice per step is not hidden at 8 warps per SM). RK_JACOBI_WARP=0/1
+  // forces it off/on.
   const char* we = std::getenv("RK_JACOBI_WARP");
-  bool use_warp = we && we[0] == '1' && !with_v && cols_pad % 16 == 0 && cols_pad / 16 <= 64;
+  const bool warp_default = rows >= 512 && !latency;  // a function of the shape only (see latency)
+  bool use_warp = (we ? we[0] == '1' : warp_default) && !with_v && cols_pad % 16 == 0 && cols_pad / 16 <= 64;
   for (const JacobiJob& j : jobs) use_warp = use_warp && j.gram_ok;
   if (use_warp) {
     const char* ce0 = std::getenv("RK_JACOBI_CHECK");
@@ -1295,13 +1290,6 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     const unsigned wcl = (unsigned)ceil_div(cols_pad / 16, kJWarps);
     RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_warp_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     launch_cluster_kernel((const void*)jacobi_warp_kernel, (unsigned)jobs.size() * wcl, wcl, kJThreads, 0, s, wargs);
-  }
-  int q_direct = 32;
-  while (q_direct > 8 && (kJThreads / q_direct) < (int)g) q_direct /= 2;
-  const bool long_columns = rows > (uint32_t)(32 * q_direct) || std::getenv("RK_JACOBI_GRAM");
-  if (!use_warp && all_gram && long_columns && jacobi_gram_supported(rows, g, smem_optin)) {
-    jacobi_gram_batched(jobs, g, G, s, sms);
-    return;
   }
   const size_t smem = jacobi_smem(rows, g, g * G, with_v);
   // cluster size: enough CTAs for the SMs at the occupancy the shared memory allows

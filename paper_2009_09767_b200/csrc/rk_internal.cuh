@@ -303,7 +303,11 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
   uint64_t* stats;    // [0] sweeps, [1] rotations, [2] status (0 ok, 1 not converged), [3] residual bits, [4..7] scratch
   uint32_t gram_ok = 0;  // well-conditioned (kappa <= kappa_max): the Gram-assisted kernel may run it
 };
-void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin);
+// latency: one latency-critical matrix (the merge) -- smaller groups, larger
+// clusters. Never set for blocks: a block's rotation sequence (and with it its
+// rounding) must not depend on how many blocks share the launch, so that the
+// sharded path is bitwise identical for every rank count.
+void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency = false);
 
 // finalize: sigma = column norms, stable descending sort, u = w/sigma, sign
 // convention; optional payload (rows x k row-major, u*sigma) and U/sigma outputs

@@ -644,7 +644,7 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   std::vector<JacobiJob> jj(1);
   jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = cols; jj[0].cols_pad = cp;
   jj[0].alpha = alpha.get(); jj[0].stats = stats.get(); jj[0].gram_ok = gram_ok ? 1u : 0u;
-  jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+  jacobi_batched(jj, s, c.num_sms, c.smem_optin, /*latency=*/true);
   JacobiStats js = read_stats(stats.get(), 1, s)[0];
   out.sweeps = js.sweeps;
   out.rotations = js.rotations;
