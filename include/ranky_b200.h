@@ -230,6 +230,14 @@ RK_API rk_status rk_dev_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t b
                           uint64_t top_k, rk_dev_outputs** out, rk_timing* timing);
 RK_API rk_status rk_dev_outputs_free(rk_dev_outputs* o);
 
+/* Reconstruction of device-resident outputs (the reference's test metric,
+ * proj/tests/test_support.hpp:57-70): residual = ||A - U[:, :k_v] diag(sigma) V^T||_F
+ * formed exactly on the device (no dense N x M copy), A being the repaired matrix
+ * the outputs were computed from (the input `a` when no repair edge was added);
+ * a_norm = ||A||_F. Requires RK_WANT_V. */
+RK_API rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
+                                 double* a_norm);
+
 /* ---- sharded path (one process per GPU) --------------------------------------
  * Column blocks are sharded over G ranks by merge-tree leaves. Rank g repairs the
  * whole matrix (the replay is deterministic, so every rank holds the same repaired

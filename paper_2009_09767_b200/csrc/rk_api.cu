@@ -1,6 +1,7 @@
 // rk_api.cu -- the C ABI (include/ranky_b200.h): argument checks with the
 // reference's messages, exception -> status mapping, host <-> device marshaling.
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -61,6 +62,7 @@ struct rk_dev_matrix {
 struct DevOutputsImpl {
   rk_dev_outputs pub;
   DBuf<double> sigma, u, v;
+  std::unique_ptr<DevMatrix> repaired;  // the matrix U, sigma, V reconstruct (null: the input)
 };
 struct rk_dev_shard {
   rk_ctx* owner;
@@ -714,6 +716,7 @@ rk_status rk_dev_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_co
     o->sigma = std::move(fr.merge.sigma);
     o->u = std::move(fr.merge.u);
     o->v = std::move(fr.v);
+    o->repaired = std::move(fr.repaired);
     o->pub.d_sigma = o->sigma.get();
     o->pub.d_u = o->u.get();
     o->pub.d_v = (flags & RK_WANT_V) ? o->v.get() : nullptr;
@@ -725,6 +728,25 @@ rk_status rk_dev_outputs_free(rk_dev_outputs* o) {
   if (!o) return RK_OK;
   delete reinterpret_cast<DevOutputsImpl*>(o);
   return RK_OK;
+}
+
+rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
+                          double* a_norm) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!a || !out || !residual || !a_norm) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    if (!out->d_v) fail(RK_INVALID_ARGUMENT, "rk_dev_residual: the outputs carry no V (RK_WANT_V)");
+    CallScope sc(&ctx->c);
+    const auto* impl = reinterpret_cast<const DevOutputsImpl*>(out);
+    const DevMatrix& m = impl->repaired ? *impl->repaired : a->m;
+    if (m.csc.rows != out->rows || m.csc.cols != out->cols)
+      fail(RK_INVALID_ARGUMENT, "rk_dev_residual: matrix and outputs differ in shape");
+    double r2 = 0.0, a2 = 0.0;
+    residual_device(m.csc, out->d_u, (uint32_t)out->k_sigma, out->d_sigma, (uint32_t)out->k_v, out->d_v,
+                    ctx->c.num_sms, &r2, &a2, ctx->c.stream);
+    *residual = std::sqrt(r2);
+    *a_norm = std::sqrt(a2);
+  });
 }
 
 uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count, uint64_t keep) {

@@ -874,7 +874,9 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
   unsigned long long* counters = reinterpret_cast<unsigned long long*>(job.stats + 4);
   double* W = job.w;
   double* alpha_g = job.alpha;
-  const uint32_t w = rank * kJWarps + warp;  // this warp's pair slot
+  const uint32_t w = rank * kJWarps + warp;  // this warp's first pair slot
+  constexpr int kWarpMaxSweeps = 40;        // leave sweeps for the direct kernel
+  double prev_ratio = INFINITY;
 
   unsigned long long total_rot = 0;
   double last_max_ratio = 0.0;
@@ -909,8 +911,8 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
     uint32_t nrot = 0;
     double max_r2 = 0.0;
     for (uint32_t step = 0; step + 1 < G; ++step) {
-      if (w < npairs) {
-        const uint32_t cA = rr_slot(w, step, G) * kWG, cB = rr_slot(G - 1 - w, step, G) * kWG;
+      for (uint32_t pw = w; pw < npairs; pw += csize * kJWarps) {
+        const uint32_t cA = rr_slot(pw, step, G) * kWG, cB = rr_slot(G - 1 - pw, step, G) * kWG;
         double* h = sH[warp];
         warp_gram(W, rows, cA, cB, h);
         double z[kWN];
@@ -965,10 +967,15 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
     last_max_ratio = __longlong_as_double(__ldcg(reinterpret_cast<long long*>(job.stats + 3)));
     cluster.sync();
     if (rank == 0 && tid == 0) job.stats[3] = 0ull;
-    if (rot == 0 || last_max_ratio < P.stop_ratio) {
+    // hand over: converged on H, in the quadratic regime, or stagnating (the
+    // rounding of H-based decisions on a badly conditioned pair) -- the direct
+    // kernel finishes on W either way
+    const bool stagnant = sweep >= 3 && last_max_ratio < 1e-4 && last_max_ratio > 0.25 * prev_ratio;
+    if (rot == 0 || last_max_ratio < P.stop_ratio || stagnant || sweep + 1 >= kWarpMaxSweeps) {
       ++sweep;
       break;
     }
+    prev_ratio = last_max_ratio;
     cluster.sync();
   }
   cluster.sync();
@@ -1227,15 +1234,20 @@ void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, 
   // column in registers (E <= 32); without the cap the plan falls back to the
   // shared-memory rounds (E = 0), several times slower
   const uint32_t gtop = (rows > 16 * 32 && rows <= 32 * 32 && !with_v) ? std::min<uint32_t>(gcap, 8) : gcap;
-  for (uint32_t gmax = gtop; gmax >= 2; gmax -= 2) {
-    G = (uint32_t)ceil_div(cols ? cols : 1, gmax);
-    if (G < 2) G = 2;
-    if (G & 1) ++G;
-    g = (uint32_t)ceil_div(cols ? cols : 1, G);
-    if (g & 1) ++g;
-    if (g < 2) g = 2;
-    if (jacobi_smem(rows, g, g * G, with_v) <= smem_budget) return;
-  }
+  // long columns run the Gram-assisted warp kernel first (groups of 8), which needs
+  // a width divisible by 16: prefer such plans (pass 0), else any (pass 1)
+  const bool want16 = rows >= 512 && !with_v;
+  for (int pass = want16 ? 0 : 1; pass < 2; ++pass)
+    for (uint32_t gmax = gtop; gmax >= 2; gmax -= 2) {
+      G = (uint32_t)ceil_div(cols ? cols : 1, gmax);
+      if (G < 2) G = 2;
+      if (G & 1) ++G;
+      g = (uint32_t)ceil_div(cols ? cols : 1, G);
+      if (g & 1) ++g;
+      if (g < 2) g = 2;
+      if (pass == 0 && (g * G) % 16 != 0) continue;
+      if (jacobi_smem(rows, g, g * G, with_v) <= smem_budget) return;
+    }
   fail(RK_INVALID_ARGUMENT, "Jacobi: a " + std::to_string(rows) + "-row matrix does not fit shared memory");
 }
 
@@ -1278,8 +1290,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // forces it off/on.
   const char* we = std::getenv("RK_JACOBI_WARP");
   const bool warp_default = rows >= 512 && !latency;  // a function of the shape only (see latency)
-  bool use_warp = (we ? we[0] == '1' : warp_default) && !with_v && cols_pad % 16 == 0 && cols_pad / 16 <= 64;
-  for (const JacobiJob& j : jobs) use_warp = use_warp && j.gram_ok;
+  bool use_warp = (we ? we[0] == '1' : warp_default) && !with_v && cols_pad % 16 == 0;
   if (use_warp) {
     const char* ce0 = std::getenv("RK_JACOBI_CHECK");
     WarpParams WP{nullptr, cols_pad / kWG, ce0 ? std::strtod(ce0, nullptr) : 1e-7};
@@ -1287,7 +1298,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     to_device(djw.get(), jobs.data(), jobs.size(), s);
     WP.jobs = djw.get();
     void* wargs[] = {&WP};
-    const unsigned wcl = (unsigned)ceil_div(cols_pad / 16, kJWarps);
+    const unsigned wcl = (unsigned)std::min<uint64_t>(8, ceil_div(cols_pad / 16, kJWarps));
     RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_warp_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     launch_cluster_kernel((const void*)jacobi_warp_kernel, (unsigned)jobs.size() * wcl, wcl, kJThreads, 0, s, wargs);
   }

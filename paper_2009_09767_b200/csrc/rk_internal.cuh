@@ -308,6 +308,9 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
 // rounding) must not depend on how many blocks share the launch, so that the
 // sharded path is bitwise identical for every rank count.
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency = false);
+// ||A - U[:, :r] diag(sigma) V^T||_F^2 (exact, tile by tile) and ||A||_F^2
+void residual_device(const DevCsc& a, const double* u, uint32_t ku, const double* sigma, uint32_t r, const double* v,
+                     int sms, double* h_res2, double* h_a2, cudaStream_t s);
 
 // finalize: sigma = column norms, stable descending sort, u = w/sigma, sign
 // convention; optional payload (rows x k row-major, u*sigma) and U/sigma outputs

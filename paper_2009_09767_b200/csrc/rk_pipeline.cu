@@ -396,7 +396,9 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   to_host(hc, counts.get(), 2 * nblk, s);
   sync(s);
   const uint64_t aux_sz = 2 * (uint64_t)M + (ceil_div(M, 16) + 1) * 256;
-  constexpr uint32_t kLeafRows = 768;  // TSQR leaf height of the tall blocks
+  // TSQR leaf height of the tall blocks: at least 2M, so every leaf is tall (a wide
+  // leaf makes the pairwise combines, ~4/3 M^3 each, dominate: c5 3x the flops)
+  const uint32_t kLeafRows = std::max<uint32_t>(768, std::min<uint32_t>(2 * M, qr_max_rows()));
 
   size_t t0 = 0;
   while (t0 < todo.size()) {

@@ -193,6 +193,7 @@ def lib():
             "rk_dev_full_svd": ([vp, vp, u64, i32, u64, u64, u32, u64, C.POINTER(C.POINTER(DevOutputs)),
                                  C.POINTER(Timing)], i32),
             "rk_dev_outputs_free": ([C.POINTER(DevOutputs)], i32),
+            "rk_dev_residual": ([vp, vp, C.POINTER(DevOutputs), pdbl, pdbl], i32),
             "rk_merge_tree_leaves": ([u64, u64, u64, u64], u64),
             "rk_dev_shard_factor": ([vp, vp, u64, i32, u64, u64, u64, u64, vp, C.POINTER(vp), C.POINTER(Timing)],
                                     i32),
@@ -865,6 +866,14 @@ def dev_full_svd(m: DeviceMatrix, block_count: int, method, keep: int = 0, seed:
 
 def dev_outputs_free(out):
     lib().rk_dev_outputs_free(out)
+
+
+def dev_residual(m: DeviceMatrix, out) -> tuple[float, float]:
+    """(||A - U diag(sigma) V^T||_F, ||A||_F) of device outputs, formed on the device
+    (A = the repaired matrix the outputs reconstruct); test_support.hpp:57-70."""
+    r, a = C.c_double(), C.c_double()
+    _check(lib().rk_dev_residual(m.ctx.handle, m.handle, out, C.byref(r), C.byref(a)))
+    return r.value, a.value
 
 
 class _CudaArray:

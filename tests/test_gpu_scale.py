@@ -118,6 +118,9 @@ def test_full_scale_config(name, n_blocks, ref):
             vtv += blk.T @ blk
         orth = float((vtv - torch.eye(M, dtype=torch.float64, device=v_d.device)).abs().max())
         assert orth <= 1e-9, (name, orth)
+        # reconstruction of the repaired matrix over all N columns, on the device
+        res, anorm = rk.ranky.dev_residual(dm, out)
+        assert res <= 1e-10 * anorm, (name, res / anorm)
         # a sampled block of V rows, bit-exact against recover_right_vectors
         d = blocks[len(blocks) // 2]
         rng_d = p.range(d)
