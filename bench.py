@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # functional dry run of the N>1 path on a one-GPU box: every rank on device 0, the
+    # collectives through gloo on host copies (not a performance configuration)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -227,10 +230,15 @@ def main():
     from paper_2009_09767_b200 import ranky as R
 
     ws, rank, local = dist_env()
+    if args.backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     ctx = rk.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
@@ -242,6 +250,12 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     L = R.lib()
     M = cfg.rows
+
+    def allreduce_max(t):
+        if args.backend == "gloo":
+            t = t.cpu()
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     def barrier():
         if ws > 1:
@@ -260,23 +274,35 @@ def main():
         roots = torch.empty((ws, M, M), dtype=torch.float64, device="cuda")
         mine = torch.empty((M, M), dtype=torch.float64, device="cuda")
 
-        def step():
+        def sharded(dmx, sink=None):
+            """this rank's share: factor its leaves, all-gather the subtree factors
+            (NCCL), finish the tree top, V for its columns; `sink(out)` sees the outputs"""
             shard = C.c_void_p()
             t = R.Timing()
-            R._check(L.rk_dev_shard_factor(ctx.handle, dm.handle, cfg.blocks, R._method(cfg.method), cfg.keep,
+            R._check(L.rk_dev_shard_factor(ctx.handle, dmx.handle, cfg.blocks, R._method(cfg.method), cfg.keep,
                                            cfg.seed, lo, hi, C.c_void_p(mine.data_ptr()), C.byref(shard),
                                            C.byref(t)))
-            torch.distributed.all_gather_into_tensor(roots, mine)
+            if args.backend == "nccl":
+                torch.distributed.all_gather_into_tensor(roots, mine)
+            else:
+                parts = [torch.empty((M, M), dtype=torch.float64) for _ in range(ws)]
+                torch.distributed.all_gather(parts, mine.cpu())
+                roots.copy_(torch.stack(parts))
             out = C.POINTER(R.DevOutputs)()
             t2 = R.Timing()
             R._check(L.rk_dev_shard_finish(ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V,
                                            cfg.top_k, c_lo, c_hi, C.byref(out), C.byref(t2)))
+            if sink:
+                sink(out)
             R.dev_outputs_free(out)
             L.rk_dev_shard_destroy(shard)
             t.merge_ms += t2.merge_ms
             t.recover_ms = t2.recover_ms
             t.kernel_launches += t2.kernel_launches
             return t
+
+        def step():
+            return sharded(dm)
 
     for _ in range(args.warmup):
         step()
@@ -303,8 +329,7 @@ def main():
     ms = sum(ms_steps) / len(ms_steps)
     if ws > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = allreduce_max(tt)
     value = a.nnz() / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (by device time) --------------------------
@@ -329,9 +354,70 @@ def main():
     v_bytes = 8.0 * cfg.cols * M
     stages["recover_hbm_frac"] = (v_bytes / (med["recover_ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"] \
         if med["recover_ms"] > 0 else None
+    # every stage against its own roof: HBM for the rank check +
+    # repair and the V SpMM (algorithmic bytes), FP64 for the factorizations
+    nnz = a.nnz()
+    repair_bytes = 12.0 * nnz + 8.0 * (M + 1) + 4.0 * M * cfg.blocks  # CSR col+val, row_ptr, presence flags
+    spmm_bytes = v_bytes + 12.0 * nnz + 8.0 * (cfg.cols + 1) + 8.0 * M * M
+    hbm = peaks["hbm_gbs"]
+
+    def frac(x, ms, peak, scale):
+        return {"achieved": x / (ms * 1e-3) / scale, "peak": peak, "frac": x / (ms * 1e-3) / scale / peak} \
+            if ms > 0 and peak else None
+    stage_roofs = {
+        "repair (HBM, GB/s)": frac(repair_bytes, med["repair_ms"], hbm, 1e9),
+        "block factor: Gram + Cholesky / QR (FP64, TF/s)": frac(med["qr_flops"], med["qr_ms"], fp64, 1e12),
+        "block Jacobi (FP64, TF/s)": frac(med["jacobi_flops"], med["jacobi_ms"], fp64, 1e12),
+        "V recovery SpMM (HBM, GB/s)": frac(spmm_bytes, med["recover_ms"], hbm, 1e9),
+    }
 
     # ---- e2e through the C ABI with host buffers -----------------------------------
     e2e = None
+    if not args.no_e2e and ws > 1:
+        # every rank: H2D of the entries (rk_dev_matrix_create from pinned memory), its
+        # share of the pipeline with the NCCL all-gather, D2H of sigma, U and its V rows;
+        # the step's time is the max over ranks
+        pinned = torch.empty(a.nnz() * R.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+        host_e = pinned.numpy().view(R.ENTRY_DTYPE)
+        host_e[:] = a.entries()
+        ha = R.SparseMatrix._trusted(a.rows(), a.cols(), host_e)
+        k_out = cfg.top_k or M
+        v_host = torch.empty((c_hi - c_lo) * k_out, dtype=torch.float64, pin_memory=True)
+        u_host = torch.empty(M * M + M, dtype=torch.float64, pin_memory=True)
+        moved = {}
+
+        def to_host(out):
+            sig_d, u_d, v_d = R.dev_outputs_tensors(out)
+            nv = v_d.numel()
+            v_host[:nv].copy_(v_d.reshape(-1), non_blocking=True)
+            u_host[:u_d.numel()].copy_(u_d.reshape(-1), non_blocking=True)
+            u_host[u_d.numel():u_d.numel() + sig_d.numel()].copy_(sig_d, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            moved["d2h"] = 8 * (nv + u_d.numel() + sig_d.numel())
+
+        def e2e_step():
+            dmx = rk.DeviceMatrix(ha, ctx)
+            sharded(dmx, to_host)
+            dmx.close()
+
+        for _ in range(max(3, args.warmup)):
+            e2e_step()
+        e2e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            dt = torch.tensor([1e3 * (time.perf_counter() - t0)], dtype=torch.float64, device="cuda")
+            e2e_ms.append(allreduce_max(dt))
+        e_ms = sum(e2e_ms) / len(e2e_ms)
+        e2e = {"value": a.nnz() / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": a.nnz() * R.ENTRY_DTYPE.itemsize, "d2h_bytes_per_step": moved.get("d2h", 0),
+               "ms_median": statistics.median(e2e_ms),
+               "path": "per rank: rk_dev_matrix_create(pinned host entries) + rk_dev_shard_factor + NCCL "
+                       "all_gather + rk_dev_shard_finish + D2H of sigma, U and the rank's V rows; max over ranks",
+               "bytes_note": "per rank"}
     if not args.no_e2e and ws == 1:
         pinned = torch.empty(a.nnz() * R.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
         host_e = pinned.numpy().view(R.ENTRY_DTYPE)
@@ -370,6 +456,7 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, csrc/gen.c)",
                 "config": config_dict(cfg, ws, {"nnz": a.nnz()}), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages_ms_median": stages,
+                "stage_rooflines": stage_roofs,
                 "wall_s_timed_region": wall, "peaks_source": peak_src}
         print(json.dumps(line), flush=True)
     if ws > 1:

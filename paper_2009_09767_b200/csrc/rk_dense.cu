@@ -1310,6 +1310,10 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
   cl = p2;
+  if (const char* ce2 = std::getenv("RK_JACOBI_CLUSTER")) {  // tuning override
+    const unsigned v = (unsigned)std::strtoul(ce2, nullptr, 10);
+    if (v >= 1 && v <= 16 && v <= G / 2) cl = v;
+  }
   DBuf<JacobiJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   const char* ce = std::getenv("RK_JACOBI_CHECK");

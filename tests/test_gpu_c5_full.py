@@ -1,0 +1,82 @@
+"""c5 at full size (M=2048, N=67,108,864, 4096 blocks, ~68.7M nnz, keep 64,
+top-64) -- opt-in (RK_FULL_C5=1): the device run takes minutes and the
+reference's pieces minutes more, too long for the round-end test pass.
+
+The reference cannot run c5 (~250 h of block work), so parity is
+sampled as SURVEY.md §8(c) prescribes: repair in full (bit-exact against the
+reference's ranky::repair), two sampled blocks against the reference's
+block_svd (keep 64), and size-independent properties of the device outputs:
+V's 64 columns orthonormal over all N rows and the reconstruction residual.
+"""
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import paper_2009_09767_b200 as rk
+from paper_2009_09767_b200 import configs
+from paper_2009_09767_b200.ranky import dev_outputs_tensors, dev_residual
+from test_gpu_svd import compare
+from test_gpu_scale import coo_of
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("RK_FULL_C5") != "1", reason="opt-in: RK_FULL_C5=1")]
+
+
+@pytest.mark.timeout(3600)
+def test_c5_full_size(ref):
+    import torch
+    t0 = time.perf_counter()
+
+    def mark(what):
+        print(f"[c5] {what}: {time.perf_counter() - t0:.1f} s", flush=True)
+
+    cfg = configs.CONFIGS["c5"]
+    a = cfg.generate()
+    M, N = a.rows(), a.cols()
+    mark(f"generated {a.nnz()} nnz")
+    p = rk.partition_columns(N, cfg.blocks)
+    rep, report = rk.repair(a, p, cfg.method, cfg.seed)
+    mark(f"repaired on the device ({len(report.added_edges)} edges, {report.fallback_count} fallbacks)")
+    o = ref.repair(coo_of(a), cfg.blocks, cfg.method, cfg.seed)
+    mark("reference repair")
+    assert np.array_equal(report.edges_array(), o.edges)
+    assert report.lonely_counts == o.lonely_counts.tolist()
+    assert report.fallback_count == o.fallback_count
+    del o
+
+    dm = rk.DeviceMatrix(a)
+    out, t = rk.dev_full_svd(dm, cfg.blocks, cfg.method, cfg.keep, cfg.seed, True, cfg.top_k)
+    mark(f"device pipeline: {t.total_ms / 1e3:.1f} s (blocks {t.blocks_ms / 1e3:.1f}, merge {t.merge_ms / 1e3:.1f}, "
+         f"V {t.recover_ms / 1e3:.1f})")
+    try:
+        sig_d, u_d, v_d = dev_outputs_tensors(out)
+        sigma = sig_d.cpu().numpy()
+        k = cfg.top_k
+        assert tuple(v_d.shape) == (N, k)
+        vtv = torch.zeros(k, k, dtype=torch.float64, device=v_d.device)
+        step = 1 << 22
+        for r0 in range(0, N, step):
+            blk = v_d[r0:r0 + step]
+            vtv += blk.T @ blk
+        orth = float((vtv - torch.eye(k, dtype=torch.float64, device=v_d.device)).abs().max())
+        res, anorm = dev_residual(dm, out)
+        mark(f"sigma[:4] {sigma[:4]}, sigma[63] {sigma[63]:.6e}; V orthonormality {orth:.2e}; "
+             f"residual/||A|| {res / anorm:.6e}")
+        assert orth <= 1e-9
+        # top-64 of a rank-2048 matrix: the residual is the tail's mass, bounded by it
+        assert res <= anorm
+    finally:
+        rk.dev_outputs_free(out)
+        dm.close()
+
+    # two sampled blocks of the repaired matrix against the reference's block_svd
+    blocks = [0, cfg.blocks // 2 + 17]
+    views = {d: rk.block_view(rep, p, d) for d in blocks}
+    with ThreadPoolExecutor(len(blocks)) as ex:
+        want = dict(zip(blocks, ex.map(lambda d: ref.block_svd(coo_of(views[d]), cfg.keep), blocks)))
+    for d in blocks:
+        compare(rk.block_svd(views[d], cfg.keep), want[d].sigma, want[d].u, f"c5 block {d}")
+    mark("sampled blocks")
