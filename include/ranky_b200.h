@@ -52,7 +52,8 @@ typedef enum rk_status {
   RK_CONVERGENCE = 3,      /* ranky::ConvergenceError (proj/include/ranky/errors.hpp:29-38) */
   RK_RUNTIME = 4,          /* std::runtime_error ("block task d failed: ...") */
   RK_CUDA = 5,             /* CUDA runtime failure or no usable device */
-  RK_NOMEM = 6             /* device or host allocation failed */
+  RK_NOMEM = 6,            /* device or host allocation failed */
+  RK_RECORD = 7            /* ranky::RecordError: damaged or truncated block record file */
 } rk_status;
 
 /* RepairMethod -- proj/include/ranky/repair.hpp:15-20 (same numbering) */
@@ -257,6 +258,24 @@ RK_API rk_status rk_dev_shard_finish(rk_ctx* ctx, rk_dev_shard* shard, const dou
                               uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi,
                               rk_dev_outputs** out, rk_timing* timing);
 RK_API rk_status rk_dev_shard_destroy(rk_dev_shard* shard);
+
+/* ---- RNKY block records (proj/src/block_record.cpp:51-144) ----------------------
+ * Files byte-identical to ranky::write_block_record: "RNKY", version u16 = 1,
+ * block index u32, rows u32, k u32, rows*k doubles row-major, CRC32 of the payload
+ * bytes, little-endian. Reader failures return RK_RECORD with the reference's
+ * RecordError message. */
+RK_API uint32_t rk_crc32(const void* data, uint64_t size); /* block_record.cpp:53-68 */
+/* CRC32 of n device-resident byte ranges [d_data + offsets[i], + lengths[i]) (GPU;
+ * offsets/lengths/crcs are host arrays) */
+RK_API rk_status rk_dev_crc32(rk_ctx* ctx, const void* d_data, const uint64_t* offsets, const uint64_t* lengths,
+                              uint64_t n, uint32_t* crcs);
+RK_API rk_status rk_write_block_record(uint32_t block_index, uint32_t rows, uint32_t kept, const double* payload,
+                                       const char* path);
+/* *payload (rows*kept doubles) is library-owned: rk_host_free */
+RK_API rk_status rk_read_block_record(const char* path, uint32_t* block_index, uint32_t* rows, uint32_t* kept,
+                                      double** payload);
+/* every record of `records` to "<path_prefix><block index>.rnky", payload CRCs on the GPU */
+RK_API rk_status rk_write_records(rk_ctx* ctx, const rk_records* records, const char* path_prefix);
 
 #ifdef __cplusplus
 }

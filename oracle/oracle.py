@@ -238,5 +238,33 @@ class Oracle:
                                                          self._p(flat, C.c_double)))
 
 
+    # ---- RNKY records (reference only): block_record.cpp:53-144 ----
+    def crc32(self, data: bytes) -> int:
+        self.lib.ref_crc32.restype = C.c_uint32
+        self.lib.ref_crc32.argtypes = [C.c_char_p, C.c_uint64]
+        return int(self.lib.ref_crc32(data, len(data)))
+
+    def write_block_record(self, index, payload, path):
+        p = np.ascontiguousarray(payload, dtype=np.float64)
+        self.lib.ref_write_block_record.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double),
+                                                    C.c_char_p]
+        if self.lib.ref_write_block_record(index, p.shape[0], p.shape[1], self._p(p, C.c_double), str(path).encode()):
+            raise OracleError(4, "write_block_record failed")
+
+    def read_block_record(self, path, cap=1 << 24):
+        """-> (index, payload) ; raises OracleError(7) on the reference's RecordError"""
+        idx, rows, kept = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        out = np.zeros(cap, dtype=np.float64)
+        self.lib.ref_read_block_record.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                                   C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.c_uint64]
+        st = self.lib.ref_read_block_record(str(path).encode(), C.byref(idx), C.byref(rows), C.byref(kept),
+                                            self._p(out, C.c_double), cap)
+        if st == 1:
+            raise OracleError(7, "RecordError")
+        if st:
+            raise OracleError(4, "read_block_record failed")
+        return idx.value, out[:rows.value * kept.value].reshape(rows.value, kept.value).copy()
+
+
 def available(kind: str) -> bool:
     return os.path.exists(PORT_SO if kind == "port" else REF_SO)

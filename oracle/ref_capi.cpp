@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "or_result.h"
+#include "ranky/block_record.hpp"
 #include "ranky/dense_matrix.hpp"
 #include "ranky/errors.hpp"
 #include "ranky/partition.hpp"
@@ -282,6 +283,40 @@ or_result* ref_full_svd(uint64_t rows, uint64_t cols, uint64_t nnz, const uint64
     res->v_cols = vm.cols();
     res->vm = copy_out(vm.values().data(), vm.values().size());
   });
+}
+
+// crc32 / write_block_record -- proj/src/block_record.cpp:53-106
+uint32_t ref_crc32(const void* data, uint64_t size) { return crc32(data, size); }
+
+int ref_write_block_record(uint32_t index, uint32_t rows, uint32_t kept, const double* payload, const char* path) {
+  try {
+    BlockResultRecord r;
+    r.block_index = index;
+    r.rows = rows;
+    r.kept = kept;
+    r.payload.assign(payload, payload + (uint64_t)rows * kept);
+    write_block_record(r, path);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// read_block_record: 0 ok (payload copied into out, rows*kept doubles), 1 RecordError, 2 other
+int ref_read_block_record(const char* path, uint32_t* index, uint32_t* rows, uint32_t* kept, double* out,
+                          uint64_t cap) {
+  try {
+    BlockResultRecord r = read_block_record(path);
+    *index = r.block_index;
+    *rows = r.rows;
+    *kept = r.kept;
+    for (uint64_t i = 0; i < r.payload.size() && i < cap; ++i) out[i] = r.payload[i];
+    return 0;
+  } catch (const RecordError&) {
+    return 1;
+  } catch (const std::exception&) {
+    return 2;
+  }
 }
 
 }  // extern "C"

@@ -730,6 +730,66 @@ rk_status rk_dev_outputs_free(rk_dev_outputs* o) {
   return RK_OK;
 }
 
+uint32_t rk_crc32(const void* data, uint64_t size) { return size ? crc32_host(data, size) : 0u; }
+
+rk_status rk_dev_crc32(rk_ctx* ctx, const void* d_data, const uint64_t* offsets, const uint64_t* lengths, uint64_t n,
+                       uint32_t* crcs) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (n && (!d_data || !offsets || !lengths || !crcs)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    crc32_device(static_cast<const unsigned char*>(d_data), std::vector<uint64_t>(offsets, offsets + n),
+                 std::vector<uint64_t>(lengths, lengths + n), crcs, ctx->c.stream);
+  });
+}
+
+rk_status rk_write_block_record(uint32_t block_index, uint32_t rows, uint32_t kept, const double* payload,
+                                const char* path) {
+  return guarded([&] {
+    if (!path) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    const uint64_t count = (uint64_t)rows * kept;
+    if (count && !payload) fail(RK_INVALID_ARGUMENT, "block record payload size mismatch");
+    write_record_file(block_index, rows, kept, payload, count ? crc32_host(payload, 8 * count) : 0u, path);
+  });
+}
+
+rk_status rk_read_block_record(const char* path, uint32_t* block_index, uint32_t* rows, uint32_t* kept,
+                               double** payload) {
+  return guarded([&] {
+    if (!path || !block_index || !rows || !kept || !payload) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    std::vector<double> p;
+    read_record_file(path, *block_index, *rows, *kept, p);
+    *payload = host_alloc<double>(p.size());
+    if (!p.empty()) std::memcpy(*payload, p.data(), p.size() * sizeof(double));
+  });
+}
+
+rk_status rk_write_records(rk_ctx* ctx, const rk_records* records, const char* path_prefix) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!records || !path_prefix) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    const uint64_t n = records->n_records, M = records->rows;
+    std::vector<uint64_t> off(n), len(n);
+    uint64_t total = 0;
+    for (uint64_t d = 0; d < n; ++d) {
+      off[d] = 8 * records->offset[d];
+      len[d] = 8 * M * records->kept[d];
+      total = std::max(total, off[d] + len[d]);
+    }
+    std::vector<uint32_t> crc(n, 0u);
+    if (total) {
+      DBuf<unsigned char> dev(total, s);
+      RK_CUDA_CHECK(cudaMemcpyAsync(dev.get(), records->payload, total, cudaMemcpyHostToDevice, s));
+      crc32_device(dev.get(), off, len, crc.data(), s);
+    }
+    for (uint64_t d = 0; d < n; ++d)
+      write_record_file((uint32_t)d, (uint32_t)M, records->kept[d], records->payload + records->offset[d], crc[d],
+                        std::string(path_prefix) + std::to_string(d) + ".rnky");
+  });
+}
+
 rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
                           double* a_norm) {
   return guarded([&] {

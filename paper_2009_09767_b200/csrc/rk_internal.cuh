@@ -308,6 +308,14 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
 // rounding) must not depend on how many blocks share the launch, so that the
 // sharded path is bitwise identical for every rank count.
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency = false);
+// RNKY records (rk_records.cu)
+uint32_t crc32_host(const void* data, uint64_t size);
+void crc32_device(const unsigned char* d_base, const std::vector<uint64_t>& off, const std::vector<uint64_t>& len,
+                  uint32_t* h_crc, cudaStream_t s);
+void write_record_file(uint32_t index, uint32_t rows, uint32_t kept, const double* payload, uint32_t crc,
+                       const std::string& path);
+void read_record_file(const std::string& path, uint32_t& index, uint32_t& rows, uint32_t& kept,
+                      std::vector<double>& payload);
 // ||A - U[:, :r] diag(sigma) V^T||_F^2 (exact, tile by tile) and ||A||_F^2
 void residual_device(const DevCsc& a, const double* u, uint32_t ku, const double* sigma, uint32_t r, const double* v,
                      int sms, double* h_res2, double* h_a2, cudaStream_t s);

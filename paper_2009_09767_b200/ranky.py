@@ -67,6 +67,10 @@ class RankyRuntimeError(RankyError, RuntimeError):
     pass
 
 
+class RecordError(RankyError, RuntimeError):
+    """ranky::RecordError (proj/include/ranky/errors.hpp:23-26): damaged block record"""
+
+
 class CudaError(RankyError, RuntimeError):
     pass
 
@@ -194,6 +198,12 @@ def lib():
                                  C.POINTER(Timing)], i32),
             "rk_dev_outputs_free": ([C.POINTER(DevOutputs)], i32),
             "rk_dev_residual": ([vp, vp, C.POINTER(DevOutputs), pdbl, pdbl], i32),
+            "rk_crc32": ([vp, u64], u32),
+            "rk_dev_crc32": ([vp, vp, pu64, pu64, u64, C.POINTER(C.c_uint32)], i32),
+            "rk_write_block_record": ([u32, u32, u32, pdbl, C.c_char_p], i32),
+            "rk_read_block_record": ([C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                      C.POINTER(pdbl)], i32),
+            "rk_write_records": ([vp, C.POINTER(_Records), C.c_char_p], i32),
             "rk_merge_tree_leaves": ([u64, u64, u64, u64], u64),
             "rk_dev_shard_factor": ([vp, vp, u64, i32, u64, u64, u64, u64, vp, C.POINTER(vp), C.POINTER(Timing)],
                                     i32),
@@ -226,6 +236,8 @@ def _check(status: int):
         raise CudaError(msg)
     if status == 6:
         raise MemoryError(msg)
+    if status == 7:
+        raise RecordError(msg)
     raise RankyError(f"status {status}: {msg}")
 
 
@@ -725,7 +737,7 @@ class BlockResultRecord:
 
     def __eq__(self, o):
         return (self.block_index == o.block_index and self.rows == o.rows and self.kept == o.kept
-                and np.array_equal(self.payload, o.payload))
+                and np.array_equal(np.ravel(self.payload), np.ravel(o.payload)))
 
 
 @dataclass
@@ -894,3 +906,51 @@ def dev_outputs_tensors(out):
     u = torch.as_tensor(_CudaArray(o.d_u, (o.rows, o.k_sigma)), device=dev) if o.k_sigma else None
     v = torch.as_tensor(_CudaArray(o.d_v, (o.cols, o.k_v)), device=dev) if o.d_v else None
     return sig, u, v
+
+
+# ---------------------------------------------------------------------------
+# RNKY block records (proj/src/block_record.cpp:51-144)
+
+def crc32(data) -> int:
+    """block_record.cpp:53-68 (CRC-32, reflected 0xEDB88320)"""
+    b = bytes(data) if not isinstance(data, np.ndarray) else np.ascontiguousarray(data).tobytes()
+    return int(lib().rk_crc32(b, len(b)))
+
+
+def write_block_record(record: BlockResultRecord, path) -> None:
+    """block_record.cpp:86-106: byte-identical RNKY file"""
+    pay = np.ascontiguousarray(record.payload, dtype=np.float64).ravel()
+    if pay.size != record.rows * record.kept:
+        raise InvalidArgument("block record payload size mismatch")
+    _check(lib().rk_write_block_record(record.block_index, record.rows, record.kept,
+                                       pay.ctypes.data_as(C.POINTER(C.c_double)), os.fsencode(str(path))))
+
+
+def read_block_record(path) -> BlockResultRecord:
+    """block_record.cpp:108-144 (RecordError on damage)"""
+    idx, rows, kept = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    p = C.POINTER(C.c_double)()
+    _check(lib().rk_read_block_record(os.fsencode(str(path)), C.byref(idx), C.byref(rows), C.byref(kept), C.byref(p)))
+    n = rows.value * kept.value
+    try:
+        pay = np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0)
+    finally:
+        lib().rk_host_free(p)
+    return BlockResultRecord(idx.value, rows.value, kept.value, pay)
+
+
+def write_records(records, path_prefix, ctx: Context | None = None) -> None:
+    """every record to '<path_prefix><block index>.rnky' (payload CRCs on the GPU);
+    records must be those of one pipeline call (block_index = 0, 1, ...)"""
+    if not records:
+        return
+    rows = records[0].rows
+    kept = np.array([r.kept for r in records], dtype=np.uint32)
+    offset = np.zeros(len(records), dtype=np.uint64)
+    offset[1:] = np.cumsum(kept.astype(np.uint64) * rows)[:-1]
+    payload = np.ascontiguousarray(np.concatenate([np.asarray(r.payload, np.float64).ravel() for r in records]))
+    if any(r.block_index != d or r.rows != rows for d, r in enumerate(records)):
+        raise InvalidArgument("write_records: records must be blocks 0..n-1 of one matrix")
+    rec = _Records(len(records), rows, kept.ctypes.data_as(C.POINTER(C.c_uint32)),
+                   offset.ctypes.data_as(C.POINTER(C.c_uint64)), payload.ctypes.data_as(C.POINTER(C.c_double)))
+    _check(lib().rk_write_records(_ctx(ctx), C.byref(rec), os.fsencode(str(path_prefix))))
