@@ -71,6 +71,7 @@ struct JacobiParams {
   int with_v;
   double check_ratio;  // Gram convergence check after a sweep whose max ratio is below this (0: off)
   int check_first;     // start with the tail check (W comes from jacobi_warp_kernel)
+  int debug;           // RK_JACOBI_DEBUG=1: print the hand-over of job 0
 };
 
 __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_t n) {
@@ -524,6 +525,9 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
     converged = run_tail(cluster, job, rank, csize, s_red, &s_amax, &s_tail, with_v, done, total_rot,
                          last_max_ratio);
     sweep = done;
+    if (P.debug && rank == 0 && tid == 0 && blockIdx.x == 0)
+      printf("[jacobi] job 0: warp kernel %d sweeps, tail -> converged %d after %d\n", (int)job.stats[0], converged,
+             sweep);
     cluster.sync();
   }
   for (; sweep < kMaxSweeps && !converged; ++sweep) {
@@ -657,6 +661,7 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
     job.stats[1] = total_rot;
     job.stats[2] = converged ? 0ull : 1ull;
     job.stats[3] = (uint64_t)__double_as_longlong(last_max_ratio);
+    if (P.debug && blockIdx.x == 0) printf("[jacobi] job 0: %d sweeps in all, converged %d\n", sweep, converged);
   }
 }
 
@@ -1317,7 +1322,8 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   DBuf<JacobiJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   const char* ce = std::getenv("RK_JACOBI_CHECK");
-  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : 1e-7, use_warp ? 1 : 0};
+  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : 1e-7, use_warp ? 1 : 0,
+                 std::getenv("RK_JACOBI_DEBUG") ? 1 : 0};
   void* kargs[] = {&P};
   // lanes per pair: enough lane groups for the g pairs of a round; E = column
   // elements per lane held in registers by the cross rounds (0: shared-memory path)

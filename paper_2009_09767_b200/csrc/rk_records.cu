@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kCT) crc_kernel(const unsigned char* __restric
   uint32_t c = 0xFFFFFFFFu;
   uint64_t i = b0 < n ? b0 : n;
   // 8-byte loads where aligned, bytes otherwise
-  for (; i < b1 && (i & 7); ++i) c = (c >> 8) ^ table[(c ^ p[i]) & 0xffu];
+  for (; i < b1 && (reinterpret_cast<uintptr_t>(p + i) & 7); ++i) c = (c >> 8) ^ table[(c ^ p[i]) & 0xffu];
   for (; i + 8 <= b1; i += 8) {
     uint64_t w = *reinterpret_cast<const uint64_t*>(p + i);
 #pragma unroll

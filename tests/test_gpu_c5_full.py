@@ -49,8 +49,8 @@ def test_c5_full_size(ref):
 
     dm = rk.DeviceMatrix(a)
     out, t = rk.dev_full_svd(dm, cfg.blocks, cfg.method, cfg.keep, cfg.seed, True, cfg.top_k)
-    mark(f"device pipeline: {t.total_ms / 1e3:.1f} s (blocks {t.blocks_ms / 1e3:.1f}, merge {t.merge_ms / 1e3:.1f}, "
-         f"V {t.recover_ms / 1e3:.1f})")
+    mark(f"device pipeline: {t.total_ms / 1e3:.1f} s (blocks {t.blocks_ms / 1e3:.1f} = QR {t.qr_ms / 1e3:.1f} + "
+         f"Jacobi {t.jacobi_ms / 1e3:.1f}; merge {t.merge_ms / 1e3:.1f}, V {t.recover_ms / 1e3:.1f})")
     try:
         sig_d, u_d, v_d = dev_outputs_tensors(out)
         sigma = sig_d.cpu().numpy()
@@ -65,9 +65,19 @@ def test_c5_full_size(ref):
         res, anorm = dev_residual(dm, out)
         mark(f"sigma[:4] {sigma[:4]}, sigma[63] {sigma[63]:.6e}; V orthonormality {orth:.2e}; "
              f"residual/||A|| {res / anorm:.6e}")
-        assert orth <= 1e-9
+        # with keep = 64 per block the proxy P P^T is A A^T minus the blocks' tails, so
+        # V = A^T U Sigma^-1 is orthonormal only up to that truncation (the reference's
+        # algorithm, not rounding): a sanity bound, not the parity check
+        assert orth <= 1e-5
         # top-64 of a rank-2048 matrix: the residual is the tail's mass, bounded by it
         assert res <= anorm
+        # V rows of a sampled block, bit-exact against the reference's recover_right_vectors
+        d = 1234
+        rng_d = p.range(d)
+        u = u_d.cpu().numpy()
+        vr = ref.recover_right_vectors(coo_of(rk.block_view(rep, p, d)), u[:, :k], sigma[:k], rk.K_RANK_TOL)
+        assert np.array_equal(v_d[rng_d.begin:rng_d.end].cpu().numpy(), vr)
+        mark("V block bit-exact")
     finally:
         rk.dev_outputs_free(out)
         dm.close()
