@@ -108,6 +108,46 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+class NvmlClockSampler:
+    """The same samples through NVML from a thread of this process (no nvidia-smi
+    process contending for the driver while the steps run)."""
+
+    def __init__(self, device, period=0.1):
+        self.device, self.period = device, period
+        self.rows, self.stop_flag, self.thread = [], False, None
+
+    def start(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            self.thread = None
+            return
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+        def loop():
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self.stop_flag:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, smax, sorted(k for k, b in bits.items() if r & b)))
+                time.sleep(self.period)
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if not self.thread:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_flag = True
+        self.thread.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({x for r in self.rows for x in r[2]}), "samples": len(self.rows), "source": "nvml"}
+
+
 # --------------------------------------------------------------------------- peaks
 
 def measured_peaks():
@@ -308,7 +348,7 @@ def main():
         step()
         flush.zero_()
     barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local) if os.environ.get("RK_CLOCKS", "nvml") == "smi" else NvmlClockSampler(local)
     clocks.start()
     ms_steps, launches, timings = [], 0, []
     barrier()
