@@ -1,3 +1,4 @@
+"""c4 (1024 x 16.8M) device pipeline timing and memory (development tool)."""
 import sys, os, time
 sys.path.insert(0, "/root/repo")
 import torch
