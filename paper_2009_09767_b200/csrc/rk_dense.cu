@@ -182,9 +182,7 @@ __device__ __forceinline__ int rotate_pair_q(double* __restrict__ wp, double* __
 // warp-uniform (the two or four lane groups of a warp may disagree on whether
 // their pair is frozen or rotates; that is handled with predication), so the
 // group reductions use full-warp shuffles that stay inside the group (xor < Q).
-// RELOAD: B values are read from shared memory again for the update instead of
-// being held in registers (E fewer registers: three CTAs per SM instead of two)
-template <int Q, int E, bool EXACT, bool RELOAD = false>
+template <int Q, int E, bool EXACT>
 __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint32_t rows_rt, uint32_t g,
                                                  double* sAlpha, double freeze, double& max_r2,
                                                  unsigned long long& my_rot) {
@@ -206,13 +204,12 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
     double* pb = bbase + (uint64_t)jl * ldS;
     const double aB = sAlpha[g + jl];
     const bool live = active && !(aA <= freeze || aB <= freeze);
-    double b[RELOAD ? 1 : E];
+    double b[E];
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const double bk = (EXACT || lq + Q * k < (int)rows) ? pb[Q * k] : 0.0;  // frozen pairs: gamma unused
-      if constexpr (!RELOAD) b[k] = bk;
-      const double pr = a[k] * bk;
+      b[k] = (EXACT || lq + Q * k < (int)rows) ? pb[Q * k] : 0.0;  // frozen pairs: gamma unused
+      const double pr = a[k] * b[k];
       if ((k & 3) == 0) acc0 += pr;
       else if ((k & 3) == 1) acc1 += pr;
       else if ((k & 3) == 2) acc2 += pr;
@@ -229,10 +226,7 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
       if (rot) rotation_cs(aA, aB, gamma, c, sn);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
-        double xq;
-        if constexpr (RELOAD) xq = (EXACT || lq + Q * k < (int)rows) ? pb[Q * k] : 0.0;
-        else xq = b[k];
-        const double xp = a[k];
+        const double xp = a[k], xq = b[k];
         a[k] = c * xp - sn * xq;
         if (rot && (EXACT || lq + Q * k < (int)rows)) pb[Q * k] = sn * xp + c * xq;
       }
@@ -325,9 +319,8 @@ __device__ uint32_t tail_check(cg::cluster_group& cluster, const JacobiJob& job,
   __syncthreads();
   const double freeze = kJacobiTol * kJacobiTol * (*s_amax);
   TailShared* ts0 = cluster.map_shared_rank(ts, 0);
-  // 16 x 16 blocks of the lower triangle (2 x 2 DMMA tiles per warp: few registers,
-  // the kernel's register budget belongs to the rounds)
-  constexpr int kTB = 2;
+  // 32 x 32 blocks of the lower triangle (4 x 4 DMMA tiles per warp)
+  constexpr int kTB = 4;
   const uint32_t nb = (n + 8 * kTB - 1) / (8 * kTB);
   const uint32_t T = nb * (nb + 1) / 2;
   const int lr = lane >> 2, lc = lane & 3;
@@ -495,8 +488,8 @@ __device__ bool run_tail(cg::cluster_group& cluster, const JacobiJob& job, unsig
   return false;
 }
 
-template <int Q, int E, bool EXACT, bool RELOAD = false>
-__global__ void __launch_bounds__(kJThreads, (RELOAD ? 3 : (E <= 16 ? 2 : 1))) jacobi_cluster_kernel(JacobiParams P) {
+template <int Q, int E, bool EXACT>
+__global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
@@ -605,7 +598,7 @@ __global__ void __launch_bounds__(kJThreads, (RELOAD ? 3 : (E <= 16 ? 2 : 1))) j
         }
         // cross rounds: (A_i, B_{(i + r) mod g})
         if constexpr (E > 0) {
-          cross_rounds_reg<Q, E, EXACT, RELOAD>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
+          cross_rounds_reg<Q, E, EXACT>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
         } else {
           for (uint32_t r = 0; r < g; ++r) {
             for (uint32_t t = grp_id; t < g; t += kGroups) {
@@ -1362,10 +1355,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     case 32: exact ? launch(jacobi_cluster_kernel<QQ, 32, true>) : launch(jacobi_cluster_kernel<QQ, 32, false>); break; \
     default: launch(jacobi_cluster_kernel<QQ, 0, false>); break;                       \
   }
-  const char* re = std::getenv("RK_JACOBI_RELOAD");
-  if (re && re[0] == '1' && Q == 16 && E == 16 && exact) {
-    launch(jacobi_cluster_kernel<16, 16, true, true>);
-  } else if (Q == 8) { RK_JAC_E(8) }
+  if (Q == 8) { RK_JAC_E(8) }
   else if (Q == 16) { RK_JAC_E(16) }
   else { RK_JAC_E(32) }
 #undef RK_JAC_E
