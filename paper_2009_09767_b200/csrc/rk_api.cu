@@ -36,13 +36,28 @@ void trace_launch(const char* file, int line) {
 }
 void* host_alloc_bytes(size_t bytes);
 
+thread_local PinnedArena* g_arena = nullptr;
+
 CallScope::CallScope(Ctx* c) {
   cudaGetDevice(&prev_device);
   if (prev_device != c->device) RK_CUDA_CHECK(cudaSetDevice(c->device));
   prev_counter = g_launch_counter;
   g_launch_counter = &c->launches;
+  PinnedArena& a = c->arena;
+  if (!a.base) {
+    constexpr size_t kArena = size_t(16) << 20;
+    if (cudaMallocHost(reinterpret_cast<void**>(&a.base), kArena) == cudaSuccess) a.cap = kArena;
+    else { a.base = nullptr; cudaGetLastError(); }
+  }
+  if (a.used) {  // the previous call's uploads must have been consumed before the rewind
+    cudaStreamSynchronize(c->stream);
+    a.used = 0;
+  }
+  prev_arena = g_arena;
+  g_arena = &a;
 }
 CallScope::~CallScope() {
+  g_arena = prev_arena;
   g_launch_counter = prev_counter;
   int cur = -1;
   cudaGetDevice(&cur);
@@ -344,6 +359,7 @@ rk_status rk_ctx_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   for (auto& ev : ctx->c.ev) cudaEventDestroy(ev);
+  if (ctx->c.arena.base) cudaFreeHost(ctx->c.arena.base);
   cudaStreamDestroy(ctx->c.own);
   delete ctx;
   return RK_OK;

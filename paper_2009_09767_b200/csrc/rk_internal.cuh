@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -114,9 +115,29 @@ inline void to_host(std::vector<T>& dst, const T* src, size_t n, cudaStream_t s)
   dst.resize(n);
   if (n) RK_CUDA_CHECK(cudaMemcpyAsync(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
 }
+// Pinned staging for the small host -> device uploads of an API call (job tables,
+// pointer arrays). cudaMemcpyAsync from pageable memory waits for the stream, so
+// every such upload would be a hidden host <-> device round trip; from the arena it
+// is asynchronous. The arena belongs to the context and is rewound at the start of
+// each call (after the previous call's uploads have been consumed).
+struct PinnedArena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+};
+extern thread_local PinnedArena* g_arena;
 template <class T>
 inline void to_device(T* dst, const T* src, size_t n, cudaStream_t s) {
-  if (n) RK_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  if (!n) return;
+  const size_t bytes = n * sizeof(T);
+  PinnedArena* a = g_arena;
+  if (a && a->base && a->used + bytes + 16 <= a->cap) {
+    char* p = a->base + ((a->used + 15) & ~size_t(15));
+    std::memcpy(p, src, bytes);
+    a->used = (size_t)(p - a->base) + bytes;
+    RK_CUDA_CHECK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s));
+  } else {
+    RK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  }
 }
 inline void sync(cudaStream_t s) { RK_CUDA_CHECK(cudaStreamSynchronize(s)); }
 
@@ -229,12 +250,14 @@ struct Ctx {
   size_t smem_optin = 227 * 1024;
   uint64_t launches = 0;
   cudaEvent_t ev[12] = {};  // [0..3] block stage, [3..7] pipeline stages, [8..11] spare
+  PinnedArena arena;        // see to_device
 };
 
 // RAII: activates the context's device and launch counter for one API call
 struct CallScope {
   int prev_device = -1;
   uint64_t* prev_counter = nullptr;
+  PinnedArena* prev_arena = nullptr;
   explicit CallScope(Ctx* c);
   ~CallScope();
 };
