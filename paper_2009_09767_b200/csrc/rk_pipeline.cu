@@ -263,6 +263,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   for (uint64_t i = 0; i < nblk; ++i) done[i] = skip[i];
 
   // Jacobi + finalize of a set of W slots; records stats and writes payloads
+  std::vector<double> sigma_host;  // sorted sigma of the Gram-route slots (read with the Jacobi stats)
   auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
                              bool gram_ok, double* sigma_all /* nullable: slots x cols_pad */) {
     const size_t nb = slots.size();
@@ -305,6 +306,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       }
     }
     finalize_batched(fj, s);
+    if (sigma_all) to_host(sigma_host, sigma_all, (uint64_t)nb * cols_pad_full, s);  // read with the stats
     std::vector<JacobiStats> js = read_stats(stats.get(), nb, s);  // synchronizes
     float ms_j = 0;
     cudaEventElapsedTime(&ms_j, c.ev[9], c.ev[10]);
@@ -369,9 +371,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       if (slots.empty()) continue;
       DBuf<double> sig((uint64_t)slots.size() * cols_pad_full, s);
       jacobi_finalize(slots, cols, blocks, true, sig.get());
-      std::vector<double> hs;
-      to_host(hs, sig.get(), sig.n, s);
-      sync(s);
+      const std::vector<double>& hs = sigma_host;
       for (size_t q = 0; q < slots.size(); ++q) {
         const double smax = hs[q * cols_pad_full], smin = hs[q * cols_pad_full + M - 1];
         const uint64_t i = blocks[q];
@@ -647,25 +647,37 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = cols; jj[0].cols_pad = cp;
   jj[0].alpha = alpha.get(); jj[0].stats = stats.get(); jj[0].gram_ok = gram_ok ? 1u : 0u;
   jacobi_batched(jj, s, c.num_sms, c.smem_optin, /*latency=*/true);
-  JacobiStats js = read_stats(stats.get(), 1, s)[0];
-  out.sweeps = js.sweeps;
-  out.rotations = js.rotations;
-  if (js.failed) {
-    if (gram_ok) return INFINITY;  // the caller falls back to the TSQR route
-    throw_convergence(js.residual);
-  }
+  // finalize right behind the Jacobi (its result is discarded if the Jacobi
+  // failed), then one readback of the statistics, the sorted sigma and the
+  // deficiency flags: one host round trip instead of three
   DBuf<uint32_t> order(cp, s);
   DBuf<double> scratch(cp, s), sig_all(cp, s);
   DBuf<uint8_t> def(k ? k : 1, s);
+  def.zero();
   FinalJob f;
   std::memset(&f, 0, sizeof f);
   f.w = W.get(); f.rows = M; f.cols = cp; f.k = k;
   f.u = out.u.get(); f.sigma = out.sigma.get(); f.sigma_all = sig_all.get();
   f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
   finalize_batched({f}, s);
+  std::vector<uint64_t> hst;
   std::vector<double> hs;
+  std::vector<uint8_t> hdef;
+  to_host(hst, stats.get(), 8, s);
   to_host(hs, sig_all.get(), cols, s);
-  if (any_flag(def.get(), k, s)) complete_and_sign(c, out.u.get(), M, k, def.get(), nullptr, 0);
+  to_host(hdef, def.get(), k, s);
+  sync(s);
+  out.sweeps = hst[0];
+  out.rotations = hst[1];
+  if (hst[2] != 0) {
+    if (gram_ok) return INFINITY;  // the caller falls back to the TSQR route
+    double residual;
+    std::memcpy(&residual, &hst[3], 8);
+    throw_convergence(residual);
+  }
+  bool deficient = false;
+  for (uint8_t x : hdef) deficient = deficient || x;
+  if (deficient) complete_and_sign(c, out.u.get(), M, k, def.get(), nullptr, 0);
   const double smin = cols ? hs[cols - 1] : 0.0;
   return smin > 0.0 ? hs[0] / smin : INFINITY;
 }
