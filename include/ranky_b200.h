@@ -15,8 +15,11 @@
  * (proj/include/ranky/errors.hpp:10-38 and the std:: exceptions it throws).
  *
  * Sparse inputs are the reference's SparseMatrix entries: an array of
- * rk_entry {row, col, value} sorted by (row, col), without duplicates,
- * explicit zeros or out-of-range indices (proj/include/ranky/sparse_matrix.hpp:9-48).
+ * rk_entry {row, col, value} without duplicates, explicit zeros or out-of-range
+ * indices (proj/include/ranky/sparse_matrix.hpp:9-48). Any order is accepted:
+ * like the reference constructor (sparse_matrix.cpp:12-30), unsorted entries
+ * are sorted by (row, col) -- on the device -- before validation, and the first
+ * invalid entry in sorted order is reported with the reference's message.
  * rk_entry has the exact layout of ranky::Entry, so a C++ caller passes
  * SparseMatrix::entries().data() unchanged.
  *
@@ -68,7 +71,7 @@ typedef struct rk_entry {
 
 typedef struct rk_sparse_view {
   uint64_t rows, cols, nnz;
-  const rk_entry* entries; /* host, sorted by (row, col) */
+  const rk_entry* entries; /* host; any order (sorted on the device if needed) */
 } rk_sparse_view;
 
 /* SvdResult -- proj/include/ranky/svd.hpp:15-19. u: u_rows x u_cols row-major,

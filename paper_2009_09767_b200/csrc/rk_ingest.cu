@@ -7,6 +7,8 @@
 //  * csr_to_csc: column-major twin, rows ascending inside each column.
 //  * apply_edges: the repaired matrix = input + repair edges with value 1.0
 //    (RepairWorkspace::to_matrix, proj/src/repair.cpp:147-160), in both formats.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "rk_internal.cuh"
 
 namespace rk {
@@ -49,6 +51,33 @@ __global__ void entries_to_csr(const rk_entry* e, uint64_t nnz, uint64_t rows, u
     if (i + 1 == nnz)
       for (uint64_t r = x.row + 1; r <= rows; ++r) row_ptr[r] = nnz;
   }
+}
+
+// first index i > 0 with e[i-1] > e[i] in (row, col) order (UINT64_MAX: sorted)
+__global__ void find_unsorted(const rk_entry* e, uint64_t nnz, unsigned long long* first) {
+  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const rk_entry x = e[i], y = e[i - 1];
+    if (y.row > x.row || (y.row == x.row && y.col > x.col)) atomicMin(first, (unsigned long long)i);
+  }
+}
+
+// sort key (row, col) in one u64; indices >= 2^32 only occur in out-of-range
+// entries (dimensions are < 2^32), clamped -- they fail validation either way
+__global__ void make_keys(const rk_entry* e, uint64_t nnz, uint64_t* key, uint64_t* idx) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e[i].row < 0xffffffffull ? e[i].row : 0xffffffffull;
+    const uint64_t c = e[i].col < 0xffffffffull ? e[i].col : 0xffffffffull;
+    key[i] = (r << 32) | c;
+    idx[i] = i;
+  }
+}
+
+__global__ void gather_entries(const rk_entry* e, const uint64_t* idx, uint64_t nnz, rk_entry* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = e[idx[i]];
 }
 
 __global__ void empty_row_ptr(uint64_t* row_ptr, uint64_t rows) {
@@ -231,7 +260,34 @@ void upload_entries(const rk_sparse_view& a, DevMatrix& m, cudaStream_t s) {
     RK_LAUNCH_CHECK();
   } else {
     DBuf<rk_entry> staged(a.nnz, s);
-    to_device(staged.get(), a.entries, a.nnz, s);
+    RK_CUDA_CHECK(cudaMemcpyAsync(staged.get(), a.entries, a.nnz * sizeof(rk_entry), cudaMemcpyHostToDevice, s));
+    // any order is accepted, as by the reference constructor, which sorts by
+    // (row, col) before validating (sparse_matrix.cpp:12-14): unsorted input is
+    // sorted here with a stable device radix sort
+    {
+      DBuf<unsigned long long> first(1, s);
+      RK_CUDA_CHECK(cudaMemsetAsync(first.get(), 0xff, sizeof(unsigned long long), s));
+      find_unsorted<<<blocks_for(a.nnz), kT, 0, s>>>(staged.get(), a.nnz, first.get());
+      RK_LAUNCH_CHECK();
+      unsigned long long h_first = 0;
+      RK_CUDA_CHECK(cudaMemcpyAsync(&h_first, first.get(), sizeof h_first, cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (h_first != ~0ull) {
+        DBuf<uint64_t> k_in(a.nnz, s), k_out(a.nnz, s), i_in(a.nnz, s), i_out(a.nnz, s);
+        make_keys<<<blocks_for(a.nnz), kT, 0, s>>>(staged.get(), a.nnz, k_in.get(), i_in.get());
+        RK_LAUNCH_CHECK();
+        size_t tmp_bytes = 0;
+        RK_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in.get(), k_out.get(), i_in.get(),
+                                                      i_out.get(), a.nnz, 0, 64, s));
+        DBuf<unsigned char> tmp(tmp_bytes ? tmp_bytes : 1, s);
+        RK_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, k_in.get(), k_out.get(), i_in.get(),
+                                                      i_out.get(), a.nnz, 0, 64, s));
+        DBuf<rk_entry> sorted(a.nnz, s);
+        gather_entries<<<blocks_for(a.nnz), kT, 0, s>>>(staged.get(), i_out.get(), a.nnz, sorted.get());
+        RK_LAUNCH_CHECK();
+        staged = std::move(sorted);
+      }
+    }
     DBuf<unsigned long long> status(2, s);
     RK_CUDA_CHECK(cudaMemsetAsync(status.get(), 0xff, 2 * sizeof(unsigned long long), s));
     entries_to_csr<<<blocks_for(a.nnz), kT, 0, s>>>(staged.get(), a.nnz, a.rows, a.cols, c.ptr.get(),
@@ -241,14 +297,19 @@ void upload_entries(const rk_sparse_view& a, DevMatrix& m, cudaStream_t s) {
     RK_CUDA_CHECK(cudaMemcpyAsync(&bad, status.get(), sizeof bad, cudaMemcpyDeviceToHost, s));
     sync(s);
     if (bad != ~0ull) {
-      const rk_entry& x = a.entries[bad];
+      rk_entry pair[2];  // (bad - 1, bad) of the (sorted) device array
+      const uint64_t lo = bad ? bad - 1 : 0;
+      RK_CUDA_CHECK(cudaMemcpyAsync(pair, staged.get() + lo, (bad ? 2 : 1) * sizeof(rk_entry),
+                                    cudaMemcpyDeviceToHost, s));
+      sync(s);
+      const rk_entry& x = bad ? pair[1] : pair[0];
       std::string at = "(" + std::to_string(x.row) + ", " + std::to_string(x.col) + ")";
       if (x.row >= a.rows || x.col >= a.cols)
         fail(RK_INVALID_ARGUMENT, "sparse entry " + at + " outside " + std::to_string(a.rows) + "x" +
                                       std::to_string(a.cols));
       if (x.value == 0.0) fail(RK_INVALID_ARGUMENT, "sparse entry " + at + " stores zero");
-      const rk_entry& y = a.entries[bad - 1];
-      if (y.row == x.row && y.col == x.col) fail(RK_INVALID_ARGUMENT, "duplicate sparse entry " + at);
+      const rk_entry& y = pair[0];
+      if (bad && y.row == x.row && y.col == x.col) fail(RK_INVALID_ARGUMENT, "duplicate sparse entry " + at);
       fail(RK_INVALID_ARGUMENT, "sparse entries must be sorted by (row, col); entry " +
                                     std::to_string(bad) + " " + at + " is out of order");
     }
