@@ -315,7 +315,7 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
     widest = std::max(widest, j.n);
   }
   if (h_max > qr_max_rows()) fail(RK_RUNTIME, "qr_batched: matrix taller than a panel can stage");
-  const size_t budget = 200 * 1024;
+  const size_t budget = 224 * 1024;  // sm_100a opt-in limit is 227 KB
   int nb = 16;
   while (nb > 1 && (nb == 16 ? qr_smem<16>(h_max) : nb == 8 ? qr_smem<8>(h_max) : nb == 4 ? qr_smem<4>(h_max)
                                                                                           : qr_smem<2>(h_max)) > budget)
