@@ -182,11 +182,16 @@ __device__ __forceinline__ int rotate_pair_q(double* __restrict__ wp, double* __
 // warp-uniform (the two or four lane groups of a warp may disagree on whether
 // their pair is frozen or rotates; that is handled with predication), so the
 // group reductions use full-warp shuffles that stay inside the group (xor < Q).
-template <int Q, int E, bool EXACT>
-__device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint32_t rows_rt, uint32_t g,
+// GT > 0: the group size g is the compile-time constant GT (with EXACT rows the
+// whole round loop unrolls: the B column of round r is a constant offset from the
+// group's own, wrapped with a mask)
+template <int Q, int E, bool EXACT, int GT = 0>
+__device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS_rt, uint32_t rows_rt, uint32_t g_rt,
                                                  double* sAlpha, double freeze, double& max_r2,
                                                  unsigned long long& my_rot) {
   const uint32_t rows = EXACT ? (uint32_t)(Q * E) : rows_rt;
+  const uint32_t g = GT > 0 ? (uint32_t)GT : g_rt;
+  const uint32_t ldS = (EXACT && GT > 0) ? (uint32_t)(Q * E + 8) : ldS_rt;
   const int tid = threadIdx.x;
   const int grp = tid / Q, lq = tid & (Q - 1);
   const bool active = (uint32_t)grp < g;
@@ -200,7 +205,9 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
   }
   uint32_t jl = active ? (uint32_t)grp : 0u;  // (grp + r) mod g, advanced incrementally
   double* const bbase = sW + (uint64_t)g * ldS + lq;
+#pragma unroll(GT > 0 ? 4 : 1)
   for (uint32_t r = 0; r < g; ++r) {
+    if (GT > 0 && (GT & (GT - 1)) == 0) jl = (uint32_t)(grp + r) & (uint32_t)(GT - 1);
     double* pb = bbase + (uint64_t)jl * ldS;
     const double aB = sAlpha[g + jl];
     const bool live = active && !(aA <= freeze || aB <= freeze);
@@ -240,7 +247,7 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS, uint3
         }
       }
     }
-    jl = (jl + 1 == g) ? 0u : jl + 1;
+    if (!(GT > 0 && (GT & (GT - 1)) == 0)) jl = (jl + 1 == g) ? 0u : jl + 1;
     __syncthreads();
   }
   if (active) {
@@ -488,7 +495,7 @@ __device__ bool run_tail(cg::cluster_group& cluster, const JacobiJob& job, unsig
   return false;
 }
 
-template <int Q, int E, bool EXACT>
+template <int Q, int E, bool EXACT, int GT = 0>
 __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
         }
         // cross rounds: (A_i, B_{(i + r) mod g})
         if constexpr (E > 0) {
-          cross_rounds_reg<Q, E, EXACT>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
+          cross_rounds_reg<Q, E, EXACT, GT>(sW, ldS, rows, g, sAlpha, freeze, my_ratio, my_rot);
         } else {
           for (uint32_t r = 0; r < g; ++r) {
             for (uint32_t t = grp_id; t < g; t += kGroups) {
@@ -1355,7 +1362,10 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     case 32: exact ? launch(jacobi_cluster_kernel<QQ, 32, true>) : launch(jacobi_cluster_kernel<QQ, 32, false>); break; \
     default: launch(jacobi_cluster_kernel<QQ, 0, false>); break;                       \
   }
-  if (Q == 8) { RK_JAC_E(8) }
+  const char* ue = std::getenv("RK_JACOBI_UNROLL");
+  if (Q == 16 && E == 16 && exact && g == 16 && !(ue && ue[0] == '0')) {
+    launch(jacobi_cluster_kernel<16, 16, true, 16>);  // c2's blocks: fully unrolled rounds
+  } else if (Q == 8) { RK_JAC_E(8) }
   else if (Q == 16) { RK_JAC_E(16) }
   else { RK_JAC_E(32) }
 #undef RK_JAC_E

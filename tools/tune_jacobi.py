@@ -6,9 +6,9 @@ from paper_2009_09767_b200 import configs
 cfg = configs.CONFIGS["c2"]
 a = cfg.generate()
 dm = rk.DeviceMatrix(a)
-variants = [dict(), dict(RK_JACOBI_CHECK="1e-5")]
+variants = [dict(), dict(RK_JACOBI_UNROLL="0")]
 for env in variants:
-    for k in ("RK_JACOBI_DIRECT", "RK_JACOBI_GMAX", "RK_JACOBI_Q", "RK_JACOBI_CHECK", "RK_JACOBI_WARP", "RK_JACOBI_SINGLE_G", "RK_JACOBI_CLUSTER", "RK_JACOBI_RELOAD"):
+    for k in ("RK_JACOBI_DIRECT", "RK_JACOBI_GMAX", "RK_JACOBI_Q", "RK_JACOBI_CHECK", "RK_JACOBI_WARP", "RK_JACOBI_SINGLE_G", "RK_JACOBI_CLUSTER", "RK_JACOBI_UNROLL"):
         os.environ.pop(k, None)
     os.environ.update(env)
     ts = []
