@@ -1363,8 +1363,11 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     default: launch(jacobi_cluster_kernel<QQ, 0, false>); break;                       \
   }
   const char* ue = std::getenv("RK_JACOBI_UNROLL");
-  if (Q == 16 && E == 16 && exact && g == 16 && !(ue && ue[0] == '0')) {
-    launch(jacobi_cluster_kernel<16, 16, true, 16>);  // c2's blocks: fully unrolled rounds
+  const bool unroll = !(ue && ue[0] == '0');
+  if (unroll && Q == 16 && E == 16 && exact && g == 16) {
+    launch(jacobi_cluster_kernel<16, 16, true, 16>);  // c2's blocks: compile-time group count
+  } else if (unroll && Q == 32 && E == 8 && exact && g == 8) {
+    launch(jacobi_cluster_kernel<32, 8, true, 8>);  // c2's merge (latency plan)
   } else if (Q == 8) { RK_JAC_E(8) }
   else if (Q == 16) { RK_JAC_E(16) }
   else { RK_JAC_E(32) }
