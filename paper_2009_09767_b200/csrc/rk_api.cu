@@ -36,6 +36,67 @@ void trace_launch(const char* file, int line) {
 }
 void* host_alloc_bytes(size_t bytes);
 
+namespace {
+struct ProfMark {
+  const char* name;
+  std::chrono::steady_clock::time_point t;
+  cudaEvent_t ev;
+};
+thread_local std::vector<ProfMark> g_prof;
+bool prof_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("RK_HOSTPROF");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+}  // namespace
+
+void prof_mark(cudaStream_t s, const char* name) {
+  if (!prof_on()) return;
+  ProfMark m{name, std::chrono::steady_clock::now(), nullptr};
+  cudaEventCreate(&m.ev);
+  cudaEventRecord(m.ev, s);
+  g_prof.push_back(m);
+}
+
+void prof_flush() {
+  if (!prof_on() || g_prof.empty()) return;
+  cudaEventSynchronize(g_prof.back().ev);
+  std::fprintf(stderr, "[rk prof] %-28s %10s %10s\n", "segment (ends at mark)", "host ms", "device ms");
+  for (size_t i = 1; i < g_prof.size(); ++i) {
+    float dev = 0;
+    cudaEventElapsedTime(&dev, g_prof[i - 1].ev, g_prof[i].ev);
+    const double host = std::chrono::duration<double, std::milli>(g_prof[i].t - g_prof[i - 1].t).count();
+    std::fprintf(stderr, "[rk prof] %-28s %10.3f %10.3f\n", g_prof[i].name, host, dev);
+  }
+  for (auto& m : g_prof) cudaEventDestroy(m.ev);
+  g_prof.clear();
+}
+
+size_t device_free_bytes(Ctx& c, uint64_t want) {
+  cudaMemPool_t pool;
+  uint64_t used = 0, reserved = 0;
+  const bool have_pool = cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess &&
+                         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+                         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess;
+  cudaGetLastError();
+  if (have_pool && c.free_known) {
+    // free now = free0 - (reserved - reserved0); the pool's reserved-but-unused part is ours too
+    const int64_t est = (int64_t)c.free0 + (int64_t)c.reserved0 - (int64_t)used;
+    if (est > 0 && (uint64_t)est >= want) return (size_t)est;
+  }
+  size_t fr = 0, tot = 0;
+  RK_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+  if (have_pool) {
+    c.free_known = true;
+    c.free0 = fr;
+    c.reserved0 = reserved;
+    return fr + (reserved - std::min(used, reserved));
+  }
+  return fr;
+}
+
 thread_local PinnedArena* g_arena = nullptr;
 
 CallScope::CallScope(Ctx* c) {
@@ -212,6 +273,7 @@ void report_to_host(const RepairOut& r, const Partition& p, rk_repair_report* ou
 std::unique_ptr<DevMatrix> repair_and_apply(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method,
                                             uint64_t seed, RepairOut& rep) {
   repair_device(a, p, method, seed, rep, c.stream);
+  prof_mark(c.stream, "repair_device");
   if (rep.edges.n == 0) return nullptr;
   auto out = std::make_unique<DevMatrix>();
   apply_edges(a, rep.edges, *out, c.stream);
@@ -262,14 +324,18 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   const uint64_t launches0 = c.launches;
   cudaEvent_t ev0 = c.ev[3], ev1 = c.ev[4], ev2 = c.ev[5], ev3 = c.ev[6], ev4 = c.ev[7];
   RK_CUDA_CHECK(cudaEventRecord(ev0, s));
+  prof_mark(s, "start");
   fr.repaired = repair_and_apply(c, a, p, method, seed, fr.rep);
+  prof_mark(s, "repair");
   const DevMatrix& rep = fr.repaired ? *fr.repaired : a;
   RK_CUDA_CHECK(cudaEventRecord(ev1, s));
   block_stage(c, rep, p, 0, p.blocks, keep, fr.blocks, nullptr);
   if (any_failure(fr.blocks)) throw_block_failure(fr.blocks, 0);
   RK_CUDA_CHECK(cudaEventRecord(ev2, s));
+  prof_mark(s, "blocks (end)");
   merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
   RK_CUDA_CHECK(cudaEventRecord(ev3, s));
+  prof_mark(s, "merge (end)");
   if (!(flags & RK_WANT_RECORDS)) fr.blocks.payload.release();  // P is not an output: make room for V
   if (flags & RK_WANT_V) {
     const uint32_t k = fr.merge.k;
@@ -289,7 +355,9 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
     }
   }
   RK_CUDA_CHECK(cudaEventRecord(ev4, s));
+  prof_mark(s, "V");
   sync(s);
+  prof_flush();
   if (t) {
     std::memset(t, 0, sizeof *t);
     t->repair_ms = elapsed(ev0, ev1);

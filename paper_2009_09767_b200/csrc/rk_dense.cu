@@ -1008,6 +1008,8 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
 // ===========================================================================
 
 constexpr int kFThreads = 512;
+// finalize_kernel leaves the output columns' flags in the high bits of order[j]
+constexpr uint32_t kOrderFlip = 0x80000000u, kOrderDef = 0x40000000u, kOrderSrc = 0x3fffffffu;
 
 __global__ void __launch_bounds__(kFThreads) finalize_kernel(const FinalJob* jobs) {
   const FinalJob J = jobs[blockIdx.x];
@@ -1039,6 +1041,7 @@ __global__ void __launch_bounds__(kFThreads) finalize_kernel(const FinalJob* job
   const double thr = kRankTol * smax;
   if (J.sigma_all)
     for (uint32_t j = tid; j < cols; j += kFThreads) J.sigma_all[j] = sig[J.order[j]];
+  __syncthreads();  // order[] gets its flag bits below
   for (uint32_t j = warp; j < J.k; j += nw) {
     const uint32_t src = J.order[j];
     const double s = sig[src];
@@ -1058,19 +1061,62 @@ __global__ void __launch_bounds__(kFThreads) finalize_kernel(const FinalJob* job
         if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
       }
     }
-    const double flip = (!deficient && (wj[arg] / s) < 0.0) ? -1.0 : 1.0;
-    if (J.sigma && lane == 0) J.sigma[j] = s;
-    if (J.deficient && lane == 0) J.deficient[j] = deficient ? 1 : 0;
-    for (uint32_t i = lane; i < rows; i += 32) {
-      const double u = deficient ? 0.0 : flip * (wj[i] / s);
-      if (J.u) J.u[(uint64_t)i * J.k + j] = u;
-      if (J.payload) J.payload[(uint64_t)i * J.k + j] = deficient ? (s > 0.0 ? wj[i] : 0.0) : u * s;
-    }
-    if (J.v_out) {
-      const double* vs = J.v_in + (uint64_t)src * J.ldv;
-      for (uint32_t i = lane; i < cols; i += 32) J.v_out[(uint64_t)i * J.k + j] = flip * vs[i];
+    const bool flip = !deficient && (wj[arg] / s) < 0.0;
+    if (lane == 0) {
+      if (J.sigma) J.sigma[j] = s;
+      if (J.deficient) J.deficient[j] = deficient ? 1 : 0;
+      J.order[j] = src | (flip ? kOrderFlip : 0u) | (deficient ? kOrderDef : 0u);
     }
   }
+}
+
+// u / payload / v_out of output columns [32 bx, 32 bx + 32) and rows
+// [32 by, 32 by + 32): a 32 x 32 tile read along W's columns (coalesced), written
+// along the row-major outputs (coalesced) through shared memory. Same arithmetic
+// as the reference: u = flip * (w / s), payload = u * s.
+__global__ void __launch_bounds__(256) finalize_write_kernel(const FinalJob* jobs) {
+  const FinalJob J = jobs[blockIdx.z];
+  __shared__ double tile[32][33];
+  __shared__ uint32_t s_src[32];
+  __shared__ double s_sig[32];
+  const uint32_t j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  if (j0 >= J.k) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+  if (threadIdx.x < 32) {
+    const uint32_t j = j0 + tx;
+    const uint32_t o = j < J.k ? J.order[j] : 0u;
+    s_src[tx] = o;
+    s_sig[tx] = j < J.k ? J.scratch[o & kOrderSrc] : 0.0;
+  }
+  __syncthreads();
+  auto pass = [&](const double* src_base, uint64_t ld, uint32_t nrows, double* out_u, double* out_p, bool is_v) {
+    if (i0 >= nrows) return;
+    for (int c = ty; c < 32; c += 8) {
+      const uint32_t j = j0 + c, i = i0 + tx;
+      double x = 0.0;
+      if (j < J.k && i < nrows) x = src_base[(uint64_t)(s_src[c] & kOrderSrc) * ld + i];
+      tile[c][tx] = x;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const uint32_t i = i0 + r, j = j0 + tx;
+      if (i < nrows && j < J.k) {
+        const uint32_t o = s_src[tx];
+        const double s = s_sig[tx], w = tile[tx][r];
+        const bool def = (o & kOrderDef) != 0u, flip = (o & kOrderFlip) != 0u;
+        if (is_v) {
+          out_u[(uint64_t)i * J.k + j] = flip ? -w : w;
+        } else {
+          const double u = def ? 0.0 : (flip ? -(w / s) : (w / s));
+          if (out_u) out_u[(uint64_t)i * J.k + j] = u;
+          if (out_p) out_p[(uint64_t)i * J.k + j] = def ? (s > 0.0 ? w : 0.0) : u * s;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  if (J.u || J.payload) pass(J.w, J.rows, J.rows, J.u, J.payload, false);
+  if (J.v_out) pass(J.v_in, J.ldv, J.cols, J.v_out, nullptr, true);
 }
 
 // ===========================================================================
@@ -1390,6 +1436,15 @@ void finalize_batched(const std::vector<FinalJob>& jobs, cudaStream_t s) {
   DBuf<FinalJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   finalize_kernel<<<(unsigned)jobs.size(), kFThreads, 0, s>>>(dj.get());
+  RK_LAUNCH_CHECK();
+  uint32_t kmax = 0, rmax = 0;
+  for (const FinalJob& f : jobs) {
+    kmax = std::max(kmax, f.k);
+    rmax = std::max(rmax, f.v_out ? std::max(f.rows, f.cols) : f.rows);
+  }
+  if (kmax == 0 || rmax == 0) return;
+  const dim3 grid((unsigned)ceil_div(kmax, 32), (unsigned)ceil_div(rmax, 32), (unsigned)jobs.size());
+  finalize_write_kernel<<<grid, 256, 0, s>>>(dj.get());
   RK_LAUNCH_CHECK();
 }
 

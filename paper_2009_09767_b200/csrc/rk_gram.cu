@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
   double* Lp = D + kCB * kCB;       // (M) x kCB panel rows below the diagonal block (column-major, ld M)
   __shared__ int s_bad;
   __shared__ double s_dmin, s_dmax;
+  __shared__ double Dinv[kCB];
   double* A = mats[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) { s_bad = 0; s_dmin = INFINITY; s_dmax = 0.0; }
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
             bad = true;
             piv = 1.0;
           }
-          const double ljj = sqrt(piv);
-          const double inv = 1.0 / ljj;
+          const double inv = rsqrt(piv);
+          const double ljj = piv * inv;
           dmin = fmin(dmin, ljj);
           dmax = fmax(dmax, ljj);
           const double l = lane > j ? r[j] * inv : (lane == j ? ljj : 0.0);
@@ -211,6 +212,8 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
     }
     // 2. panel below: L21 = A21 L11^{-T}; row-wise forward substitution (thread per row)
     const uint32_t below = M - k0 - nb;
+    if (tid < kCB) Dinv[tid] = tid < (int)nb ? 1.0 / D[tid + tid * kCB] : 0.0;
+    __syncthreads();
     for (uint32_t rr = tid; rr < below; rr += kCT) {
       const uint32_t i = k0 + nb + rr;
       double x[kCB];
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
         if (j < (int)nb) {
           double v = x[j];
           for (int q = 0; q < j; ++q) v -= x[q] * D[j + q * kCB];
-          x[j] = v / D[j + j * kCB];
+          x[j] = v * Dinv[j];
         }
       }
 #pragma unroll
@@ -237,7 +240,8 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
     const int lr = lane >> 2, lc = lane & 3;
     // a warp owns tile rows ti = warp, warp + 8, ...: its A fragments (L21 rows of
     // the tile row) are loaded once and reused across the row's tiles tj <= ti,
-    // two tiles at a time so their C loads are in flight together
+    // kTB tiles at a time so their C loads (L2 round trips) are in flight together
+    constexpr int kTB = 4;
     for (uint32_t ti = warp; ti < nt; ti += kCT / 32) {
       const uint32_t r = ti * 8 + lr;
       double af[kCB / 4];
@@ -246,12 +250,12 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
         const int q = 4 * kk + lc;
         af[kk] = (r < below && q < (int)nb) ? Lp[r + (uint64_t)q * M] : 0.0;
       }
-      for (uint32_t tj = 0; tj <= ti; tj += 2) {
-        double d0[2], d1[2];
-        double* cp[2];
-        bool ok0[2], ok1[2];
+      for (uint32_t tj = 0; tj <= ti; tj += kTB) {
+        double d0[kTB], d1[kTB];
+        double* cp[kTB];
+        bool ok0[kTB], ok1[kTB];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kTB; ++u) {
           const uint32_t t = tj + u, s0 = t * 8 + 2 * lc;
           cp[u] = A + (k0 + nb + r) + (uint64_t)(k0 + nb + s0) * M;
           const bool live = t <= ti && r < below;
@@ -264,14 +268,14 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
         for (int kk = 0; kk < kCB / 4; ++kk) {
           const int q = 4 * kk + lc;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kTB; ++u) {
             const uint32_t sb = (tj + u) * 8 + lr;
             const double bv = (sb < below && q < (int)nb) ? Lp[sb + (uint64_t)q * M] : 0.0;
             dmma(d0[u], d1[u], af[kk], bv);  // accumulates -C + L L^T
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kTB; ++u) {
           if (ok0[u]) *cp[u] = -d0[u];
           if (ok1[u]) cp[u][M] = -d1[u];
         }

@@ -139,6 +139,11 @@ inline void to_device(T* dst, const T* src, size_t n, cudaStream_t s) {
     RK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
   }
 }
+// RK_HOSTPROF=1: named marks (host wall clock + an event on the stream); prof_flush
+// prints the host and device time of every segment between consecutive marks
+void prof_mark(cudaStream_t s, const char* name);
+void prof_flush();
+
 inline void sync(cudaStream_t s) { RK_CUDA_CHECK(cudaStreamSynchronize(s)); }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
@@ -251,7 +256,17 @@ struct Ctx {
   uint64_t launches = 0;
   cudaEvent_t ev[12] = {};  // [0..3] block stage, [3..7] pipeline stages, [8..11] spare
   PinnedArena arena;        // see to_device
+  // device_free_bytes: cudaMemGetInfo at the first call, then tracked through the
+  // stream-ordered pool's reservation
+  bool free_known = false;
+  size_t free0 = 0;
+  uint64_t reserved0 = 0;
 };
+
+// free device memory for planning. Exact (cudaMemGetInfo, slow) at the first call
+// and whenever the estimate is below `want` bytes; otherwise the first reading
+// adjusted by the pool memory in use since then.
+size_t device_free_bytes(Ctx& c, uint64_t want);
 
 // RAII: activates the context's device and launch counter for one API call
 struct CallScope {

@@ -243,6 +243,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     std::vector<uint32_t> hb;
     to_host(hb, bad.get() + d_lo, nblk, s);
     sync(s);
+    prof_mark(s, "blk nonfinite+sync");
     for (uint64_t i = 0; i < nblk; ++i)
       if (hb[i] && !skip[i]) {
         out.failures[i] = "block_svd: block has non-finite values";
@@ -286,6 +287,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
     jacobi_batched(jj, s, c.num_sms, c.smem_optin);
     RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
+    prof_mark(s, "blk jacobi");
     std::vector<FinalJob> fj(nb);
     for (size_t q = 0; q < nb; ++q) {
       const uint64_t i = blocks[q];
@@ -308,6 +310,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     finalize_batched(fj, s);
     if (sigma_all) to_host(sigma_host, sigma_all, (uint64_t)nb * cols_pad_full, s);  // read with the stats
     std::vector<JacobiStats> js = read_stats(stats.get(), nb, s);  // synchronizes
+    prof_mark(s, "blk finalize+stats");
     float ms_j = 0;
     cudaEventElapsedTime(&ms_j, c.ev[9], c.ev[10]);
     out.jacobi_ms += ms_j;
@@ -326,9 +329,11 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     return js;
   };
 
-  size_t free_b = 0, total_b = 0;
-  RK_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-  const uint64_t budget = std::max<uint64_t>((uint64_t)(free_b * 0.4), 256ull << 20);
+  // 40 % of the free device memory; the estimate avoids cudaMemGetInfo (2-3 ms per
+  // call on the B200 box) unless the whole stage may not fit in it
+  const uint64_t need_all = nblk * (uint64_t)M * cols_pad_full * 8 * 2;
+  const uint64_t budget = std::max<uint64_t>((uint64_t)(device_free_bytes(c, need_all * 3) * 0.4), 256ull << 20);
+  prof_mark(s, "blk budget");
 
   // ---- route 1: W = chol(A_d A_d^T), accepted when kappa <= kappa_max(M) ----
   if (gram_route_enabled() && M <= cholesky_max_rows()) {
@@ -354,6 +359,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       to_host(hst, status.get(), nb, s);
       to_host(hrat, ratio.get(), nb, s);
       sync(s);
+      prof_mark(s, "blk gram+chol+sync");
       float ms_g = 0;
       cudaEventElapsedTime(&ms_g, c.ev[8], c.ev[11]);
       out.qr_ms += ms_g;
@@ -647,6 +653,7 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   jj[0].w = W.get(); jj[0].v = nullptr; jj[0].rows = M; jj[0].cols = cols; jj[0].cols_pad = cp;
   jj[0].alpha = alpha.get(); jj[0].stats = stats.get(); jj[0].gram_ok = gram_ok ? 1u : 0u;
   jacobi_batched(jj, s, c.num_sms, c.smem_optin, /*latency=*/true);
+  prof_mark(s, "mrg jacobi");
   // finalize right behind the Jacobi (its result is discarded if the Jacobi
   // failed), then one readback of the statistics, the sorted sigma and the
   // deficiency flags: one host round trip instead of three
@@ -667,6 +674,7 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   to_host(hs, sig_all.get(), cols, s);
   to_host(hdef, def.get(), k, s);
   sync(s);
+  prof_mark(s, "mrg finalize+sync");
   out.sweeps = hst[0];
   out.rotations = hst[1];
   if (hst[2] != 0) {
@@ -720,7 +728,9 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
       const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
       DBuf<double> W((uint64_t)M * cp, s);
       W.zero();
+      prof_mark(s, "mrg alloc");
       records_gram(payload, offset, kept, M, W.get(), s);
+      prof_mark(s, "mrg syrk");
       double* ptr = W.get();
       DBuf<double*> dptr(1, s);
       DBuf<uint32_t> status(1, s);
@@ -732,6 +742,7 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
       RK_CUDA_CHECK(cudaMemcpyAsync(&hst, status.get(), sizeof hst, cudaMemcpyDeviceToHost, s));
       RK_CUDA_CHECK(cudaMemcpyAsync(&hr, ratio.get(), sizeof hr, cudaMemcpyDeviceToHost, s));
       sync(s);
+      prof_mark(s, "mrg chol+sync");
       const double kmax = kappa_max(M);
       if (hst == 0 && hr <= kmax) {
         MergeOut tmp;
