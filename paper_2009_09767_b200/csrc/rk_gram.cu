@@ -295,6 +295,202 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
   }
 }
 
+// the nb x nb diagonal block at P (column-major, ld ldp) factored in place by one
+// warp: lane i holds row i in registers. FP64 latency sets the speed here (DFMA
+// 23 cycles, rsqrt 78, a double shuffle 49 on the B200 -- tools/probe_latency.cu),
+// so the critical path goes through the pivot lane's own registers: after column
+// j, lane j+1 updates its diagonal entry and takes its rsqrt before the other
+// rank-1 updates, and only the reciprocal pivot is broadcast (32x32: 11.9k cycles
+// vs 26k for the textbook order). Dinv[j] = 1 / L_jj.
+template <int kCB, bool FULL>
+__device__ __forceinline__ void factor_diag(double* P, uint32_t ldp, uint32_t nb_rt, int lane, double* Dinv,
+                                            int* s_bad, double* s_dmin, double* s_dmax) {
+  const uint32_t nb = FULL ? (uint32_t)kCB : nb_rt;  // FULL: no per-column guards
+  double rg[kCB];
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) rg[c] = (lane < (int)nb && c < (int)nb) ? P[lane + c * ldp] : 0.0;
+  bool bad = false;
+  double dmin = INFINITY, dmax = 0.0;
+  // lane j's candidate pivot and its reciprocal square root
+  auto pivot = [&](double d, double& inv) {
+    const bool ok = d > 0.0;
+    inv = rsqrt(ok ? d : 1.0);
+    return ok;
+  };
+  double inv_mine;
+  bool ok_mine = pivot(rg[0], inv_mine);
+#pragma unroll
+  for (int j = 0; j < kCB; ++j) {
+    if (j < (int)nb) {
+      const double inv = __shfl_sync(0xffffffffu, inv_mine, j);
+      const double l = lane >= j ? rg[j] * inv : 0.0;
+      const bool me = lane == j;
+      bad = bad || (me && !ok_mine);
+      dmin = me ? fmin(dmin, l) : dmin;
+      dmax = me ? fmax(dmax, l) : dmax;
+      if (me) Dinv[j] = inv;
+      rg[j] = l;
+      if (j + 1 < kCB) {
+        ok_mine = pivot(rg[j + 1] - l * l, inv_mine);  // valid in lane j + 1
+#pragma unroll
+        for (int c = j + 1; c < kCB; ++c) {
+          const double lcj = __shfl_sync(0xffffffffu, l, c);
+          if (lane >= c) rg[c] -= l * lcj;
+        }
+      }
+    }
+  }
+  if (lane < (int)nb) {
+#pragma unroll
+    for (int c = 0; c < kCB; ++c)
+      if (c < (int)nb) P[lane + c * ldp] = lane >= c ? rg[c] : 0.0;
+  }
+  for (int o = 16; o; o >>= 1) {
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    if (bad) *s_bad = 1;
+    *s_dmin = fmin(*s_dmin, dmin);
+    *s_dmax = fmax(*s_dmax, dmax);
+  }
+  __syncwarp();
+}
+
+// Left-looking variant: panel by panel (kCB columns), the update of the panel by
+// the finished columns, P -= L[k0:, :k0] L[k0:k0+kCB, :k0]^T, runs as a DMMA GEMM
+// over K chunks of kCB columns staged in shared memory with coalesced loads (one
+// L2 round trip per chunk for the whole CTA), the accumulators in registers (warp
+// w owns tile rows w, w + 8, ...; at most NP of them). Then the panel is loaded
+// into the same buffer, the accumulators subtracted, the diagonal block factored
+// in registers (factor_diag), the rows below solved against it and the panel
+// written back once (zeros above the diagonal). No read-modify-write passes over
+// the trailing matrix. Same status / ratio outputs as cholesky_kernel.
+template <int kCB>
+__host__ __device__ constexpr uint32_t ll_ld(uint32_t rows) {
+  // >= rows, == 4 (mod 16): the DMMA fragment reads (lr + lc ld) hit distinct banks
+  return ((rows + 11) / 16) * 16 + 4;
+}
+
+template <int kCB, int NP>
+__global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __restrict__ mats, uint32_t M,
+                                                             uint32_t* __restrict__ status,
+                                                             double* __restrict__ diag_ratio) {
+  extern __shared__ __align__(16) double sm[];
+  double* S = sm;  // rows_p x kCB, column-major, ld ll_ld(rows_p)
+  __shared__ int s_bad;
+  __shared__ double s_dmin, s_dmax;
+  __shared__ double Dinv[kCB];
+  double* A = mats[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  constexpr int kW = kCT / 32;
+  if (tid == 0) { s_bad = 0; s_dmin = INFINITY; s_dmax = 0.0; }
+  for (uint32_t k0 = 0; k0 < M; k0 += kCB) {
+    const uint32_t nb = min((uint32_t)kCB, M - k0), rows_p = M - k0;
+    const uint32_t ld = ll_ld<kCB>(rows_p);
+    const uint32_t TR = (rows_p + 7) / 8;
+    double acc[NP][kCB / 8][2];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+      for (int u = 0; u < kCB / 8; ++u) acc[pp][u][0] = acc[pp][u][1] = 0.0;
+    // GEMM over the finished columns, kCB at a time
+    for (uint32_t kc = 0; kc < k0; kc += kCB) {
+      __syncthreads();  // previous users of S are done
+      // (2-D loops: a runtime t / rows_p, t % rows_p per element was most of the
+      // kernel's instructions)
+#pragma unroll 8
+      for (int c = 0; c < kCB; ++c) {
+        const double* src = A + k0 + (uint64_t)(kc + c) * M;
+        for (uint32_t i = tid; i < rows_p; i += kCT) S[i + c * ld] = src[i];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const uint32_t tr = warp + kW * pp;
+        if (tr < TR) {
+          const uint32_t ia = tr * 8 + lr;
+#pragma unroll
+          for (int kk = 0; kk < kCB; kk += 4) {
+            const uint32_t q = kk + lc;
+            const double av = ia < rows_p ? S[ia + q * ld] : 0.0;
+#pragma unroll
+            for (int u = 0; u < kCB / 8; ++u) {
+              const uint32_t ib = u * 8 + lr;
+              const double bv = ib < nb ? S[ib + q * ld] : 0.0;
+              dmma(acc[pp][u][0], acc[pp][u][1], av, bv);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // the panel minus the update
+#pragma unroll 8
+    for (int c = 0; c < kCB; ++c) {
+      if (c >= (int)nb) break;
+      const double* src = A + k0 + (uint64_t)(k0 + c) * M;
+      for (uint32_t i = tid; i < rows_p; i += kCT) S[i + c * ld] = src[i];
+    }
+    __syncthreads();
+    if (k0 > 0) {
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) {
+        const uint32_t tr = warp + kW * pp;
+        const uint32_t i = tr * 8 + lr;
+        if (tr < TR && i < rows_p) {
+#pragma unroll
+          for (int u = 0; u < kCB / 8; ++u) {
+            const uint32_t j = u * 8 + 2 * lc;
+            if (j < nb) S[i + j * ld] -= acc[pp][u][0];
+            if (j + 1 < nb) S[i + (j + 1) * ld] -= acc[pp][u][1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      if (nb == kCB) factor_diag<kCB, true>(S, ld, nb, lane, Dinv, &s_bad, &s_dmin, &s_dmax);
+      else factor_diag<kCB, false>(S, ld, nb, lane, Dinv, &s_bad, &s_dmin, &s_dmax);
+    }
+    __syncthreads();
+    if (s_bad) break;
+    // rows below: x = p L11^{-T} (forward substitution, thread per row)
+    for (uint32_t i = nb + tid; i < rows_p; i += kCT) {
+      double x[kCB];
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) x[j] = j < (int)nb ? S[i + j * ld] : 0.0;
+      // right-looking: x_j is final after the scaling, its updates of x_c (c > j)
+      // are independent of each other (a 2-op chain per column, not j ops)
+#pragma unroll
+      for (int j = 0; j < kCB; ++j) {
+        if (j < (int)nb) {
+          x[j] *= Dinv[j];
+#pragma unroll
+          for (int c = j + 1; c < kCB; ++c) x[c] -= x[j] * S[c + j * ld];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCB; ++j)
+        if (j < (int)nb) S[i + j * ld] = x[j];
+    }
+    __syncthreads();
+    // write the finished columns (zeros above the diagonal)
+#pragma unroll 8
+    for (int j = 0; j < kCB; ++j) {
+      if (j >= (int)nb) break;
+      double* dst = A + (uint64_t)(k0 + j) * M;
+      for (uint32_t i = tid; i < M; i += kCT) dst[i] = i < k0 ? 0.0 : S[(i - k0) + j * ld];
+    }
+  }
+  if (tid == 0) {
+    status[blockIdx.x] = s_bad ? 1u : 0u;
+    diag_ratio[blockIdx.x] = s_bad ? INFINITY : s_dmax / s_dmin;
+  }
+}
+
 unsigned grid_for(uint64_t n, unsigned cap = 1u << 20) {
   uint64_t g = ceil_div(n, 256);
   if (g == 0) g = 1;
@@ -351,8 +547,28 @@ void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32
     kern<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
     RK_LAUNCH_CHECK();
   };
-  if (M <= 640) launch(cholesky_kernel<32>, 32);
-  else launch(cholesky_kernel<16>, 16);
+  const char* ce = std::getenv("RK_CHOL");
+  const bool ll = !(ce && ce[0] == 'r');  // RK_CHOL=r: the right-looking kernel (A/B)
+  auto launch_ll = [&](auto kern, int cb) {
+    const size_t smem = (size_t)ll_ld<16>(M) * cb * sizeof(double);
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
+    RK_LAUNCH_CHECK();
+  };
+  // NP = tile rows per warp = ceil(M / 64)
+  if (ll && M <= 256) {
+    launch_ll(cholesky_ll_kernel<32, 4>, 32);
+  } else if (ll && M <= 512) {
+    launch_ll(cholesky_ll_kernel<32, 8>, 32);
+  } else if (ll && M <= 1024) {
+    launch_ll(cholesky_ll_kernel<16, 16>, 16);
+  } else if (ll && M <= 1280) {
+    launch_ll(cholesky_ll_kernel<16, 20>, 16);
+  } else if (M <= 640) {
+    launch(cholesky_kernel<32>, 32);
+  } else {
+    launch(cholesky_kernel<16>, 16);
+  }
 }
 
 uint32_t cholesky_max_rows() { return 1280; }  // the panel buffer (M x 16 doubles) must fit shared memory
