@@ -80,14 +80,21 @@ __device__ __forceinline__ uint32_t rr_slot(uint32_t pos, uint32_t step, uint32_
 }
 
 // Rotation (c, s) for a pair with norms^2 ap, aq and inner product gamma, the
-// reference's zeta/t formulas (svd.cpp:238-242) evaluated cheaply:
+// reference's angle (svd.cpp:238-242: tan(theta) = t = sign(zeta) / (|zeta| +
+// sqrt(1 + zeta^2)), zeta = (aq - ap) / (2 gamma), the root with |theta| <= pi/4),
+// evaluated for latency -- this is on every round's dependent chain, and on the
+// B200 an FP64 op costs 23 cycles, rsqrt 78, a conversion ~26:
 //   * d = aq - ap and e = 2 gamma are scaled by an exact power of two so that
-//     max(|d|, |e|) is in [1, 2), then t = sign(zeta)|e| / (|d| + sqrt(d^2+e^2))
-//     is computed in FP32 (MUFU) -- the angle only steers convergence;
-//   * (c, s) = (1, t)/sqrt(1+t^2) is rounded to FP64 and renormalized with two
-//     Newton steps for 1/sqrt(c^2+s^2), so the applied rotation is orthogonal to
-//     FP64 precision whatever the angle's accuracy. The convergence test itself
-//     uses the FP64 gamma, so the stopping rule is the reference's.
+//     max(|d|, |e|) is in [1, 2), then rounded to FP32;
+//   * with cos(2 theta) = |d| / r, sin(2 theta) = |e| / r (r = |(d, e)|):
+//     c = sqrt((1 + cos 2theta) / 2), s = sign(d e) sin(2 theta) / (2 c), two
+//     MUFU rsqrts and a few FP32 multiplies (the angle only steers convergence);
+//   * (c, s) is rounded to FP64 and renormalized: with delta = c^2 + s^2 - 1
+//     (~1e-7, formed with FMAs), 1 / sqrt(1 + delta) = 1 - delta/2 + 3 delta^2/8
+//     + O(delta^3), so the applied rotation is orthogonal to FP64 rounding.
+// The rotation decision itself uses the FP64 gamma, so the stopping rule is the
+// reference's. (The previous form -- t in FP32, then two Newton steps for
+// 1/sqrt(c^2 + s^2) in FP64 -- had a ~480-cycle chain; this one ~300.)
 __device__ __forceinline__ void rotation_cs(double ap, double aq, double gamma, double& c, double& s) {
   const double d = aq - ap, e = 2.0 * gamma;
   const double m = fmax(fabs(d), fabs(e));
@@ -95,16 +102,15 @@ __device__ __forceinline__ void rotation_cs(double ap, double aq, double gamma, 
   const int ex = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;
   const double f = __hiloint2double((1023 - ex) << 20, 0);
   const float df = (float)(d * f), ef = (float)(e * f);
-  const float r = sqrtf(fmaf(df, df, ef * ef));
+  const float rr = rsqrtf(fmaf(df, df, ef * ef));    // 1 / r
+  const float x = fmaf(0.5f * fabsf(df), rr, 0.5f);  // (1 + cos 2theta) / 2, in [1/2, 1]
+  const float rx = rsqrtf(x);                        // 1 / c
   const float sgn = (df == 0.0f || ((df > 0.0f) == (ef > 0.0f))) ? 1.0f : -1.0f;
-  const float t = sgn * __fdividef(fabsf(ef), fabsf(df) + r);  // |df| + r >= 1: no range issue
-  const float c32 = rsqrtf(fmaf(t, t, 1.0f));
-  double cc = (double)c32, ss = (double)(c32 * t);
-  const double n = cc * cc + ss * ss;
-  double r1 = 1.5 - 0.5 * n;
-  r1 = r1 * (1.5 - 0.5 * n * r1 * r1);
-  c = cc * r1;
-  s = ss * r1;
+  const double cc = (double)(x * rx), ss = (double)(sgn * 0.5f * fabsf(ef) * rr * rx);
+  const double dl = fma(cc, cc, fma(ss, ss, -1.0));
+  const double r = fma(dl, fma(dl, 0.375, -0.5), 1.0);
+  c = cc * r;
+  s = ss * r;
 }
 
 // Rotate one pair (p, q) of staged columns with a group of Q lanes (Q | 32);
@@ -574,6 +580,28 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
       for (uint32_t pi = rank; pi < G / 2; pi += csize) {
         const uint32_t gA = rr_slot(pi, step, G), gB = rr_slot(G - 1 - pi, step, G);
         // stage the two groups: slots 0..g-1 = group A, g..2g-1 = group B
+        if constexpr (EXACT && GT > 0) {
+          // compile-time shape: every load of the step is issued before the first
+          // store (one L2 round trip per step instead of one per column chunk)
+          constexpr uint32_t kR = (uint32_t)(Q * E), kC = 2 * GT / kJWarps, kI = kR / 32;
+          double v[kC * kI];
+#pragma unroll
+          for (uint32_t cc = 0; cc < kC; ++cc) {
+            const uint32_t c = warp + cc * kJWarps;
+            const uint32_t col = (c < GT ? gA * GT + c : gB * GT + (c - GT));
+            const double* src = W + (uint64_t)col * kR + lane;
+#pragma unroll
+            for (uint32_t i = 0; i < kI; ++i) v[cc * kI + i] = __ldcg(src + 32 * i);
+          }
+#pragma unroll
+          for (uint32_t cc = 0; cc < kC; ++cc) {
+            const uint32_t c = warp + cc * kJWarps;
+            double* dst = sW + (uint64_t)c * (kR + 8) + lane;
+#pragma unroll
+            for (uint32_t i = 0; i < kI; ++i) dst[32 * i] = v[cc * kI + i];
+            if (lane == 0) sAlpha[c] = __ldcg(alpha_g + (c < GT ? gA * GT + c : gB * GT + (c - GT)));
+          }
+        } else
         for (uint32_t c = warp; c < 2 * g; c += kJWarps) {
           const uint32_t col = (c < g ? gA * g + c : gB * g + (c - g));
           const double* src = W + (uint64_t)col * rows;
@@ -1394,6 +1422,13 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   if (E < 4) E = 4;
   if (E > 32 || with_v) E = 0;  // a[E] + b[E] must stay in registers
   const bool exact = E > 0 && (int)rows == Q * E;
+  // well-conditioned square jobs: FP32 sweeps + an orthogonal FP64 right factor
+  // first (rk_precond.cu); the FP64 kernel below then finishes and certifies
+  if (!use_warp && !with_v) {
+    bool all = true;
+    for (const JacobiJob& j : jobs) all = all && precondition_eligible(j);
+    if (all) precondition_fp32(jobs, s, sms, smem_optin, g, G, Q);
+  }
   auto launch = [&](auto kern) {
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

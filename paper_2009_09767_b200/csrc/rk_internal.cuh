@@ -346,6 +346,11 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
 // rounding) must not depend on how many blocks share the launch, so that the
 // sharded path is bitwise identical for every rank count.
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency = false);
+// rk_precond.cu: FP32 Jacobi sweeps, then W <- W V with V the (Newton-Schulz
+// orthogonalized) right singular vectors they give -- for gram_ok square jobs
+bool precondition_eligible(const JacobiJob& j);
+void precondition_fp32(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, uint32_t g,
+                       uint32_t G, int Q);
 // RNKY records (rk_records.cu)
 uint32_t crc32_host(const void* data, uint64_t size);
 void crc32_device(const unsigned char* d_base, const std::vector<uint64_t>& off, const std::vector<uint64_t>& len,
