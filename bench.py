@@ -19,6 +19,7 @@ threads) on the same workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -55,8 +56,26 @@ def dist_env():
     return ws, rank, local
 
 
+def weak_matrix(base, ws, R):
+    """The weak-scaling workload for ws GPUs: the config's matrix tiled ws times
+    along the columns ([A A ... A], ws x the blocks), so every GPU's share of
+    column blocks is exactly the single-GPU workload."""
+    import numpy as np
+    a = base.generate()
+    e = a.entries()
+    t = np.concatenate([e] * ws)
+    n = len(e)
+    for k in range(1, ws):
+        t["col"][k * n:(k + 1) * n] += k * base.cols
+    t = t[np.lexsort((t["col"], t["row"]))]
+    return R.SparseMatrix._trusted(base.rows, base.cols * ws, t)
+
+
 def config_dict(cfg, n_gpus, extra=None):
-    d = {"workload": cfg.name, "rows": cfg.rows, "cols": cfg.cols, "blocks": cfg.blocks, "method": cfg.method,
+    d = {"workload": cfg.name if n_gpus == 1 else f"{cfg.name} tiled x{n_gpus} along the columns (one {cfg.name} "
+                                                   f"per GPU: {cfg.blocks // n_gpus} blocks, {cfg.cols // n_gpus} "
+                                                   f"columns)",
+         "rows": cfg.rows, "cols": cfg.cols, "blocks": cfg.blocks, "method": cfg.method,
          "keep": cfg.keep, "top_k": cfg.top_k, "seed": cfg.seed, "description": cfg.description,
          "parallelism": f"block-shard x{n_gpus}" if n_gpus > 1 else "single GPU",
          "l2": "flushed between steps (256 MiB write)"}
@@ -223,12 +242,15 @@ def reference_arm(args, cfg):
     ms = 1e3 * sum(times) / len(times)
     value = a.nnz() / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": config_dict(cfg, 1, {"nnz": a.nnz()}),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_dict(dataclasses.replace(cfg, cols=cfg.cols * ws, blocks=cfg.blocks * ws) if ws > 1
+                                  else cfg, ws, {"nnz": a.nnz()}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"full {cfg.name} per step (run_pipeline workers={cores} + "
-                                       f"recover_right_vectors), {args.steps} steps"},
+                                       f"recover_right_vectors), {args.steps} steps" +
+                                       (f"; for {ws} GPUs (weak scaling) one GPU's {cfg.name}-sized share is the "
+                                        f"sample" if ws > 1 else "")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -270,6 +292,11 @@ def main():
     from paper_2009_09767_b200 import ranky as R
 
     ws, rank, local = dist_env()
+    if ws > 1:
+        # weak scaling: every GPU gets the single-GPU workload as its share -- the
+        # matrix is [A A ... A] with ws x the columns and blocks (weak_matrix), the
+        # paper's one-level distribution of column blocks over machines
+        cfg = dataclasses.replace(cfg, cols=cfg.cols * ws, blocks=cfg.blocks * ws)
     if args.backend == "gloo":
         local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
@@ -285,7 +312,7 @@ def main():
 
     # FP64 peak first, before the library's stream-ordered pool holds the big buffers
     fp64 = fp64_peak_tflops(torch) if rank == 0 else 0.0
-    a = cfg.generate()
+    a = weak_matrix(configs.CONFIGS[args.config], ws, R) if ws > 1 else cfg.generate()
     dm = rk.DeviceMatrix(a, ctx)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     L = R.lib()
@@ -391,14 +418,14 @@ def main():
     stages = {k: med[k] for k in ("repair_ms", "blocks_ms", "qr_ms", "jacobi_ms", "merge_ms", "recover_ms",
                                   "total_ms")}
     stages["jacobi_sweeps_max"] = med["jacobi_sweeps_max"]
-    v_bytes = 8.0 * cfg.cols * M
+    v_bytes = 8.0 * (cfg.cols // ws) * M  # this rank's V rows
     stages["recover_hbm_frac"] = (v_bytes / (med["recover_ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"] \
         if med["recover_ms"] > 0 else None
     # every stage against its own roof: HBM for the rank check +
     # repair and the V SpMM (algorithmic bytes), FP64 for the factorizations
     nnz = a.nnz()
     repair_bytes = 12.0 * nnz + 8.0 * (M + 1) + 4.0 * M * cfg.blocks  # CSR col+val, row_ptr, presence flags
-    spmm_bytes = v_bytes + 12.0 * nnz + 8.0 * (cfg.cols + 1) + 8.0 * M * M
+    spmm_bytes = v_bytes + 12.0 * nnz / ws + 8.0 * (cfg.cols // ws + 1) + 8.0 * M * M
     hbm = peaks["hbm_gbs"]
 
     def frac(x, ms, peak, scale):
@@ -492,7 +519,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak" if ws > 1 else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, csrc/gen.c)",
                 "config": config_dict(cfg, ws, {"nnz": a.nnz()}), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages_ms_median": stages,
