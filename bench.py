@@ -203,7 +203,7 @@ def profiled_traffic(dominant):
     committed `ncu --set full` summary (profiles/*_kernels.json, written by
     profiles/summarize.py); None when there is none."""
     import glob
-    names = {"block_jacobi": "jacobi_cluster_kernel<16, 16, 1>", "block_qr": "qr_kernel"}
+    names = {"block_jacobi": "jacobi_cluster_kernel<16, 16, 1", "block_qr": "qr_kernel"}
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
     for f in reversed(files):
         try:

@@ -10,6 +10,6 @@ python bench.py --steps 10 --warmup 3 > gpurun_out/${tag}_bench.jsonl 2> gpurun_
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_launches.log 2>&1 || exit 2
 ncu --set full --clock-control none --import-source on \
-    -k regex:'jacobi|qr_kernel|spmm|sparse_gram|cholesky|syrk_records|neighbor|presence|random_fill|single_sums|multi_counts' \
+    -k regex:'jacobi|qr_kernel|spmm|sparse_gram|cholesky|syrk_records|neighbor|presence|random_fill|single_sums|multi_counts|finalize' \
     --launch-count 16 -f -o gpurun_out/${tag}_full \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_full.log 2>&1 || exit 3
