@@ -341,24 +341,40 @@ def main():
         roots = torch.empty((ws, M, M), dtype=torch.float64, device="cuda")
         mine = torch.empty((M, M), dtype=torch.float64, device="cuda")
 
-        def sharded(dmx, sink=None):
-            """this rank's share: factor its leaves, all-gather the subtree factors
-            (NCCL), finish the tree top, V for its columns; `sink(out)` sees the outputs"""
-            shard = C.c_void_p()
-            t = R.Timing()
-            R._check(L.rk_dev_shard_factor(ctx.handle, dmx.handle, cfg.blocks, R._method(cfg.method), cfg.keep,
-                                           cfg.seed, lo, hi, C.c_void_p(mine.data_ptr()), C.byref(shard),
-                                           C.byref(t)))
+        def gather():
             if args.backend == "nccl":
                 torch.distributed.all_gather_into_tensor(roots, mine)
             else:
                 parts = [torch.empty((M, M), dtype=torch.float64) for _ in range(ws)]
                 torch.distributed.all_gather(parts, mine.cpu())
                 roots.copy_(torch.stack(parts))
+
+        def sharded(dmx, sink=None):
+            """this rank's share: factor its leaves, all-gather the subtree's Gram
+            partial (NCCL), finish the merge, V for its columns; the TSQR factors
+            instead when the Gram route is rejected (identically on every rank);
+            `sink(out)` sees the outputs"""
+            shard = C.c_void_p()
+            t = R.Timing()
+            fargs = (ctx.handle, dmx.handle, cfg.blocks, R._method(cfg.method), cfg.keep, cfg.seed, lo, hi,
+                     C.c_void_p(mine.data_ptr()), C.byref(shard), C.byref(t))
+            st = L.rk_dev_shard_factor_gram(*fargs)
+            gram = st == 0
+            if st == R.GRAM_REJECTED:
+                R._check(L.rk_dev_shard_factor(*fargs))
+            else:
+                R._check(st)
+            gather()
             out = C.POINTER(R.DevOutputs)()
             t2 = R.Timing()
-            R._check(L.rk_dev_shard_finish(ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V,
-                                           cfg.top_k, c_lo, c_hi, C.byref(out), C.byref(t2)))
+            gargs = (ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V, cfg.top_k, c_lo, c_hi,
+                     C.byref(out), C.byref(t2))
+            st = L.rk_dev_shard_finish_gram(*gargs) if gram else L.rk_dev_shard_finish(*gargs)
+            if gram and st == R.GRAM_REJECTED:
+                R._check(L.rk_dev_shard_tsqr(ctx.handle, shard, C.c_void_p(mine.data_ptr())))
+                gather()
+                st = L.rk_dev_shard_finish(*gargs)
+            R._check(st)
             if sink:
                 sink(out)
             R.dev_outputs_free(out)

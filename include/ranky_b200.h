@@ -56,7 +56,8 @@ typedef enum rk_status {
   RK_RUNTIME = 4,          /* std::runtime_error ("block task d failed: ...") */
   RK_CUDA = 5,             /* CUDA runtime failure or no usable device */
   RK_NOMEM = 6,            /* device or host allocation failed */
-  RK_RECORD = 7            /* ranky::RecordError: damaged or truncated block record file */
+  RK_RECORD = 7,           /* ranky::RecordError: damaged or truncated block record file */
+  RK_GRAM_REJECTED = 8     /* sharded Gram route not applicable: take the TSQR path (rk_dev_shard_tsqr) */
 } rk_status;
 
 /* RepairMethod -- proj/include/ranky/repair.hpp:15-20 (same numbering) */
@@ -247,9 +248,10 @@ RK_API rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_d
  * whole matrix (the replay is deterministic, so every rank holds the same repaired
  * matrix without communication), factors the blocks of leaves [leaf_lo, leaf_hi)
  * and reduces their records to the R factor of that subtree of the fixed merge tree
- * (rk_merge_tree_leaves). The caller all-gathers the G factors (NCCL) and every rank
- * finishes the same top of the tree, then recovers V for its own columns. With
- * (leaves / G) a power of two the results are bitwise identical for every G. */
+ * (rk_merge_tree_leaves) -- or, on the Gram route below, to the subtree's Gram. The
+ * caller all-gathers the G factors (NCCL) and every rank finishes the same top of
+ * the tree, then recovers V for its own columns. With (leaves / G) a power of two
+ * the results are bitwise identical for every G. */
 RK_API uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count, uint64_t keep);
 typedef struct rk_dev_shard rk_dev_shard;
 /* d_root_out: device, rows*rows doubles, column-major upper-triangular R */
@@ -261,6 +263,26 @@ RK_API rk_status rk_dev_shard_finish(rk_ctx* ctx, rk_dev_shard* shard, const dou
                               uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi,
                               rk_dev_outputs** out, rk_timing* timing);
 RK_API rk_status rk_dev_shard_destroy(rk_dev_shard* shard);
+/* Gram route of the sharded merge (the single-GPU merge's route, merge_records):
+ * rk_dev_shard_factor_gram does the same repair and block stage and writes
+ * d_gram_out = the Gram (rows x rows, column-major, full) of the shard's stacked
+ * records -- each leaf's records, then the leaves by the fixed pairwise tree, so an
+ * aligned power-of-two run of leaves is a node of the whole matrix's tree; it
+ * returns RK_GRAM_REJECTED without a shard when the route does not apply (rows >
+ * 1280 or not a multiple of 8, RK_BLOCK_ROUTE=householder). The caller all-gathers
+ * the G partials; rk_dev_shard_finish_gram finishes the pairwise tree, Cholesky, the
+ * kappa guard and the Jacobi, then V for [col_lo, col_hi). When the guard rejects
+ * (RK_GRAM_REJECTED, identically on every rank) each rank calls rk_dev_shard_tsqr
+ * for its subtree's R factor, the caller all-gathers those and rk_dev_shard_finish
+ * completes as on the TSQR path. One 512 KiB all-gather per rank at c2 either way. */
+RK_API rk_status rk_dev_shard_factor_gram(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count,
+                                          rk_method method, uint64_t keep, uint64_t seed, uint64_t leaf_lo,
+                                          uint64_t leaf_hi, double* d_gram_out, rk_dev_shard** shard_out,
+                                          rk_timing* timing);
+RK_API rk_status rk_dev_shard_finish_gram(rk_ctx* ctx, rk_dev_shard* shard, const double* d_grams, uint64_t n_roots,
+                                          uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi,
+                                          rk_dev_outputs** out, rk_timing* timing);
+RK_API rk_status rk_dev_shard_tsqr(rk_ctx* ctx, rk_dev_shard* shard, double* d_root_out);
 
 /* ---- RNKY block records (proj/src/block_record.cpp:51-144) ----------------------
  * Files byte-identical to ranky::write_block_record: "RNKY", version u16 = 1,

@@ -148,6 +148,11 @@ struct rk_dev_shard {
   uint64_t seed;
   std::unique_ptr<DevMatrix> repaired;  // null: the input itself (no edges)
   const DevMatrix* rep() const { return repaired ? repaired.get() : &a->m; }
+  // rk_dev_shard_factor_gram keeps the shard's block records for the TSQR
+  // fallback (rk_dev_shard_tsqr)
+  BlockStageResult blocks;
+  std::vector<TreeLeaf> local;  // the shard's leaves, block indices relative to its first block
+  bool has_records = false;
 };
 
 namespace {
@@ -907,64 +912,192 @@ uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count
   }
 }
 
+}  // extern "C"
+
+namespace {
+
+// the shard's part of a sharded run: repair (whole matrix, redundantly), block
+// stage of the leaves [leaf_lo, leaf_hi), then either the TSQR subtree factor
+// (gram = false) or the Gram partial of the subtree (gram = true, records kept)
+void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method, uint64_t keep,
+                  uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi, double* d_out, rk_dev_shard** shard_out,
+                  rk_timing* timing, bool gram) {
+  check_ctx(ctx);
+  if (!a || !shard_out || !d_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+  CallScope sc(&ctx->c);
+  Ctx& c = ctx->c;
+  cudaStream_t s = c.stream;
+  const uint64_t launches0 = c.launches;
+  const uint32_t M = (uint32_t)a->m.csr.rows;
+  if (gram && !gram_merge_eligible(M))
+    fail(RK_GRAM_REJECTED, "the merge's Gram route does not apply to " + std::to_string(M) + " rows");
+  auto sh = std::make_unique<rk_dev_shard>();
+  sh->owner = ctx;
+  sh->a = a;
+  sh->p = make_partition(a->m.csr.cols, block_count);
+  sh->method = method;
+  sh->seed = seed;
+  // the tree's leaves from the per-block kept counts
+  std::vector<uint32_t> kept(block_count);
+  for (uint64_t d = 0; d < block_count; ++d) {
+    const uint64_t w = sh->p.end(d) - sh->p.begin(d), k_full = std::min<uint64_t>(M, w);
+    kept[d] = (uint32_t)(keep == 0 ? k_full : std::min(keep, k_full));
+  }
+  std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
+  if (leaf_lo >= leaf_hi || leaf_hi > leaves.size()) fail(RK_OUT_OF_RANGE, "leaf range outside the merge tree");
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
+  RepairOut rep;
+  sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, rep);
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
+  const uint64_t d_lo = leaves[leaf_lo].r0, d_hi = leaves[leaf_hi - 1].r1;
+  BlockStageResult& br = sh->blocks;
+  block_stage(c, *sh->rep(), sh->p, d_lo, d_hi, keep, br, nullptr);
+  if (any_failure(br)) throw_block_failure(br, d_lo);
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
+  // leaves re-indexed to the shard's records
+  sh->local.assign(leaves.begin() + leaf_lo, leaves.begin() + leaf_hi);
+  for (TreeLeaf& L : sh->local) { L.r0 -= (uint32_t)d_lo; L.r1 -= (uint32_t)d_lo; }
+  if (gram) {
+    std::vector<std::pair<uint32_t, uint32_t>> lr;
+    for (const TreeLeaf& L : sh->local) lr.push_back({L.r0, L.r1});
+    leaf_gram_tree(br.payload.get(), br.offset, br.kept, M, lr, d_out, s);
+    sh->has_records = true;
+  } else {
+    DBuf<double> R;
+    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, sh->local, 0, sh->local.size(), R);
+    RK_CUDA_CHECK(cudaMemcpyAsync(d_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice, s));
+    br.payload.release();
+  }
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[6], s));
+  sync(s);
+  if (timing) {
+    std::memset(timing, 0, sizeof *timing);
+    timing->repair_ms = elapsed(c.ev[3], c.ev[4]);
+    timing->blocks_ms = elapsed(c.ev[4], c.ev[5]);
+    timing->merge_ms = elapsed(c.ev[5], c.ev[6]);
+    timing->total_ms = elapsed(c.ev[3], c.ev[6]);
+    timing->qr_ms = br.qr_ms;
+    timing->jacobi_ms = br.jacobi_ms;
+    timing->jacobi_sweeps_max = br.sweeps_max;
+    timing->jacobi_rotations = br.rotations;
+    timing->kernel_launches = c.launches - launches0;
+    timing->jacobi_sweeps_sum = br.sweeps_sum;
+    timing->qr_flops = br.qr_flops;
+    timing->jacobi_flops = br.jacobi_flops;
+  }
+  *shard_out = sh.release();
+}
+
+// V for the shard's columns from the finished merge, packaged as rk_dev_outputs
+void shard_outputs(Ctx& c, const DevMatrix& rep, MergeOut& mo, uint32_t flags, uint64_t top_k, uint64_t col_lo,
+                   uint64_t col_hi, rk_dev_outputs** out, rk_timing* timing, uint64_t launches0) {
+  cudaStream_t s = c.stream;
+  const uint32_t M = (uint32_t)rep.csr.rows;
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
+  auto o = std::make_unique<DevOutputsImpl>();
+  uint32_t r = 0;
+  if (flags & RK_WANT_V) {
+    const uint32_t kk = (top_k && top_k < mo.k) ? (uint32_t)top_k : mo.k;
+    std::vector<double> sig;
+    to_host(sig, mo.sigma.get(), kk, s);
+    sync(s);
+    std::vector<uint32_t> ret = retained_of(sig.data(), kk, 1e-10);
+    r = (uint32_t)ret.size();
+    o->v.alloc((col_hi - col_lo) * (uint64_t)std::max<uint32_t>(r, 1), s);
+    if (r) {
+      DBuf<uint32_t> dret(r, s);
+      to_device(dret.get(), ret.data(), r, s);
+      recover_v_device(rep.csc, mo.u.get(), mo.k, dret.get(), mo.sigma.get(), r, o->v.get(), col_lo, col_hi, s);
+      sync(s);
+    }
+  }
+  RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
+  sync(s);
+  o->pub.rows = M;
+  o->pub.cols = col_hi - col_lo;
+  o->pub.k_sigma = mo.k;
+  o->pub.k_v = r;
+  o->sigma = std::move(mo.sigma);
+  o->u = std::move(mo.u);
+  o->pub.d_sigma = o->sigma.get();
+  o->pub.d_u = o->u.get();
+  o->pub.d_v = (flags & RK_WANT_V) ? o->v.get() : nullptr;
+  if (timing) {
+    std::memset(timing, 0, sizeof *timing);
+    timing->merge_ms = elapsed(c.ev[3], c.ev[4]);
+    timing->recover_ms = elapsed(c.ev[4], c.ev[5]);
+    timing->total_ms = elapsed(c.ev[3], c.ev[5]);
+    timing->kernel_launches = c.launches - launches0;
+  }
+  *out = &o.release()->pub;
+}
+
+}  // namespace
+
+extern "C" {
+
 rk_status rk_dev_shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
                               uint64_t keep, uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi, double* d_root_out,
                               rk_dev_shard** shard_out, rk_timing* timing) {
   return guarded([&] {
+    shard_factor(ctx, a, block_count, method, keep, seed, leaf_lo, leaf_hi, d_root_out, shard_out, timing, false);
+  });
+}
+
+rk_status rk_dev_shard_factor_gram(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
+                                   uint64_t keep, uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi,
+                                   double* d_gram_out, rk_dev_shard** shard_out, rk_timing* timing) {
+  return guarded([&] {
+    shard_factor(ctx, a, block_count, method, keep, seed, leaf_lo, leaf_hi, d_gram_out, shard_out, timing, true);
+  });
+}
+
+rk_status rk_dev_shard_tsqr(rk_ctx* ctx, rk_dev_shard* shard, double* d_root_out) {
+  return guarded([&] {
     check_ctx(ctx);
-    if (!a || !shard_out || !d_root_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    if (!shard || !d_root_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    if (!shard->has_records) fail(RK_INVALID_ARGUMENT, "the shard was not made by rk_dev_shard_factor_gram");
+    CallScope sc(&ctx->c);
+    Ctx& c = ctx->c;
+    const uint32_t M = (uint32_t)shard->rep()->csr.rows;
+    BlockStageResult& br = shard->blocks;
+    DBuf<double> R;
+    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, shard->local, 0, shard->local.size(), R);
+    RK_CUDA_CHECK(cudaMemcpyAsync(d_root_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice,
+                                  c.stream));
+    sync(c.stream);
+  });
+}
+
+rk_status rk_dev_shard_finish_gram(rk_ctx* ctx, rk_dev_shard* shard, const double* d_grams, uint64_t n_roots,
+                                   uint32_t flags, uint64_t top_k, uint64_t col_lo, uint64_t col_hi,
+                                   rk_dev_outputs** out, rk_timing* timing) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!shard || !d_grams || !out || n_roots == 0) fail(RK_INVALID_ARGUMENT, "NULL argument");
     CallScope sc(&ctx->c);
     Ctx& c = ctx->c;
     cudaStream_t s = c.stream;
     const uint64_t launches0 = c.launches;
-    auto sh = std::make_unique<rk_dev_shard>();
-    sh->owner = ctx;
-    sh->a = a;
-    sh->p = make_partition(a->m.csr.cols, block_count);
-    sh->method = method;
-    sh->seed = seed;
-    const uint32_t M = (uint32_t)a->m.csr.rows;
-    // the tree's leaves from the per-block kept counts
-    std::vector<uint32_t> kept(block_count);
-    for (uint64_t d = 0; d < block_count; ++d) {
-      const uint64_t w = sh->p.end(d) - sh->p.begin(d), k_full = std::min<uint64_t>(M, w);
-      kept[d] = (uint32_t)(keep == 0 ? k_full : std::min(keep, k_full));
-    }
-    std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
-    if (leaf_lo >= leaf_hi || leaf_hi > leaves.size()) fail(RK_OUT_OF_RANGE, "leaf range outside the merge tree");
+    const DevMatrix& rep = *shard->rep();
+    const uint32_t M = (uint32_t)rep.csr.rows;
+    if (col_hi > rep.csc.cols || col_lo > col_hi) fail(RK_OUT_OF_RANGE, "column range outside the matrix");
     RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
-    RepairOut rep;
-    sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, rep);
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
-    const uint64_t d_lo = leaves[leaf_lo].r0, d_hi = leaves[leaf_hi - 1].r1;
-    BlockStageResult br;
-    block_stage(c, *sh->rep(), sh->p, d_lo, d_hi, keep, br, nullptr);
-    if (any_failure(br)) throw_block_failure(br, d_lo);
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
-    // leaves re-indexed to the shard's records
-    std::vector<TreeLeaf> local(leaves.begin() + leaf_lo, leaves.begin() + leaf_hi);
-    for (TreeLeaf& L : local) { L.r0 -= (uint32_t)d_lo; L.r1 -= (uint32_t)d_lo; }
-    DBuf<double> R;
-    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, local, 0, local.size(), R);
-    RK_CUDA_CHECK(cudaMemcpyAsync(d_root_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice, s));
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[6], s));
-    sync(s);
-    if (timing) {
-      std::memset(timing, 0, sizeof *timing);
-      timing->repair_ms = elapsed(c.ev[3], c.ev[4]);
-      timing->blocks_ms = elapsed(c.ev[4], c.ev[5]);
-      timing->merge_ms = elapsed(c.ev[5], c.ev[6]);
-      timing->total_ms = elapsed(c.ev[3], c.ev[6]);
-      timing->qr_ms = br.qr_ms;
-      timing->jacobi_ms = br.jacobi_ms;
-      timing->jacobi_sweeps_max = br.sweeps_max;
-      timing->jacobi_rotations = br.rotations;
-      timing->kernel_launches = c.launches - launches0;
-      timing->jacobi_sweeps_sum = br.sweeps_sum;
-      timing->qr_flops = br.qr_flops;
-      timing->jacobi_flops = br.jacobi_flops;
-    }
-    *shard_out = sh.release();
+    const uint64_t mm = (uint64_t)M * M;
+    // the ranks' partials are aligned subtrees: finish the same pairwise tree
+    DBuf<double> g(n_roots * mm, s);
+    RK_CUDA_CHECK(cudaMemcpyAsync(g.get(), d_grams, sizeof(double) * n_roots * mm, cudaMemcpyDeviceToDevice, s));
+    gram_tree_sum(g.get(), n_roots, M, s);
+    const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
+    DBuf<double> W((uint64_t)M * cp, s);
+    W.zero();
+    RK_CUDA_CHECK(cudaMemcpyAsync(W.get(), g.get(), sizeof(double) * mm, cudaMemcpyDeviceToDevice, s));
+    g.release();
+    MergeOut mo;
+    if (!gram_merge(c, W, M, mo))
+      fail(RK_GRAM_REJECTED, "the kappa guard rejected the merge's Gram route: rk_dev_shard_tsqr, all-gather, "
+                             "rk_dev_shard_finish");
+    shard_outputs(c, rep, mo, flags, top_k, col_lo, col_hi, out, timing, launches0);
   });
 }
 
@@ -990,43 +1123,7 @@ rk_status rk_dev_shard_finish(rk_ctx* ctx, rk_dev_shard* shard, const double* d_
     }
     MergeOut mo;
     merge_finish(c, roots, M, mo);
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
-    auto o = std::make_unique<DevOutputsImpl>();
-    uint32_t r = 0;
-    if (flags & RK_WANT_V) {
-      const uint32_t kk = (top_k && top_k < mo.k) ? (uint32_t)top_k : mo.k;
-      std::vector<double> sig;
-      to_host(sig, mo.sigma.get(), kk, s);
-      sync(s);
-      std::vector<uint32_t> ret = retained_of(sig.data(), kk, 1e-10);
-      r = (uint32_t)ret.size();
-      o->v.alloc((col_hi - col_lo) * (uint64_t)std::max<uint32_t>(r, 1), s);
-      if (r) {
-        DBuf<uint32_t> dret(r, s);
-        to_device(dret.get(), ret.data(), r, s);
-        recover_v_device(rep.csc, mo.u.get(), mo.k, dret.get(), mo.sigma.get(), r, o->v.get(), col_lo, col_hi, s);
-        sync(s);
-      }
-    }
-    RK_CUDA_CHECK(cudaEventRecord(c.ev[5], s));
-    sync(s);
-    o->pub.rows = M;
-    o->pub.cols = col_hi - col_lo;
-    o->pub.k_sigma = mo.k;
-    o->pub.k_v = r;
-    o->sigma = std::move(mo.sigma);
-    o->u = std::move(mo.u);
-    o->pub.d_sigma = o->sigma.get();
-    o->pub.d_u = o->u.get();
-    o->pub.d_v = (flags & RK_WANT_V) ? o->v.get() : nullptr;
-    if (timing) {
-      std::memset(timing, 0, sizeof *timing);
-      timing->merge_ms = elapsed(c.ev[3], c.ev[4]);
-      timing->recover_ms = elapsed(c.ev[4], c.ev[5]);
-      timing->total_ms = elapsed(c.ev[3], c.ev[5]);
-      timing->kernel_launches = c.launches - launches0;
-    }
-    *out = &o.release()->pub;
+    shard_outputs(c, rep, mo, flags, top_k, col_lo, col_hi, out, timing, launches0);
   });
 }
 

@@ -133,6 +133,36 @@ __global__ void reduce_partials(const double* __restrict__ partial, uint32_t n_c
   }
 }
 
+// out[l] = sum of the partials of leaf l's chunks [c0[l], c1[l]) in chunk order
+// (as reduce_partials), mirrored to the upper triangle
+__global__ void reduce_leaf_partials(const double* __restrict__ partial, const uint32_t* __restrict__ c0,
+                                     const uint32_t* __restrict__ c1, uint32_t M, double* __restrict__ out) {
+  const uint64_t total = (uint64_t)M * M;
+  const uint32_t l = blockIdx.y;
+  double* G = out + (uint64_t)l * total;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(t % M), s = (uint32_t)(t / M);
+    if ((r / 8) < (s / 8)) continue;
+    double acc = 0.0;
+    for (uint32_t k = c0[l]; k < c1[l]; ++k) acc += partial[(uint64_t)k * total + t];
+    G[t] = acc;
+    G[s + (uint64_t)r * M] = acc;
+  }
+}
+
+// one level of the pairwise tree (csrc/rk_pipeline.cu forest_reduce's shape):
+// out node i = in node 2i + in node 2i+1; an odd last node is carried up unchanged
+__global__ void add_pairs_to(const double* __restrict__ in, double* __restrict__ out, uint64_t n_nodes,
+                             uint64_t mm) {
+  const uint64_t half = n_nodes / 2, out_nodes = (n_nodes + 1) / 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < out_nodes * mm;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = t / mm, e = t - i * mm;
+    out[t] = i < half ? in[2 * i * mm + e] + in[(2 * i + 1) * mm + e] : in[2 * i * mm + e];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // blocked right-looking Cholesky, one CTA per matrix, in place on the lower
 // triangle (column-major, ld M). On exit the strict upper triangle is zeroed so
@@ -534,6 +564,65 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
   reduce_partials<<<grid_for((uint64_t)M * M), 256, 0, s>>>(partial.get(), (uint32_t)ch.size(), M, G);
   RK_LAUNCH_CHECK();
   sync(s);  // host chunk list
+}
+
+void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s) {
+  const uint64_t mm = (uint64_t)M * M;
+  // level by level, ping-pong between mats and a scratch buffer
+  if (n <= 1) return;
+  DBuf<double> tmp(((n + 1) / 2) * mm, s);
+  double* src = mats;
+  double* dst = tmp.get();
+  while (n > 1) {
+    const uint64_t out_nodes = (n + 1) / 2;
+    add_pairs_to<<<grid_for(out_nodes * mm), 256, 0, s>>>(src, dst, n, mm);
+    RK_LAUNCH_CHECK();
+    n = out_nodes;
+    std::swap(src, dst);
+  }
+  if (src != mats) RK_CUDA_CHECK(cudaMemcpyAsync(mats, src, sizeof(double) * mm, cudaMemcpyDeviceToDevice, s));
+}
+
+void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
+                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s) {
+  if (M % 8) fail(RK_RUNTIME, "leaf_gram_tree: M must be a multiple of 8");
+  const uint64_t mm = (uint64_t)M * M, L = leaves.size();
+  if (L == 0) {
+    RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * mm, s));
+    return;
+  }
+  std::vector<SyrkChunk> ch;
+  std::vector<uint32_t> c0(L), c1(L);
+  for (uint64_t l = 0; l < L; ++l) {
+    c0[l] = (uint32_t)ch.size();
+    for (uint32_t d = leaves[l].first; d < leaves[l].second; ++d) {
+      if (!kept[d]) continue;
+      for (uint32_t j0 = 0; j0 < kept[d]; j0 += 256)
+        ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + 256)});
+    }
+    c1[l] = (uint32_t)ch.size();
+  }
+  DBuf<double> leafG(L * mm, s);
+  if (!ch.empty()) {
+    DBuf<SyrkChunk> dch(ch.size(), s);
+    to_device(dch.get(), ch.data(), ch.size(), s);
+    DBuf<double> partial(ch.size() * mm, s);
+    const uint64_t tiles = M / 8;
+    const uint64_t warps = tiles * (tiles + 1) / 2 * ch.size();
+    syrk_records_kernel<<<grid_for(warps * 32), 256, 0, s>>>(dch.get(), (uint32_t)ch.size(), M, partial.get());
+    RK_LAUNCH_CHECK();
+    DBuf<uint32_t> d0(L, s), d1(L, s);
+    to_device(d0.get(), c0.data(), L, s);
+    to_device(d1.get(), c1.data(), L, s);
+    reduce_leaf_partials<<<dim3(grid_for(mm, 1u << 12), (unsigned)L), 256, 0, s>>>(partial.get(), d0.get(), d1.get(),
+                                                                                  M, leafG.get());
+    RK_LAUNCH_CHECK();
+    sync(s);  // chunk lists are host memory
+  } else {
+    leafG.zero();
+  }
+  gram_tree_sum(leafG.get(), L, M, s);
+  RK_CUDA_CHECK(cudaMemcpyAsync(G, leafG.get(), sizeof(double) * mm, cudaMemcpyDeviceToDevice, s));
 }
 
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,

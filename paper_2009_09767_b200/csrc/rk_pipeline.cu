@@ -711,6 +711,38 @@ void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut
   merge_jacobi(c, W, M, M, cp, out);
 }
 
+bool gram_merge_eligible(uint32_t M) { return gram_route_enabled() && M <= cholesky_max_rows() && M % 8 == 0; }
+
+// Gram route of the merge: W holds P P^T (M x cols_pad slot); R_P^T = chol(P P^T),
+// accepted when kappa(P) <= kappa_max(M) (checked on the Cholesky diagonal, then on
+// the computed sigma). Returns false -- out untouched -- when rejected.
+bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out) {
+  cudaStream_t s = c.stream;
+  const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
+  double* ptr = W.get();
+  DBuf<double*> dptr(1, s);
+  DBuf<uint32_t> status(1, s);
+  DBuf<double> ratio(1, s);
+  to_device(dptr.get(), &ptr, 1, s);
+  cholesky_batched(dptr.get(), 1, M, status.get(), ratio.get(), s);
+  uint32_t hst = 1;
+  double hr = INFINITY;
+  RK_CUDA_CHECK(cudaMemcpyAsync(&hst, status.get(), sizeof hst, cudaMemcpyDeviceToHost, s));
+  RK_CUDA_CHECK(cudaMemcpyAsync(&hr, ratio.get(), sizeof hr, cudaMemcpyDeviceToHost, s));
+  sync(s);
+  prof_mark(s, "mrg chol+sync");
+  const double kmax = kappa_max(M);
+  if (hst == 0 && hr <= kmax) {
+    MergeOut tmp;
+    const double kappa = merge_jacobi(c, W, M, M, cp, tmp, true);
+    if (kappa <= kmax) {
+      out = std::move(tmp);
+      return true;
+    }
+  }
+  return false;
+}
+
 void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
                    const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out) {
   cudaStream_t s = c.stream;
@@ -724,34 +756,14 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   }
   if (total > M) {
     // Gram route: R_P^T = chol(P P^T), accepted when kappa(P) <= kappa_max(M)
-    if (gram_route_enabled() && M <= cholesky_max_rows() && M % 8 == 0) {
+    if (gram_merge_eligible(M)) {
       const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
       DBuf<double> W((uint64_t)M * cp, s);
       W.zero();
       prof_mark(s, "mrg alloc");
       records_gram(payload, offset, kept, M, W.get(), s);
       prof_mark(s, "mrg syrk");
-      double* ptr = W.get();
-      DBuf<double*> dptr(1, s);
-      DBuf<uint32_t> status(1, s);
-      DBuf<double> ratio(1, s);
-      to_device(dptr.get(), &ptr, 1, s);
-      cholesky_batched(dptr.get(), 1, M, status.get(), ratio.get(), s);
-      uint32_t hst = 1;
-      double hr = INFINITY;
-      RK_CUDA_CHECK(cudaMemcpyAsync(&hst, status.get(), sizeof hst, cudaMemcpyDeviceToHost, s));
-      RK_CUDA_CHECK(cudaMemcpyAsync(&hr, ratio.get(), sizeof hr, cudaMemcpyDeviceToHost, s));
-      sync(s);
-      prof_mark(s, "mrg chol+sync");
-      const double kmax = kappa_max(M);
-      if (hst == 0 && hr <= kmax) {
-        MergeOut tmp;
-        const double kappa = merge_jacobi(c, W, M, M, cp, tmp, true);
-        if (kappa <= kmax) {
-          out = std::move(tmp);
-          return;
-        }
-      }
+      if (gram_merge(c, W, M, out)) return;
     }
     std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
     std::vector<DBuf<double>> roots(1);

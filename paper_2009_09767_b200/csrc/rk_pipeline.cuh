@@ -1,6 +1,8 @@
 // rk_pipeline.cuh -- orchestration interfaces shared by rk_pipeline.cu and rk_api.cu
 #pragma once
 
+#include <utility>
+
 #include "rk_internal.cuh"
 
 namespace rk {
@@ -59,6 +61,11 @@ void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut
 void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
                    const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out);
 
+// the merge's Gram route (see merge_records): eligibility, and the finish from
+// W = P P^T (M x jacobi_cols_pad slot, consumed); false when the kappa guard rejects
+bool gram_merge_eligible(uint32_t M);
+bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out);
+
 // dense_svd on the device: a is rows x cols row-major (device). Outputs row-major.
 struct DenseSvdOut {
   uint32_t k = 0;
@@ -73,6 +80,14 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
                   uint32_t M, double* G, cudaStream_t s);
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
                       cudaStream_t s);
+// the Gram of the stacked records of the given leaves (block ranges [first, second)):
+// each leaf's records summed in chunk order, the leaves combined by the fixed
+// pairwise tree -- so a rank's aligned power-of-two run of leaves is a node of the
+// whole matrix's tree. G: M x M column-major (full).
+void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
+                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s);
+// pairwise tree sum of n M x M matrices stored back to back; the result in mats[0, M*M)
+void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s);
 double kappa_max(uint32_t M);
 uint32_t cholesky_max_rows();
 bool gram_route_enabled();

@@ -67,6 +67,14 @@ class RankyRuntimeError(RankyError, RuntimeError):
     pass
 
 
+GRAM_REJECTED = 8  # rk_status RK_GRAM_REJECTED
+
+
+class GramRejected(RankyError):
+    """RK_GRAM_REJECTED: the sharded merge's Gram route does not apply; the caller
+    takes the TSQR path (rk_dev_shard_tsqr, all-gather, rk_dev_shard_finish)."""
+
+
 class RecordError(RankyError, RuntimeError):
     """ranky::RecordError (proj/include/ranky/errors.hpp:23-26): damaged block record"""
 
@@ -210,6 +218,11 @@ def lib():
             "rk_dev_shard_finish": ([vp, vp, vp, u64, u32, u64, u64, u64, C.POINTER(C.POINTER(DevOutputs)),
                                      C.POINTER(Timing)], i32),
             "rk_dev_shard_destroy": ([vp], i32),
+            "rk_dev_shard_factor_gram": ([vp, vp, u64, i32, u64, u64, u64, u64, vp, C.POINTER(vp),
+                                          C.POINTER(Timing)], i32),
+            "rk_dev_shard_finish_gram": ([vp, vp, vp, u64, u32, u64, u64, u64, C.POINTER(C.POINTER(DevOutputs)),
+                                          C.POINTER(Timing)], i32),
+            "rk_dev_shard_tsqr": ([vp, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -238,6 +251,8 @@ def _check(status: int):
         raise MemoryError(msg)
     if status == 7:
         raise RecordError(msg)
+    if status == GRAM_REJECTED:
+        raise GramRejected(msg)
     raise RankyError(f"status {status}: {msg}")
 
 

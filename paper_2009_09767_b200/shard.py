@@ -2,10 +2,12 @@
 
 Column blocks are grouped into the leaves of the fixed merge tree
 (rk_merge_tree_leaves). Rank g of G owns a contiguous, aligned range of leaves:
-it factors those blocks, reduces them to its subtree's R factor
-(rk_dev_shard_factor), and owns the V rows of those blocks' columns. The G
-factors are all-gathered (NCCL) and every rank finishes the same top of the
-pairwise tree (rk_dev_shard_finish). With leaves/G a power of two every rank's
+it factors those blocks, reduces them to its subtree's Gram partial
+(rk_dev_shard_factor_gram; or its R factor, rk_dev_shard_factor /
+rk_dev_shard_tsqr, when the Gram route is rejected), and owns the V rows of
+those blocks' columns. The G factors are all-gathered (NCCL) and every rank
+finishes the same top of the pairwise tree (rk_dev_shard_finish_gram /
+rk_dev_shard_finish). With leaves/G a power of two every rank's
 subtree is a node of the single-GPU tree, so the result is bitwise independent
 of G.
 """

@@ -20,7 +20,11 @@ from test_gpu_svd import compare
 pytestmark = pytest.mark.gpu
 
 
-def run_sharded(dm, cfg, world):
+def run_sharded(dm, cfg, world, route="tsqr"):
+    """route "tsqr": rk_dev_shard_factor + rk_dev_shard_finish. route "gram": the
+    protocol of bench.py -- rk_dev_shard_factor_gram, all-gather of the Gram
+    partials, rk_dev_shard_finish_gram, with the TSQR fallback when either call
+    returns RK_GRAM_REJECTED. Returns the outputs and whether the Gram route held."""
     import torch
     L = R.lib()
     M = cfg.rows
@@ -28,25 +32,55 @@ def run_sharded(dm, cfg, world):
              for g in range(world)]
     roots = torch.empty((world, M, M), dtype=torch.float64, device="cuda")
     handles = []
+    gram = route == "gram"
     for g, sp in enumerate(plans):
         h = C.c_void_p()
         t = R.Timing()
-        R._check(L.rk_dev_shard_factor(dm.ctx.handle, dm.handle, cfg.blocks, R._method(cfg.method), cfg.keep,
-                                       cfg.seed, sp.leaf_lo, sp.leaf_hi, C.c_void_p(roots[g].data_ptr()),
-                                       C.byref(h), C.byref(t)))
+        args = (dm.ctx.handle, dm.handle, cfg.blocks, R._method(cfg.method), cfg.keep, cfg.seed, sp.leaf_lo,
+                sp.leaf_hi, C.c_void_p(roots[g].data_ptr()), C.byref(h), C.byref(t))
+        st = L.rk_dev_shard_factor_gram(*args) if gram else R.GRAM_REJECTED
+        if st == R.GRAM_REJECTED:
+            assert g == 0 or not gram, "the Gram route's applicability must not depend on the rank"
+            gram = False
+            st = L.rk_dev_shard_factor(*args)
+        R._check(st)
         handles.append(h)
     dm.ctx.synchronize()
     outs = []
+    rejected = False
     for g, sp in enumerate(plans):
         out = C.POINTER(R.DevOutputs)()
         t = R.Timing()
-        R._check(L.rk_dev_shard_finish(dm.ctx.handle, handles[g], C.c_void_p(roots.data_ptr()), world, R.WANT_V,
-                                       cfg.top_k, sp.col_lo, sp.col_hi, C.byref(out), C.byref(t)))
+        args = (dm.ctx.handle, handles[g], C.c_void_p(roots.data_ptr()), world, R.WANT_V, cfg.top_k, sp.col_lo,
+                sp.col_hi, C.byref(out), C.byref(t))
+        if gram:
+            st = L.rk_dev_shard_finish_gram(*args)
+            if st == R.GRAM_REJECTED:
+                assert g == 0 or rejected, "the kappa guard must decide identically on every rank"
+                rejected = True
+                break
+            R._check(st)
+        else:
+            R._check(L.rk_dev_shard_finish(*args))
         sig, u, v = R.dev_outputs_tensors(out)
         outs.append((sp, sig.cpu().numpy(), u.cpu().numpy(), v.cpu().numpy()))
         R.dev_outputs_free(out)
-        L.rk_dev_shard_destroy(handles[g])
-    return outs
+    if rejected:  # every rank: its TSQR factor, all-gather, the TSQR finish
+        gram = False
+        for g in range(world):
+            R._check(L.rk_dev_shard_tsqr(dm.ctx.handle, handles[g], C.c_void_p(roots[g].data_ptr())))
+        dm.ctx.synchronize()
+        for g, sp in enumerate(plans):
+            out = C.POINTER(R.DevOutputs)()
+            t = R.Timing()
+            R._check(L.rk_dev_shard_finish(dm.ctx.handle, handles[g], C.c_void_p(roots.data_ptr()), world,
+                                           R.WANT_V, cfg.top_k, sp.col_lo, sp.col_hi, C.byref(out), C.byref(t)))
+            sig, u, v = R.dev_outputs_tensors(out)
+            outs.append((sp, sig.cpu().numpy(), u.cpu().numpy(), v.cpu().numpy()))
+            R.dev_outputs_free(out)
+    for h in handles:
+        L.rk_dev_shard_destroy(h)
+    return (outs, gram) if route == "gram" else outs
 
 
 @pytest.mark.parametrize("name,scale", [("c2", None), ("c1", None)])
@@ -78,3 +112,48 @@ def test_sharded_matches_single_gpu(name, scale):
                 assert np.allclose(s2, s1, rtol=1e-10, atol=0), (name, world, sp.rank)
         # the ranks' V rows tile the matrix's columns
         assert sum(sp.col_hi - sp.col_lo for sp, *_ in outs) == a.cols()
+
+
+@pytest.mark.parametrize("name", ["c2", "c1"])
+def test_sharded_gram_route(name):
+    """The Gram route of the sharded merge: bitwise identical for every G (the
+    ranks' partials are nodes of one pairwise tree), parity with the single-GPU
+    call; c1's merge (kappa > kappa_max) exercises the rejection and the TSQR
+    fallback, which must then equal the TSQR route bitwise."""
+    cfg = configs.CONFIGS[name]
+    a = cfg.generate()
+    dm = rk.DeviceMatrix(a)
+    out, _ = R.dev_full_svd(dm, cfg.blocks, cfg.method, cfg.keep, cfg.seed, True, cfg.top_k)
+    sig, u, v = R.dev_outputs_tensors(out)
+    sig, u, v = sig.cpu().numpy(), u.cpu().numpy(), v.cpu().numpy()
+    R.dev_outputs_free(out)
+    n_leaves = shard.merge_tree_leaves(cfg.rows, a.cols(), cfg.blocks, cfg.keep)
+    ref = None
+    for world in (1, 2, 4, 8):
+        if world > n_leaves or not shard.bitwise_invariant(n_leaves, world):
+            continue
+        outs, held = run_sharded(dm, cfg, world, "gram")
+        if ref is None:
+            ref = outs[0]
+            compare(SimpleNamespace(sigma=ref[1], u=ref[2]), sig, u, f"{name} gram shard(1) vs single")
+            if not held:  # rejected: the fallback is the TSQR route exactly
+                [(_, s_t, u_t, v_t)] = run_sharded(dm, cfg, 1)
+                assert np.array_equal(s_t, ref[1]) and np.array_equal(u_t, ref[2])
+        for sp, s2, u2, v2 in outs:
+            assert np.array_equal(s2, ref[1]) and np.array_equal(u2, ref[2]), (name, world, sp.rank)
+            assert np.array_equal(v2, ref[3][sp.col_lo:sp.col_hi]), (name, world, sp.rank)
+    if name == "c2":
+        assert held, "c2's merge is well conditioned: the Gram route must hold"
+
+
+def test_sharded_gram_not_applicable(monkeypatch):
+    """RK_BLOCK_ROUTE=householder turns the Gram routes off: factor_gram reports
+    RK_GRAM_REJECTED (no shard) and the protocol takes the TSQR path."""
+    monkeypatch.setenv("RK_BLOCK_ROUTE", "householder")
+    cfg = configs.CONFIGS["c1"]
+    dm = rk.DeviceMatrix(cfg.generate())
+    outs, held = run_sharded(dm, cfg, 2, "gram")
+    assert not held
+    tsqr = run_sharded(dm, cfg, 2)
+    for (sp, s1, u1, v1), (_, s2, u2, v2) in zip(outs, tsqr):
+        assert np.array_equal(s1, s2) and np.array_equal(u1, u2) and np.array_equal(v1, v2)
