@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -388,6 +389,23 @@ __device__ __forceinline__ void factor_diag(double* P, uint32_t ldp, uint32_t nb
   __syncwarp();
 }
 
+// S[i + c ld] = src[i + c M] for i < rows, c < ncols (<= kCB): a thread's loads of
+// all kCB columns are issued before its stores (one L2 round trip per 256 rows, not
+// one per column: the per-column loop serialized 32 round trips per chunk and was
+// half of the kernel's time)
+template <int kCB>
+__device__ __forceinline__ void stage_cols(double* S, uint32_t ld, const double* src, uint32_t M, uint32_t rows,
+                                           uint32_t ncols, int tid) {
+  for (uint32_t i = tid; i < rows; i += kCT) {
+    double v[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) v[c] = c < (int)ncols ? src[i + (uint64_t)c * M] : 0.0;
+#pragma unroll
+    for (int c = 0; c < kCB; ++c)
+      if (c < (int)ncols) S[i + c * ld] = v[c];
+  }
+}
+
 // Left-looking variant: panel by panel (kCB columns), the update of the panel by
 // the finished columns, P -= L[k0:, :k0] L[k0:k0+kCB, :k0]^T, runs as a DMMA GEMM
 // over K chunks of kCB columns staged in shared memory with coalesced loads (one
@@ -403,6 +421,9 @@ __host__ __device__ constexpr uint32_t ll_ld(uint32_t rows) {
   return ((rows + 11) / 16) * 16 + 4;
 }
 
+#ifndef CHOL_PROBE
+#define CHOL_PROBE 0
+#endif
 template <int kCB, int NP>
 __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __restrict__ mats, uint32_t M,
                                                              uint32_t* __restrict__ status,
@@ -417,6 +438,15 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
   const int lr = lane >> 2, lc = lane & 3;
   constexpr int kW = kCT / 32;
   if (tid == 0) { s_bad = 0; s_dmin = INFINITY; s_dmax = 0.0; }
+  long long tm[6] = {0, 0, 0, 0, 0, 0};
+  long long tcl = clock64();
+  auto tick = [&](int k) {
+    if (CHOL_PROBE) {
+      const long long t = clock64();
+      tm[k] += t - tcl;
+      tcl = t;
+    }
+  };
   for (uint32_t k0 = 0; k0 < M; k0 += kCB) {
     const uint32_t nb = min((uint32_t)kCB, M - k0), rows_p = M - k0;
     const uint32_t ld = ll_ld<kCB>(rows_p);
@@ -429,13 +459,7 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
     // GEMM over the finished columns, kCB at a time
     for (uint32_t kc = 0; kc < k0; kc += kCB) {
       __syncthreads();  // previous users of S are done
-      // (2-D loops: a runtime t / rows_p, t % rows_p per element was most of the
-      // kernel's instructions)
-#pragma unroll 8
-      for (int c = 0; c < kCB; ++c) {
-        const double* src = A + k0 + (uint64_t)(kc + c) * M;
-        for (uint32_t i = tid; i < rows_p; i += kCT) S[i + c * ld] = src[i];
-      }
+      stage_cols<kCB>(S, ld, A + k0 + (uint64_t)kc * M, M, rows_p, kCB, tid);
       __syncthreads();
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {
@@ -457,13 +481,9 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
       }
     }
     __syncthreads();
+    tick(0);
     // the panel minus the update
-#pragma unroll 8
-    for (int c = 0; c < kCB; ++c) {
-      if (c >= (int)nb) break;
-      const double* src = A + k0 + (uint64_t)(k0 + c) * M;
-      for (uint32_t i = tid; i < rows_p; i += kCT) S[i + c * ld] = src[i];
-    }
+    stage_cols<kCB>(S, ld, A + k0 + (uint64_t)k0 * M, M, rows_p, nb, tid);
     __syncthreads();
     if (k0 > 0) {
 #pragma unroll
@@ -481,11 +501,13 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
       }
       __syncthreads();
     }
+    tick(1);
     if (warp == 0) {
       if (nb == kCB) factor_diag<kCB, true>(S, ld, nb, lane, Dinv, &s_bad, &s_dmin, &s_dmax);
       else factor_diag<kCB, false>(S, ld, nb, lane, Dinv, &s_bad, &s_dmin, &s_dmax);
     }
     __syncthreads();
+    tick(2);
     if (s_bad) break;
     // rows below: x = p L11^{-T} (forward substitution, thread per row)
     for (uint32_t i = nb + tid; i < rows_p; i += kCT) {
@@ -507,6 +529,7 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
         if (j < (int)nb) S[i + j * ld] = x[j];
     }
     __syncthreads();
+    tick(3);
     // write the finished columns (zeros above the diagonal)
 #pragma unroll 8
     for (int j = 0; j < kCB; ++j) {
@@ -515,6 +538,10 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_ll_kernel(double* const* __re
       for (uint32_t i = tid; i < M; i += kCT) dst[i] = i < k0 ? 0.0 : S[(i - k0) + j * ld];
     }
   }
+  tick(4);
+  if (CHOL_PROBE && tid == 0 && blockIdx.x == 0)
+    printf("[chol] M %u cycles: gemm %lld panel %lld diag %lld trsm %lld writeback %lld\n", M, tm[0], tm[1], tm[2],
+           tm[3], tm[4]);
   if (tid == 0) {
     status[blockIdx.x] = s_bad ? 1u : 0u;
     diag_ratio[blockIdx.x] = s_bad ? INFINITY : s_dmax / s_dmin;
