@@ -211,6 +211,8 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS_rt, ui
   }
   uint32_t jl = active ? (uint32_t)grp : 0u;  // (grp + r) mod g, advanced incrementally
   double* const bbase = sW + (uint64_t)g * ldS + lq;
+  constexpr bool kWide = (Q == 32 && GT == 8);  // the latency plan's instantiation (1 CTA / SM)
+  double best_g2 = 0.0, best_prod = 1.0;
 #pragma unroll(GT > 0 ? 4 : 1)
   for (uint32_t r = 0; r < g; ++r) {
     if (GT > 0 && (GT & (GT - 1)) == 0) jl = (uint32_t)(grp + r) & (uint32_t)(GT - 1);
@@ -232,7 +234,18 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS_rt, ui
 #pragma unroll
     for (int o = Q / 2; o; o >>= 1) gamma += __shfl_xor_sync(0xffffffffu, gamma, o);
     const double prod = aA * aB, g2 = gamma * gamma;
-    if (live && g2 > max_r2 * prod) max_r2 = g2 / prod;
+    if constexpr (kWide) {
+      // the largest ratio as a (g2, prod) pair compared by cross multiplication: no
+      // division on the round's chain (one per call, below). Only where registers
+      // allow (the one-CTA-per-SM instantiation): at the 128-register cap the two
+      // extra live values spill
+      if (live && g2 * best_prod > best_g2 * prod) {
+        best_g2 = g2;
+        best_prod = prod;
+      }
+    } else {
+      if (live && g2 > max_r2 * prod) max_r2 = g2 / prod;
+    }
     const bool rot = live && (g2 > kJacobiTol * kJacobiTol * prod);
     if (__any_sync(0xffffffffu, rot)) {
       double c = 1.0, sn = 0.0;
@@ -256,6 +269,7 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS_rt, ui
     if (!(GT > 0 && (GT & (GT - 1)) == 0)) jl = (jl + 1 == g) ? 0u : jl + 1;
     __syncthreads();
   }
+  if (kWide && best_g2 > max_r2 * best_prod) max_r2 = best_g2 / best_prod;
   if (active) {
     double* pa = sW + (uint64_t)grp * ldS + lq;
 #pragma unroll
@@ -502,7 +516,7 @@ __device__ bool run_tail(cg::cluster_group& cluster, const JacobiJob& job, unsig
 }
 
 template <int Q, int E, bool EXACT, int GT = 0>
-__global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
+__global__ void __launch_bounds__(kJThreads, (E <= 16 && !(Q == 32 && GT == 8) ? 2 : 1)) jacobi_cluster_kernel(JacobiParams P) {
   extern __shared__ __align__(16) double smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
@@ -648,6 +662,27 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 ? 2 : 1)) jacobi_cluster_k
           }
         }
         // write back
+        if constexpr (EXACT && Q == 32 && GT == 8) {
+          // the one-CTA-per-SM instantiation has the registers: all shared-memory
+          // loads of the warp first, then the global stores
+          constexpr uint32_t kR = (uint32_t)(Q * E), kC = 2 * GT / kJWarps, kI = kR / 32;
+          double v[kC * kI];
+#pragma unroll
+          for (uint32_t cc = 0; cc < kC; ++cc) {
+            const double* src = sW + (uint64_t)(warp + cc * kJWarps) * (kR + 8) + lane;
+#pragma unroll
+            for (uint32_t i = 0; i < kI; ++i) v[cc * kI + i] = src[32 * i];
+          }
+#pragma unroll
+          for (uint32_t cc = 0; cc < kC; ++cc) {
+            const uint32_t c = warp + cc * kJWarps;
+            const uint32_t col = (c < GT ? gA * GT + c : gB * GT + (c - GT));
+            double* dst = W + (uint64_t)col * kR + lane;
+#pragma unroll
+            for (uint32_t i = 0; i < kI; ++i) dst[32 * i] = v[cc * kI + i];
+            if (lane == 0) alpha_g[col] = sAlpha[c];
+          }
+        } else
         for (uint32_t c = warp; c < 2 * g; c += kJWarps) {
           const uint32_t col = (c < g ? gA * g + c : gB * g + (c - g));
           double* dst = W + (uint64_t)col * rows;
