@@ -9,6 +9,8 @@
 // reference. U's retained columns are gathered once into a compact M x r table
 // (L2-resident); V rows are written once, 16-byte vectorised, with streaming
 // stores: the kernel is bound by the 8*N*r-byte V write.
+#include <cstdlib>
+
 #include "rk_internal.cuh"
 
 namespace rk {
@@ -92,6 +94,57 @@ __global__ void __launch_bounds__(256) spmm_kernel(const uint64_t* __restrict__ 
   }
 }
 
+// Half a warp per column (two columns per warp in flight), r % 32 == 0 and
+// r <= 32 * kH: lane l of a half owns the double pairs 2 l + 32 k. Twice the
+// columns' load chains (col_ptr -> entries -> U rows) in flight per warp of the
+// one-warp-per-column kernel; same arithmetic and entry order, so V is the same
+// bits.
+template <int kH>
+__global__ void __launch_bounds__(256) spmm_half_kernel(const uint64_t* __restrict__ col_ptr,
+                                                        const uint32_t* __restrict__ row_idx,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ u_ret,
+                                                        const double* __restrict__ inv, uint32_t r, uint64_t col_lo,
+                                                        uint64_t col_hi, double* __restrict__ v) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, l = lane & 15;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c0 = col_lo + 2 * warp0; c0 < col_hi; c0 += 2 * nwarps) {
+    const uint64_t c = c0 + half;
+    const bool live = c < col_hi;
+    const uint64_t e0 = live ? col_ptr[c] : 0, e1 = live ? col_ptr[c + 1] : 0;
+    double2 acc[kH];
+#pragma unroll
+    for (int k = 0; k < kH; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (uint64_t e = e0; e < e1; ++e) {
+      const double x = val[e];
+      const double2* ur = reinterpret_cast<const double2*>(u_ret + (uint64_t)row_idx[e] * r);
+#pragma unroll
+      for (int k = 0; k < kH; ++k) {
+        const uint32_t j = 32 * k + 2 * l;
+        if (j < r) {
+          const double2 uu = ur[j / 2];
+          acc[k].x = __dadd_rn(acc[k].x, __dmul_rn(x, uu.x));
+          acc[k].y = __dadd_rn(acc[k].y, __dmul_rn(x, uu.y));
+        }
+      }
+    }
+    if (live) {
+      double* vrow = v + (c - col_lo) * r;
+#pragma unroll
+      for (int k = 0; k < kH; ++k) {
+        const uint32_t j = 32 * k + 2 * l;
+        if (j < r) {
+          double2 o;
+          o.x = __dmul_rn(acc[k].x, inv[j]);
+          o.y = __dmul_rn(acc[k].y, inv[j + 1]);
+          __stcs(reinterpret_cast<double2*>(vrow + j), o);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const uint32_t* retained,
@@ -109,7 +162,15 @@ void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const u
   const uint64_t cols = col_hi - col_lo;
   unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(cols * 32, 256), (uint64_t)sms * 16);
   if (grid == 0) grid = 1;
-  if ((r & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0)
+  const char* se = std::getenv("RK_SPMM_WARP");
+  if (!(se && se[0] == '1') && r % 32 == 0 && r <= 512 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    if (r <= 256)
+      spmm_half_kernel<8><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r,
+                                               col_lo, col_hi, v);
+    else
+      spmm_half_kernel<16><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r,
+                                                col_lo, col_hi, v);
+  } else if ((r & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0)
     spmm_kernel<true><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
                                            col_hi, v);
   else

@@ -173,3 +173,22 @@ def test_block_routes_agree(route, monkeypatch, ref):
         res = rk.run_pipeline(a, blocks, cfg.method, cfg.keep, cfg.seed, 1)
         o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), blocks, cfg.method, cfg.keep, cfg.seed)
         compare(res.svd, o.sigma, o.u, f"{name} {route}")
+
+
+@pytest.mark.parametrize("env", [("RK_PRECOND", "1"), ("RK_CHOL", "r"), ("RK_SPMM_WARP", "1")])
+def test_variant_switches_agree(env, monkeypatch, ref):
+    """The opt-in variants (FP32-preconditioned Jacobi, the right-looking Cholesky,
+    the one-warp-per-column V SpMM) reproduce the reference on a c2 slice like the
+    defaults: only how the result is reached changes, not the stopping rule or
+    the V arithmetic."""
+    monkeypatch.setenv(*env)
+    cfg = configs.CONFIGS["c2"]
+    scale = 262144 // 8
+    a = cfg.generate(scale)
+    r, c, v = a.coo()
+    blocks = cfg.blocks // 8
+    res = rk.run_pipeline(a, blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True)
+    o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), blocks, cfg.method, cfg.keep, cfg.seed)
+    compare(res.svd, o.sigma, o.u, f"c2 slice {env}")
+    vr = ref.recover_right_vectors((a.rows(), a.cols(), *res.repaired.coo()), res.svd.u, res.svd.sigma, 1e-10)
+    assert np.array_equal(res.svd.v, vr)
