@@ -81,7 +81,11 @@ size_t device_free_bytes(Ctx& c, uint64_t want) {
                          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
                          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess;
   cudaGetLastError();
-  if (have_pool && c.free_known) {
+  static const bool exact = [] {
+    const char* e = std::getenv("RK_MEMINFO");
+    return e && e[0] == 'x';
+  }();
+  if (have_pool && c.free_known && !exact) {
     // free now = free0 - (reserved - reserved0); the pool's reserved-but-unused part is ours too
     const int64_t est = (int64_t)c.free0 + (int64_t)c.reserved0 - (int64_t)used;
     if (est > 0 && (uint64_t)est >= want) return (size_t)est;

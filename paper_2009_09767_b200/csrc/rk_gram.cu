@@ -570,11 +570,15 @@ void sparse_gram(const DevCsr& a, const Partition& p, uint64_t d_lo, uint64_t nb
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
                   uint32_t M, double* G, cudaStream_t s) {
   if (M % 8) fail(RK_RUNTIME, "records_gram: M must be a multiple of 8");
+  // split-K chunks of at most kChunk columns of one record; each chunk has an
+  // M x M partial, so the chunk width grows with M to bound that buffer (c4:
+  // 1024 records x 1024 columns -> 1024 partials of 8 MiB, not 4096)
+  const uint32_t kChunk = M <= 256 ? 256u : 1024u;
   std::vector<SyrkChunk> ch;
   for (size_t d = 0; d < kept.size(); ++d) {
     if (!kept[d]) continue;
-    for (uint32_t j0 = 0; j0 < kept[d]; j0 += 256)
-      ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + 256)});
+    for (uint32_t j0 = 0; j0 < kept[d]; j0 += kChunk)
+      ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + kChunk)});
   }
   if (ch.empty()) {
     RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * M * M, s));
