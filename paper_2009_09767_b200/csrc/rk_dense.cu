@@ -1114,14 +1114,19 @@ __global__ void __launch_bounds__(kFThreads) finalize_kernel(const FinalJob* job
     double best = -1.0;
     uint32_t arg = 0;
     if (!deficient) {
+      // the first index (in the ORIGINAL row order) of the largest |u|
+      const uint32_t* rp = J.row_perm;
+      uint32_t argo = 0xffffffffu;
       for (uint32_t i = lane; i < rows; i += 32) {
         const double mag = fabs(wj[i] / s);
-        if (mag > best) { best = mag; arg = i; }
+        const uint32_t io = rp ? rp[i] : i;
+        if (mag > best || (mag == best && io < argo)) { best = mag; arg = i; argo = io; }
       }
       for (int o = 16; o; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const uint32_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
-        if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+        const uint32_t oo = __shfl_xor_sync(0xffffffffu, argo, o);
+        if (ob > best || (ob == best && oo < argo)) { best = ob; arg = oa; argo = oo; }
       }
     }
     const bool flip = !deficient && (wj[arg] / s) < 0.0;
@@ -1164,6 +1169,7 @@ __global__ void __launch_bounds__(256) finalize_write_kernel(const FinalJob* job
     for (int r = ty; r < 32; r += 8) {
       const uint32_t i = i0 + r, j = j0 + tx;
       if (i < nrows && j < J.k) {
+        const uint32_t io = (!is_v && J.row_perm) ? J.row_perm[i] : i;  // output row
         const uint32_t o = s_src[tx];
         const double s = s_sig[tx], w = tile[tx][r];
         const bool def = (o & kOrderDef) != 0u, flip = (o & kOrderFlip) != 0u;
@@ -1171,8 +1177,8 @@ __global__ void __launch_bounds__(256) finalize_write_kernel(const FinalJob* job
           out_u[(uint64_t)i * J.k + j] = flip ? -w : w;
         } else {
           const double u = def ? 0.0 : (flip ? -(w / s) : (w / s));
-          if (out_u) out_u[(uint64_t)i * J.k + j] = u;
-          if (out_p) out_p[(uint64_t)i * J.k + j] = def ? (s > 0.0 ? w : 0.0) : u * s;
+          if (out_u) out_u[(uint64_t)io * J.k + j] = u;
+          if (out_p) out_p[(uint64_t)io * J.k + j] = def ? (s > 0.0 ? w : 0.0) : u * s;
         }
       }
     }

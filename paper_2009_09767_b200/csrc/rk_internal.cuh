@@ -378,6 +378,7 @@ struct FinalJob {
   uint64_t ldv;
   double* v_out;      // cols x k row-major (nullable)
   uint8_t* deficient; // k flags out (nullable): sigma <= kRankTol * sigma_max or zero
+  const uint32_t* row_perm;  // nullable: W's row i is original row row_perm[i] (u / payload rows un-permuted)
 };
 void finalize_batched(const std::vector<FinalJob>& jobs, cudaStream_t s);
 // deterministic orthonormal completion of flagged columns -- svd.cpp:150-201

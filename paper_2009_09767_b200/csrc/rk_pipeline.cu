@@ -266,7 +266,8 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   // Jacobi + finalize of a set of W slots; records stats and writes payloads
   std::vector<double> sigma_host;  // sorted sigma of the Gram-route slots (read with the Jacobi stats)
   auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
-                             bool gram_ok, double* sigma_all /* nullable: slots x cols_pad */) {
+                             bool gram_ok, double* sigma_all /* nullable: slots x cols_pad */,
+                             const std::vector<const uint32_t*>* row_perms = nullptr) {
     const size_t nb = slots.size();
     DBuf<double> alpha((uint64_t)nb * cols_pad_full, s);
     DBuf<uint64_t> stats(8 * nb, s);
@@ -301,6 +302,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       f.order = order.get() + (uint64_t)q * cols_pad_full;
       f.scratch = fscratch.get() + (uint64_t)q * cols_pad_full;
       f.sigma_all = sigma_all ? sigma_all + (uint64_t)q * cols_pad_full : nullptr;
+      f.row_perm = row_perms ? (*row_perms)[q] : nullptr;
       if (api) {
         f.u = api->u.get() + out.offset[i];
         f.sigma = api->sigma.get() + i * (uint64_t)M;
@@ -346,6 +348,17 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       W.zero();
       RK_CUDA_CHECK(cudaEventRecord(c.ev[8], s));
       sparse_gram(a.csr, p, d_lo + i0, nb, W.get(), (uint64_t)M * cols_pad_full, s);
+      // rows by descending Gram diagonal (fewer Jacobi sweeps); U's rows are
+      // un-permuted by the finalize (FinalJob::row_perm)
+      DBuf<uint32_t> perm;
+      const bool order = diag_order_enabled() && M <= 1280;
+      if (order) {
+        perm.alloc(nb * M, s);
+        DBuf<double> Wp(nb * M * cols_pad_full, s);
+        if (cols_pad_full != M) Wp.zero();
+        diag_order(W.get(), (uint64_t)M * cols_pad_full, M, nb, perm.get(), Wp.get(), s);
+        W = std::move(Wp);
+      }
       std::vector<double*> ptrs(nb);
       for (uint64_t q = 0; q < nb; ++q) ptrs[q] = W.get() + q * M * cols_pad_full;
       DBuf<double*> dptrs(nb, s);
@@ -367,16 +380,18 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       std::vector<double*> slots;
       std::vector<uint32_t> cols;
       std::vector<uint64_t> blocks;
+      std::vector<const uint32_t*> perms;
       for (uint64_t q = 0; q < nb; ++q) {
         const uint64_t i = i0 + q;
         if (skip[i] || hst[q] != 0 || !(hrat[q] <= kmax)) continue;
         slots.push_back(ptrs[q]);
         cols.push_back(M);
         blocks.push_back(i);
+        perms.push_back(order ? perm.get() + q * M : nullptr);
       }
       if (slots.empty()) continue;
       DBuf<double> sig((uint64_t)slots.size() * cols_pad_full, s);
-      jacobi_finalize(slots, cols, blocks, true, sig.get());
+      jacobi_finalize(slots, cols, blocks, true, sig.get(), &perms);
       const std::vector<double>& hs = sigma_host;
       for (size_t q = 0; q < slots.size(); ++q) {
         const double smax = hs[q * cols_pad_full], smin = hs[q * cols_pad_full + M - 1];
@@ -640,7 +655,7 @@ namespace {
 // Jacobi on W (M x cp, ld M, `cols` real columns) and finalize into out (sigma, U);
 // returns kappa = sigma_max / sigma_min over the `cols` columns
 double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t cp, MergeOut& out,
-                    bool gram_ok = false) {
+                    bool gram_ok = false, const uint32_t* row_perm = nullptr) {
   cudaStream_t s = c.stream;
   const uint32_t k = std::min(M, cols);
   out.k = k;
@@ -666,6 +681,7 @@ double merge_jacobi(Ctx& c, DBuf<double>& W, uint32_t M, uint32_t cols, uint32_t
   f.w = W.get(); f.rows = M; f.cols = cp; f.k = k;
   f.u = out.u.get(); f.sigma = out.sigma.get(); f.sigma_all = sig_all.get();
   f.order = order.get(); f.scratch = scratch.get(); f.deficient = def.get();
+  f.row_perm = row_perm;
   finalize_batched({f}, s);
   std::vector<uint64_t> hst;
   std::vector<double> hs;
@@ -719,6 +735,15 @@ bool gram_merge_eligible(uint32_t M) { return gram_route_enabled() && M <= chole
 bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out) {
   cudaStream_t s = c.stream;
   const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
+  // rows by descending diagonal, as the blocks' Grams (fewer sweeps)
+  DBuf<uint32_t> perm;
+  if (diag_order_enabled()) {
+    perm.alloc(M, s);
+    DBuf<double> Wp((uint64_t)M * cp, s);
+    if (cp != M) Wp.zero();
+    diag_order(W.get(), (uint64_t)M * cp, M, 1, perm.get(), Wp.get(), s);
+    W = std::move(Wp);
+  }
   double* ptr = W.get();
   DBuf<double*> dptr(1, s);
   DBuf<uint32_t> status(1, s);
@@ -734,7 +759,7 @@ bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out) {
   const double kmax = kappa_max(M);
   if (hst == 0 && hr <= kmax) {
     MergeOut tmp;
-    const double kappa = merge_jacobi(c, W, M, M, cp, tmp, true);
+    const double kappa = merge_jacobi(c, W, M, M, cp, tmp, true, perm.n ? perm.get() : nullptr);
     if (kappa <= kmax) {
       out = std::move(tmp);
       return true;

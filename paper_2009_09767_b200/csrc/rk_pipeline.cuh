@@ -88,6 +88,11 @@ void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, 
                     uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s);
 // pairwise tree sum of n M x M matrices stored back to back; the result in mats[0, M*M)
 void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s);
+// symmetric diagonal ordering of nb Grams (slots of `stride` doubles, M x M,
+// ld M): perm (nb x M, position -> original row), Gp = the permuted Grams
+void diag_order(const double* G, uint64_t stride, uint32_t M, uint64_t nb, uint32_t* perm, double* Gp,
+                cudaStream_t s);
+bool diag_order_enabled();  // RK_DIAG_ORDER=0 turns it off
 double kappa_max(uint32_t M);
 uint32_t cholesky_max_rows();
 bool gram_route_enabled();

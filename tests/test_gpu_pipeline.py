@@ -175,12 +175,12 @@ def test_block_routes_agree(route, monkeypatch, ref):
         compare(res.svd, o.sigma, o.u, f"{name} {route}")
 
 
-@pytest.mark.parametrize("env", [("RK_PRECOND", "1"), ("RK_CHOL", "r"), ("RK_SPMM_WARP", "1")])
+@pytest.mark.parametrize("env", [("RK_PRECOND", "1"), ("RK_CHOL", "r"), ("RK_SPMM_WARP", "1"), ("RK_DIAG_ORDER", "0")])
 def test_variant_switches_agree(env, monkeypatch, ref):
     """The opt-in variants (FP32-preconditioned Jacobi, the right-looking Cholesky,
-    the one-warp-per-column V SpMM) reproduce the reference on a c2 slice like the
-    defaults: only how the result is reached changes, not the stopping rule or
-    the V arithmetic."""
+    the one-warp-per-column V SpMM, the Gram route without diagonal ordering)
+    reproduce the reference on a c2 slice like the defaults: only how the result
+    is reached changes, not the stopping rule or the V arithmetic."""
     monkeypatch.setenv(*env)
     cfg = configs.CONFIGS["c2"]
     scale = 262144 // 8
