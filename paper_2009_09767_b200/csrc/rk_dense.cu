@@ -296,7 +296,10 @@ __device__ __forceinline__ void cross_rounds_reg(double* sW, uint32_t ldS_rt, ui
 //      every other pair was tested and left alone -- then checks again;
 //   4. many violations: back to full sweeps.
 // Each check computes all the sweep's dot products, so it counts as a sweep.
-constexpr int kViolCap = 64;
+#ifndef RK_VIOL_CAP
+#define RK_VIOL_CAP 64
+#endif
+constexpr int kViolCap = RK_VIOL_CAP;
 constexpr int kTailIters = 8;  // then back to full sweeps
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
