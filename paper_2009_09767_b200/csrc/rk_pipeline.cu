@@ -347,7 +347,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       DBuf<double> W(nb * M * cols_pad_full, s);
       W.zero();
       RK_CUDA_CHECK(cudaEventRecord(c.ev[8], s));
-      sparse_gram(a.csr, p, d_lo + i0, nb, W.get(), (uint64_t)M * cols_pad_full, s);
+      sparse_gram(a, p, d_lo + i0, nb, W.get(), (uint64_t)M * cols_pad_full, s);
       // rows by descending Gram diagonal (fewer Jacobi sweeps); U's rows are
       // un-permuted by the finalize (FinalJob::row_perm)
       DBuf<uint32_t> perm;

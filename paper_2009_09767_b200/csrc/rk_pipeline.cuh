@@ -74,7 +74,7 @@ struct DenseSvdOut {
 void dense_svd_dev(Ctx& c, const double* a, uint32_t rows, uint32_t cols, DenseSvdOut& out);
 
 // rk_gram.cu: Gram + Cholesky route (see the file header)
-void sparse_gram(const DevCsr& a, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
+void sparse_gram(const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
                  cudaStream_t s);
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
                   uint32_t M, double* G, cudaStream_t s);

@@ -192,3 +192,22 @@ def test_variant_switches_agree(env, monkeypatch, ref):
     compare(res.svd, o.sigma, o.u, f"c2 slice {env}")
     vr = ref.recover_right_vectors((a.rows(), a.cols(), *res.repaired.coo()), res.svd.u, res.svd.sigma, 1e-10)
     assert np.array_equal(res.svd.v, vr)
+
+
+def test_gram_kernels_bitwise(monkeypatch):
+    """The block Gram from rows x columns (default) and from row pairs (the
+    merge-join kernel, RK_GRAM_PAIRS=1) add every G(r, s) in ascending column
+    order from zero: the pipeline's outputs are bitwise the same."""
+    from paper_2009_09767_b200 import ranky as R
+    cfg = configs.CONFIGS["c2"]
+    a = cfg.generate(262144 // 4)
+    dm = rk.DeviceMatrix(a)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RK_GRAM_PAIRS", flag)
+        out, _ = R.dev_full_svd(dm, cfg.blocks // 4, cfg.method, cfg.keep, cfg.seed, True, cfg.top_k)
+        sig, u, v = R.dev_outputs_tensors(out)
+        outs.append((sig.cpu().numpy(), u.cpu().numpy(), v.cpu().numpy()))
+        R.dev_outputs_free(out)
+    for x, y in zip(outs[0], outs[1]):
+        assert np.array_equal(x, y)
