@@ -150,35 +150,50 @@ __global__ void add_counts(const uint64_t* old_ptr, const uint64_t* eptr, uint64
     cnt[s] = (old_ptr[s + 1] - old_ptr[s]) + (eptr[s + 1] - eptr[s]);
 }
 
-// warp per segment: merged = old entries (sorted) + edge keys (sorted) with value 1.0
-__global__ void merge_segments(const uint64_t* old_ptr, const uint32_t* old_key, const double* old_val,
-                               const uint64_t* eptr, const uint32_t* ekey, uint64_t nseg,
-                               const uint64_t* new_ptr, uint32_t* new_key, double* new_val) {
-  const int lane = threadIdx.x & 31;
-  for (uint64_t s = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; s < nseg;
-       s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
-    const uint64_t o0 = old_ptr[s], o1 = old_ptr[s + 1];
-    const uint64_t e0 = eptr[s], e1 = eptr[s + 1];
-    const uint64_t base = new_ptr[s];
-    for (uint64_t i = o0 + lane; i < o1; i += 32) {
+// merged segment = old entries (sorted) + edge keys (sorted, value 1.0):
+// one thread per entry (old entries, then edges): the entry's
+// segment by binary search over the segment pointers, its rank among the other
+// list's keys of that segment by binary search. Flat parallelism for both shapes
+// -- 256 long CSR rows (a warp per row left most of the GPU idle: 47 us) and
+// 262k one-entry CSC columns (a warp per column left most lanes idle)
+__device__ __forceinline__ uint64_t segment_of(const uint64_t* ptr, uint64_t nseg, uint64_t i) {
+  uint64_t lo = 0, hi = nseg;  // last s with ptr[s] <= i
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi + 1) >> 1;
+    if (ptr[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void merge_flat(const uint64_t* __restrict__ old_ptr, const uint32_t* __restrict__ old_key,
+                           const double* __restrict__ old_val, uint64_t old_n, const uint64_t* __restrict__ eptr,
+                           const uint32_t* __restrict__ ekey, uint64_t e_n, uint64_t nseg,
+                           const uint64_t* __restrict__ new_ptr, uint32_t* __restrict__ new_key,
+                           double* __restrict__ new_val) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < old_n + e_n;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    if (t < old_n) {
+      const uint64_t i = t, sg = segment_of(old_ptr, nseg, i);
       const uint32_t k = old_key[i];
-      uint64_t lo = e0, hi = e1;  // number of edge keys < k
+      uint64_t lo = eptr[sg], hi = eptr[sg + 1];
+      const uint64_t e0 = lo;
       while (lo < hi) {
-        uint64_t mid = (lo + hi) >> 1;
+        const uint64_t mid = (lo + hi) >> 1;
         if (ekey[mid] < k) lo = mid + 1; else hi = mid;
       }
-      const uint64_t pos = base + (i - o0) + (lo - e0);
+      const uint64_t pos = new_ptr[sg] + (i - old_ptr[sg]) + (lo - e0);
       new_key[pos] = k;
       new_val[pos] = old_val[i];
-    }
-    for (uint64_t j = e0 + lane; j < e1; j += 32) {
+    } else {
+      const uint64_t j = t - old_n, sg = segment_of(eptr, nseg, j);
       const uint32_t k = ekey[j];
-      uint64_t lo = o0, hi = o1;  // number of old keys < k
+      uint64_t lo = old_ptr[sg], hi = old_ptr[sg + 1];
+      const uint64_t o0 = lo;
       while (lo < hi) {
-        uint64_t mid = (lo + hi) >> 1;
+        const uint64_t mid = (lo + hi) >> 1;
         if (old_key[mid] < k) lo = mid + 1; else hi = mid;
       }
-      const uint64_t pos = base + (lo - o0) + (j - e0);
+      const uint64_t pos = new_ptr[sg] + (lo - o0) + (j - eptr[sg]);
       new_key[pos] = k;
       new_val[pos] = 1.0;
     }
@@ -236,9 +251,9 @@ void merge_format(const DBuf<uint64_t>& old_ptr, const DBuf<uint32_t>& old_key, 
   out.nnz = old_nnz + n_edges;
   out.idx.alloc(out.nnz ? out.nnz : 1, s);
   out.val.alloc(out.nnz ? out.nnz : 1, s);
-  merge_segments<<<blocks_for(nseg * 32), kT, 0, s>>>(old_ptr.get(), old_key.get(), old_val.get(), eptr.get(),
-                                                      ekey.get(), nseg, out.ptr.get(), out.idx.get(),
-                                                      out.val.get());
+  merge_flat<<<blocks_for(old_nnz + n_edges), kT, 0, s>>>(old_ptr.get(), old_key.get(), old_val.get(), old_nnz,
+                                                          eptr.get(), ekey.get(), n_edges, nseg, out.ptr.get(),
+                                                          out.idx.get(), out.val.get());
   RK_LAUNCH_CHECK();
 }
 
