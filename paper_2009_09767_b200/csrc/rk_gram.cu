@@ -100,6 +100,9 @@ __global__ void sparse_gram_rows_kernel(const uint64_t* __restrict__ row_ptr, co
       if (col[mid] < b) lo = mid + 1; else hi = mid;
     }
     double* g = G + bi * stride;
+    // G(r, r) gets one product per entry: kept in a register (the same sequence of
+    // fmas from zero), so the loop carries no store -> load dependency through it
+    double diag = 0.0;
     for (uint64_t i = lo, iend = row_ptr[r + 1]; i < iend; ++i) {
       const uint32_t c = col[i];
       if (c >= e) break;
@@ -107,10 +110,15 @@ __global__ void sparse_gram_rows_kernel(const uint64_t* __restrict__ row_ptr, co
       for (uint64_t k = col_ptr[c], kend = col_ptr[c + 1]; k < kend; ++k) {
         const uint32_t sr = row_idx[k];
         if (sr > r) break;
-        double* gp = g + r + (uint64_t)sr * M;
-        *gp = fma(vr, cval[k], *gp);
+        if (sr == r) {
+          diag = fma(vr, cval[k], diag);
+        } else {
+          double* gp = g + r + (uint64_t)sr * M;
+          *gp = fma(vr, cval[k], *gp);
+        }
       }
     }
+    g[r + (uint64_t)r * M] = diag;
   }
 }
 
@@ -658,7 +666,8 @@ void sparse_gram(const DevMatrix& m, const Partition& p, uint64_t d_lo, uint64_t
     return;
   }
   // G is zero on entry (the caller's slot buffer)
-  sparse_gram_rows_kernel<<<grid_for((uint64_t)M * nblk), 256, 0, s>>>(
+  // 64 threads per CTA: one thread per (block, row) is only M x nblk threads
+  sparse_gram_rows_kernel<<<grid_for((uint64_t)M * nblk * 4), 64, 0, s>>>(
       a.ptr.get(), a.idx.get(), a.val.get(), m.csc.ptr.get(), m.csc.idx.get(), m.csc.val.get(), M, p, d_lo, nblk, G,
       stride);
   RK_LAUNCH_CHECK();
