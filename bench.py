@@ -380,6 +380,8 @@ def main():
             R.dev_outputs_free(out)
             L.rk_dev_shard_destroy(shard)
             t.merge_ms += t2.merge_ms
+            t.merge_flops += t2.merge_flops
+            t.merge_sweeps = t2.merge_sweeps
             t.recover_ms = t2.recover_ms
             t.kernel_launches += t2.kernel_launches
             return t
@@ -434,6 +436,7 @@ def main():
     stages = {k: med[k] for k in ("repair_ms", "blocks_ms", "qr_ms", "jacobi_ms", "merge_ms", "recover_ms",
                                   "total_ms")}
     stages["jacobi_sweeps_max"] = med["jacobi_sweeps_max"]
+    stages["merge_sweeps"] = med["merge_sweeps"]
     v_bytes = 8.0 * (cfg.cols // ws) * M  # this rank's V rows
     stages["recover_hbm_frac"] = (v_bytes / (med["recover_ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"] \
         if med["recover_ms"] > 0 else None
@@ -451,6 +454,7 @@ def main():
         "repair (HBM, GB/s)": frac(repair_bytes, med["repair_ms"], hbm, 1e9),
         "block factor: Gram + Cholesky / QR (FP64, TF/s)": frac(med["qr_flops"], med["qr_ms"], fp64, 1e12),
         "block Jacobi (FP64, TF/s)": frac(med["jacobi_flops"], med["jacobi_ms"], fp64, 1e12),
+        "merge: SYRK + Cholesky + Jacobi (FP64, TF/s)": frac(med["merge_flops"], med["merge_ms"], fp64, 1e12),
         "V recovery SpMM (HBM, GB/s)": frac(spmm_bytes, med["recover_ms"], hbm, 1e9),
     }
 

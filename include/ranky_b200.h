@@ -123,6 +123,10 @@ typedef struct rk_timing {
   double qr_flops;               /* algorithmic FP64 flops of the block QRs: sum 2 n_d M^2 - 2/3 M^3 */
   double jacobi_flops;           /* algorithmic FP64 flops of the block Jacobi: per block
                                     sweeps*(c(c-1)/2*2M + 2Mc) + rotations*6M, c = active columns */
+  uint64_t merge_sweeps;         /* the merge's Jacobi */
+  uint64_t merge_rotations;
+  double merge_flops;            /* algorithmic FP64 flops of the merge: Gram route M(M+1)*sum k (SYRK) +
+                                    M^3/3 (Cholesky), TSQR route 2*sum k*M^2; + its Jacobi as above */
 } rk_timing;
 
 /* PipelineResult (+ V) -- proj/include/ranky/pipeline.hpp:30-36 */

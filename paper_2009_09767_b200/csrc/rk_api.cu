@@ -382,6 +382,9 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
     t->jacobi_sweeps_sum = fr.blocks.sweeps_sum;
     t->qr_flops = fr.blocks.qr_flops;
     t->jacobi_flops = fr.blocks.jacobi_flops;
+    t->merge_sweeps = fr.merge.sweeps;
+    t->merge_rotations = fr.merge.rotations;
+    t->merge_flops = fr.merge.flops;
   }
 }
 
@@ -997,6 +1000,10 @@ void shard_outputs(Ctx& c, const DevMatrix& rep, MergeOut& mo, uint32_t flags, u
                    uint64_t col_hi, rk_dev_outputs** out, rk_timing* timing, uint64_t launches0) {
   cudaStream_t s = c.stream;
   const uint32_t M = (uint32_t)rep.csr.rows;
+  const uint64_t sweeps = mo.sweeps, rotations = mo.rotations;
+  // the finish's share of the merge flops: the top of the tree's Jacobi (+ the
+  // caller's Cholesky / combines, passed in mo.flops)
+  const double merge_flops = mo.flops + jacobi_flops_of(sweeps, rotations, M, M);
   RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
   auto o = std::make_unique<DevOutputsImpl>();
   uint32_t r = 0;
@@ -1032,6 +1039,9 @@ void shard_outputs(Ctx& c, const DevMatrix& rep, MergeOut& mo, uint32_t flags, u
     timing->recover_ms = elapsed(c.ev[4], c.ev[5]);
     timing->total_ms = elapsed(c.ev[3], c.ev[5]);
     timing->kernel_launches = c.launches - launches0;
+    timing->merge_sweeps = sweeps;
+    timing->merge_rotations = rotations;
+    timing->merge_flops = merge_flops;
   }
   *out = &o.release()->pub;
 }
@@ -1101,6 +1111,7 @@ rk_status rk_dev_shard_finish_gram(rk_ctx* ctx, rk_dev_shard* shard, const doubl
     if (!gram_merge(c, W, M, mo))
       fail(RK_GRAM_REJECTED, "the kappa guard rejected the merge's Gram route: rk_dev_shard_tsqr, all-gather, "
                              "rk_dev_shard_finish");
+    mo.flops = (double)M * M * M / 3.0;  // the Cholesky of the summed Gram (its Jacobi: shard_outputs)
     shard_outputs(c, rep, mo, flags, top_k, col_lo, col_hi, out, timing, launches0);
   });
 }

@@ -727,6 +727,11 @@ void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut
   merge_jacobi(c, W, M, M, cp, out);
 }
 
+double jacobi_flops_of(uint64_t sweeps, uint64_t rotations, uint32_t rows, uint32_t cols) {
+  const double c = cols, m = rows;
+  return (double)sweeps * (c * (c - 1) / 2 * 2 * m + 2 * m * c) + (double)rotations * 6 * m;
+}
+
 bool gram_merge_eligible(uint32_t M) { return gram_route_enabled() && M <= cholesky_max_rows() && M % 8 == 0; }
 
 // Gram route of the merge: W holds P P^T (M x cols_pad slot); R_P^T = chol(P P^T),
@@ -788,12 +793,17 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
       prof_mark(s, "mrg alloc");
       records_gram(payload, offset, kept, M, W.get(), s);
       prof_mark(s, "mrg syrk");
-      if (gram_merge(c, W, M, out)) return;
+      if (gram_merge(c, W, M, out)) {
+        const double Md = M;
+        out.flops = Md * (Md + 1) * (double)total + Md * Md * Md / 3.0 + jacobi_flops_of(out.sweeps, out.rotations, M, M);
+        return;
+      }
     }
     std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
     std::vector<DBuf<double>> roots(1);
     merge_subtree(c, payload, offset, kept, M, leaves, 0, leaves.size(), roots[0]);
     merge_finish(c, roots, M, out);
+    out.flops = 2.0 * (double)total * M * (double)M + jacobi_flops_of(out.sweeps, out.rotations, M, M);
     return;
   }
   // P^T is not taller than wide: Jacobi straight on P's columns (W = P)

@@ -33,6 +33,7 @@ struct MergeOut {
   DBuf<double> sigma;      // k, descending
   DBuf<double> u;          // M x k row-major, sign convention applied
   uint64_t sweeps = 0, rotations = 0;
+  double flops = 0.0;      // algorithmic FP64 flops (rk_timing::merge_flops)
 };
 
 // TSQR over a forest: every tree's leaves (column-major, factored in place) are
@@ -64,6 +65,8 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
 // the merge's Gram route (see merge_records): eligibility, and the finish from
 // W = P P^T (M x jacobi_cols_pad slot, consumed); false when the kappa guard rejects
 bool gram_merge_eligible(uint32_t M);
+// the reference-algorithm flop count of a Jacobi run (rk_timing::jacobi_flops)
+double jacobi_flops_of(uint64_t sweeps, uint64_t rotations, uint32_t rows, uint32_t cols);
 bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out);
 
 // dense_svd on the device: a is rows x cols row-major (device). Outputs row-major.

@@ -147,7 +147,8 @@ class Timing(C.Structure):
                 ("recover_ms", C.c_double), ("total_ms", C.c_double), ("qr_ms", C.c_double),
                 ("jacobi_ms", C.c_double), ("jacobi_sweeps_max", C.c_uint64), ("jacobi_rotations", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("jacobi_sweeps_sum", C.c_uint64), ("qr_flops", C.c_double),
-                ("jacobi_flops", C.c_double)]
+                ("jacobi_flops", C.c_double), ("merge_sweeps", C.c_uint64), ("merge_rotations", C.c_uint64),
+                ("merge_flops", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
