@@ -332,6 +332,15 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   cudaStream_t s = c.stream;
   const uint64_t launches0 = c.launches;
   cudaEvent_t ev0 = c.ev[3], ev1 = c.ev[4], ev2 = c.ev[5], ev3 = c.ev[6], ev4 = c.ev[7];
+  // V (the largest buffer: N x r doubles, 137 GB at c4) is taken from the pool
+  // first, sized for the largest r (= min(M, top_k)), while the previous call's
+  // block is still whole; allocated after the block stage and the merge it often
+  // found the pool fragmented and had to trim and map it again (c4: 0.1-0.4 s)
+  if (flags & RK_WANT_V) {
+    const uint64_t M = a.csr.rows;
+    const uint64_t rmax = std::max<uint64_t>(1, top_k ? std::min<uint64_t>(top_k, M) : M);
+    fr.v.alloc(a.csr.cols * rmax, s);
+  }
   RK_CUDA_CHECK(cudaEventRecord(ev0, s));
   prof_mark(s, "start");
   fr.repaired = repair_and_apply(c, a, p, method, seed, fr.rep);
@@ -354,7 +363,8 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
     sync(s);
     std::vector<uint32_t> ret = retained_of(sig.data(), kk, 1e-10);
     fr.r = (uint32_t)ret.size();
-    fr.v.alloc(rep.csc.cols * (uint64_t)std::max<uint32_t>(fr.r, 1), s);
+    if (fr.v.n < rep.csc.cols * (uint64_t)std::max<uint32_t>(fr.r, 1))
+      fr.v.alloc(rep.csc.cols * (uint64_t)std::max<uint32_t>(fr.r, 1), s);
     if (fr.r) {
       DBuf<uint32_t> dret(fr.r, s);
       to_device(dret.get(), ret.data(), ret.size(), s);
