@@ -332,11 +332,13 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   cudaStream_t s = c.stream;
   const uint64_t launches0 = c.launches;
   cudaEvent_t ev0 = c.ev[3], ev1 = c.ev[4], ev2 = c.ev[5], ev3 = c.ev[6], ev4 = c.ev[7];
-  // V (the largest buffer: N x r doubles, 137 GB at c4) is taken from the pool
-  // first, sized for the largest r (= min(M, top_k)), while the previous call's
-  // block is still whole; allocated after the block stage and the merge it often
-  // found the pool fragmented and had to trim and map it again (c4: 0.1-0.4 s)
-  if (flags & RK_WANT_V) {
+  // A full V (N x M doubles, 137 GB at c4: by far the call's largest buffer) is
+  // taken from the pool first, while the previous call's block is still whole;
+  // allocated after the block stage and the merge it often found the pool
+  // fragmented and had to trim and map it again (c4: 0.1-0.4 s). With top_k (c5:
+  // N x 64) it stays where it was: allocated early it only shrinks the block
+  // stage's staging budget (c5 QR 98 -> 112 s)
+  if ((flags & RK_WANT_V) && top_k == 0) {
     const uint64_t M = a.csr.rows;
     const uint64_t rmax = std::max<uint64_t>(1, top_k ? std::min<uint64_t>(top_k, M) : M);
     fr.v.alloc(a.csr.cols * rmax, s);
