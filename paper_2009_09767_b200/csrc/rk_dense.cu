@@ -1073,7 +1073,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
 // finalize
 // ===========================================================================
 
-constexpr int kFThreads = 512;
+constexpr int kFThreads = 1024;
 // finalize_kernel leaves the output columns' flags in the high bits of order[j]
 constexpr uint32_t kOrderFlip = 0x80000000u, kOrderDef = 0x40000000u, kOrderSrc = 0x3fffffffu;
 
