@@ -141,6 +141,12 @@ typedef struct rk_pipeline_result {
 /* ---- errors & context ---------------------------------------------------- */
 RK_API const char* rk_last_error(void);
 RK_API double rk_last_residual(void);
+/* Re-read the RK_* tuning/debug environment switches (read once per process
+ * otherwise). Not thread-safe against calls in flight. */
+RK_API void rk_reload_tuning(void);
+/* Build flags: bit 0 = experiments build (RK_EXPERIMENTS: the measured-and-not-kept
+ * variants RK_PRECOND, RK_CHOL=r, RK_GRAM_PAIRS are compiled in). */
+RK_API uint32_t rk_build_flags(void);
 RK_API int32_t rk_abi_version(void);
 
 typedef struct rk_ctx rk_ctx;

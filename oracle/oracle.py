@@ -238,6 +238,24 @@ class Oracle:
                                                          self._p(flat, C.c_double)))
 
 
+    def sampled_pipeline(self, a, D, method, keep, seed, workers, sample, slice_cols, phase) -> np.ndarray:
+        """ref_sampled_pipeline (reference only): per-stage std::chrono times of the
+        reference's run_pipeline stages on a block sample (see ref_capi.cpp)."""
+        rows, cols, r, c, v = self._coo(a)
+        fn = self.lib.ref_sampled_pipeline
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                       C.POINTER(C.c_double), C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                       C.POINTER(C.c_uint64), C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+        smp = np.ascontiguousarray(sample, dtype=np.uint64)
+        t = np.zeros(8)
+        st = fn(rows, cols, len(r), self._p(r, C.c_uint64), self._p(c, C.c_uint64), self._p(v, C.c_double), D,
+                METHODS[method], keep, seed, workers, self._p(smp, C.c_uint64), len(smp), slice_cols, phase,
+                self._p(t, C.c_double))
+        if st:
+            raise OracleError(4, f"ref_sampled_pipeline failed ({st})")
+        return t
+
     # ---- RNKY records (reference only): block_record.cpp:53-144 ----
     def crc32(self, data: bytes) -> int:
         self.lib.ref_crc32.restype = C.c_uint32

@@ -5,8 +5,11 @@
 // the same or_result record as the C restatement so tests can run both
 // oracles -- and the CUDA path -- on identical inputs. It adds no arithmetic
 // of its own: every number comes from the reference routines named below.
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
+#include <thread>
 #include <exception>
 #include <stdexcept>
 #include <vector>
@@ -314,6 +317,88 @@ int ref_read_block_record(const char* path, uint32_t* index, uint32_t* rows, uin
     return 0;
   } catch (const RecordError&) {
     return 1;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+// ---- the reference arm's bounded sample (bench.py --impl reference) ----------
+// run_pipeline (proj/src/pipeline.cpp:61-121) + recover_right_vectors
+// (proj/src/proxy.cpp:48-72) are serial except the block-task pool, so their
+// time is the sum of the stages below. Each stage calls the reference's own
+// functions and is timed here with std::chrono around those calls only (no
+// marshalling inside the timed regions). phase selects what runs:
+//   phase & 1: repair in full (pipeline.cpp:70) ............ t[0]
+//   phase & 2: block_view of the n sampled blocks .......... t[1]  (pipeline.cpp:73-75)
+//              run_block_task over them on min(workers, n) threads pulling from an
+//              atomic, as pipeline.cpp:79-101 does ........ t[2]
+//   phase & 4: proxy_from_records + proxy_svd on the first n/2 and on all n
+//              sampled records (proj/src/pipeline.cpp:18-59, proxy.cpp:40-46) ... t[3], t[4]
+//              recover_right_vectors of the repaired matrix's first slice_cols
+//              columns with that proxy's U, sigma ............................... t[5]
+// t[6] = sum of the kept sigma count of the full-n proxy (its Σk), t[7] = the n/2 one's.
+int ref_sampled_pipeline(uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* r, const uint64_t* c,
+                         const double* v, uint64_t D, int method, uint64_t keep, uint64_t seed, uint64_t workers,
+                         const uint64_t* sample, uint64_t n, uint64_t slice_cols, int phase, double* t) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  try {
+    SparseMatrix a = make_sparse(rows, cols, nnz, r, c, v);
+    BlockPartition p = partition_columns(a.cols(), D);
+    auto t0 = clk::now();
+    auto [repaired, report] = repair(a, p, method_of(method), seed);
+    auto t1 = clk::now();
+    if (phase & 1) t[0] = secs(t0, t1);
+    if (!(phase & 6)) return 0;
+    std::vector<BlockTask> tasks;
+    t0 = clk::now();
+    for (uint64_t i = 0; i < n; ++i) tasks.push_back({sample[i], block_view(repaired, p, sample[i]), keep});
+    t1 = clk::now();
+    t[1] = secs(t0, t1);
+    std::vector<BlockResultRecord> recs(n);
+    std::atomic<std::size_t> next{0};
+    auto loop = [&] {
+      for (;;) {
+        const std::size_t i = next.fetch_add(1);
+        if (i >= n) return;
+        recs[i] = run_block_task(tasks[i]);
+      }
+    };
+    const std::size_t pool = std::min<uint64_t>(workers, n);
+    t0 = clk::now();
+    {
+      std::vector<std::thread> th;
+      for (std::size_t i = 0; i < pool; ++i) th.emplace_back(loop);
+      for (auto& x : th) x.join();
+    }
+    t1 = clk::now();
+    t[2] = secs(t0, t1);
+    if (!(phase & 4)) return 0;
+    for (std::size_t i = 0; i < n; ++i) recs[i].block_index = static_cast<uint32_t>(i);
+    const std::size_t half = std::max<std::size_t>(1, n / 2);
+    double sk_half = 0, sk_all = 0;
+    for (std::size_t i = 0; i < n; ++i) (i < half ? sk_half : sk_all) += recs[i].kept;
+    sk_all += sk_half;
+    t0 = clk::now();
+    SvdResult s_half = proxy_svd(proxy_from_records(std::span<const BlockResultRecord>(recs.data(), half), rows));
+    t1 = clk::now();
+    t[4] = secs(t0, t1);
+    t0 = clk::now();
+    SvdResult s_all = proxy_svd(proxy_from_records(recs, rows));
+    t1 = clk::now();
+    t[3] = secs(t0, t1);
+    t[6] = sk_all;
+    t[7] = sk_half;
+    const uint64_t sc = std::min<uint64_t>(slice_cols, cols);
+    std::vector<Entry> es;
+    for (const Entry& e : repaired.entries())
+      if (e.col < sc) es.push_back(e);
+    SparseMatrix slice(rows, sc, std::move(es));
+    t0 = clk::now();
+    DenseMatrix vm = recover_right_vectors(slice, s_all.u, s_all.sigma, kRankTol);
+    t1 = clk::now();
+    t[5] = secs(t0, t1);
+    return vm.rows() == sc ? 0 : 1;
   } catch (const std::exception&) {
     return 2;
   }

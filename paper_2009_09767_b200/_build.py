@@ -50,7 +50,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _needs(o, [s] + headers):
-            cmd = [cc, *ARCH, *FLAGS, *os.environ.get("RK_NVCC_EXTRA", "").split(), "-I", os.path.join(ROOT, "include"),
+            exp = ["-DRK_EXPERIMENTS"] if os.environ.get("RK_EXPERIMENTS") == "1" else []
+            cmd = [cc, *ARCH, *FLAGS, *exp, *os.environ.get("RK_NVCC_EXTRA", "").split(), "-I", os.path.join(ROOT, "include"),
                    "-I", CSRC, "-c", s, "-o", o]
             jobs.append(cmd)
     def run(cmd):

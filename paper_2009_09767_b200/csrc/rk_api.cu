@@ -1,5 +1,6 @@
 // rk_api.cu -- the C ABI (include/ranky_b200.h): argument checks with the
 // reference's messages, exception -> status mapping, host <-> device marshaling.
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -8,6 +9,8 @@
 #include <memory>
 #include <mutex>
 #include <unordered_map>
+
+#include <unistd.h>
 
 #include "rk_pipeline.cuh"
 
@@ -23,12 +26,59 @@ void trim_pool(cudaStream_t s) {
   cudaGetLastError();
 }
 
+namespace {
+Tuning read_tuning() {
+  Tuning t;
+  auto flag = [](const char* name, char on) {
+    const char* e = std::getenv(name);
+    return e && e[0] == on;
+  };
+  auto num = [](const char* name, double def) {
+    const char* e = std::getenv(name);
+    return e ? std::strtod(e, nullptr) : def;
+  };
+  t.trace = flag("RK_TRACE", '1');
+  t.hostprof = flag("RK_HOSTPROF", '1');
+  t.meminfo_exact = flag("RK_MEMINFO", 'x');
+  t.jacobi_gmax = (int)std::max(2.0, std::min(32.0, num("RK_JACOBI_GMAX", 16))) & ~1;
+  t.jacobi_single_g = (int)num("RK_JACOBI_SINGLE_G", 8);
+  if (const char* e = std::getenv("RK_JACOBI_WARP")) t.jacobi_warp = e[0] == '1' ? 1 : 0;
+  t.jacobi_check = num("RK_JACOBI_CHECK", -1.0);
+  t.jacobi_cluster = (int)num("RK_JACOBI_CLUSTER", 0);
+  t.jacobi_debug = std::getenv("RK_JACOBI_DEBUG") != nullptr;
+  t.jacobi_q = (int)num("RK_JACOBI_Q", 0);
+  t.jacobi_unroll = !flag("RK_JACOBI_UNROLL", '0');
+  t.gram_pairs = flag("RK_GRAM_PAIRS", '1');
+  t.diag_order = !flag("RK_DIAG_ORDER", '0');
+  t.chol_right = flag("RK_CHOL", 'r');
+  if (const char* e = std::getenv("RK_BLOCK_ROUTE")) t.householder_only = std::string(e) == "householder";
+  t.precond = flag("RK_PRECOND", '1');
+  t.precond_stop = (float)num("RK_PRECOND_STOP", 1e-5);
+  t.spmm_warp = flag("RK_SPMM_WARP", '1');
+  return t;
+}
+std::mutex g_tuning_mu;
+Tuning g_tuning = read_tuning();
+std::atomic<int> g_sms[64];
+}  // namespace
+
+const Tuning& tuning() { return g_tuning; }
+void reload_tuning() {
+  std::lock_guard<std::mutex> lk(g_tuning_mu);
+  g_tuning = read_tuning();
+}
+int device_sms(int device) {
+  if (device < 0 || device >= 64) fail(RK_INVALID_ARGUMENT, "device index");
+  int v = g_sms[device].load(std::memory_order_relaxed);
+  if (!v) {
+    RK_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    g_sms[device].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 void trace_launch(const char* file, int line) {
-  static const bool on = [] {
-    const char* e = std::getenv("RK_TRACE");
-    return e && e[0] == '1';
-  }();
-  if (!on) return;
+  if (!tuning().trace) return;
   const auto t0 = std::chrono::steady_clock::now();
   const cudaError_t e = cudaDeviceSynchronize();
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -43,13 +93,7 @@ struct ProfMark {
   cudaEvent_t ev;
 };
 thread_local std::vector<ProfMark> g_prof;
-bool prof_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("RK_HOSTPROF");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+bool prof_on() { return tuning().hostprof; }
 }  // namespace
 
 void prof_mark(cudaStream_t s, const char* name) {
@@ -81,10 +125,7 @@ size_t device_free_bytes(Ctx& c, uint64_t want) {
                          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
                          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess;
   cudaGetLastError();
-  static const bool exact = [] {
-    const char* e = std::getenv("RK_MEMINFO");
-    return e && e[0] == 'x';
-  }();
+  const bool exact = tuning().meminfo_exact;
   if (have_pool && c.free_known && !exact) {
     // free now = free0 - (reserved - reserved0); the pool's reserved-but-unused part is ours too
     const int64_t est = (int64_t)c.free0 + (int64_t)c.reserved0 - (int64_t)used;
@@ -190,7 +231,16 @@ std::mutex g_pinned_mu;
 std::unordered_map<void*, size_t> g_pinned;          // live pinned buffers -> bytes
 std::unordered_multimap<size_t, void*> g_pinned_free;  // cached for reuse
 size_t g_pinned_cached = 0;
-constexpr size_t kPinnedCacheMax = size_t(8) << 30;
+// up to a third of physical memory (at most 64 GiB): c3's full result (16 GiB of V +
+// 1 GiB of records) is reused call after call instead of page-locked afresh each time
+size_t pinned_cache_max() {
+  static const size_t cap = [] {
+    const long pages = sysconf(_SC_PHYS_PAGES), page = sysconf(_SC_PAGE_SIZE);
+    const size_t phys = pages > 0 && page > 0 ? (size_t)pages * (size_t)page : (size_t(24) << 30);
+    return std::min<size_t>(size_t(64) << 30, phys / 3);
+  }();
+  return cap;
+}
 
 template <class T>
 T* host_alloc(size_t n) {
@@ -225,7 +275,7 @@ void host_free(void* p) {
     if (it != g_pinned.end()) {
       const size_t bytes = it->second;
       g_pinned.erase(it);
-      if (g_pinned_cached + bytes <= kPinnedCacheMax) {
+      if (g_pinned_cached + bytes <= pinned_cache_max()) {
         g_pinned_free.emplace(bytes, p);
         g_pinned_cached += bytes;
       } else {
@@ -408,6 +458,14 @@ extern "C" {
 
 const char* rk_last_error(void) { return g_error.c_str(); }
 double rk_last_residual(void) { return g_residual; }
+void rk_reload_tuning(void) { reload_tuning(); }
+uint32_t rk_build_flags(void) {
+#ifdef RK_EXPERIMENTS
+  return 1u;
+#else
+  return 0u;
+#endif
+}
 int32_t rk_abi_version(void) { return RK_ABI_VERSION; }
 
 rk_status rk_ctx_create(int32_t device, rk_ctx** out) {

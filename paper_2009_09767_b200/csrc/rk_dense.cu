@@ -1358,11 +1358,7 @@ size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v);
 void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, uint32_t& g, uint32_t& G) {
   // largest even group size (<= gcap) whose two staged groups fit the budget; a
   // smaller cap trades longer tournaments for more CTAs per SM (latency hiding)
-  const uint32_t gcap = [] {
-    const char* e = std::getenv("RK_JACOBI_GMAX");
-    const long v = e ? std::strtol(e, nullptr, 10) : 16;
-    return (uint32_t)std::max<long>(2, std::min<long>(32, v & ~1L));
-  }();
+  const uint32_t gcap = (uint32_t)tuning().jacobi_gmax;
   // columns longer than 16 lanes x 32 registers: 8 groups of 32 lanes keep the A
   // column in registers (E <= 32); without the cap the plan falls back to the
   // shared-memory rounds (E = 0), several times slower
@@ -1400,8 +1396,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // pair (shorter dot and update chains per round), up to 16 CTAs per matrix
   unsigned max_cluster = 8;
   if (latency && jobs.size() == 1 && !with_v) {
-    const char* ge = std::getenv("RK_JACOBI_SINGLE_G");
-    const uint32_t g1 = ge ? (uint32_t)std::strtoul(ge, nullptr, 10) : 8u;
+    const uint32_t g1 = (uint32_t)tuning().jacobi_single_g;
     if (g1 >= 2 && g1 % 2 == 0 && g1 < g && cols_pad % g1 == 0 && (cols_pad / g1) % 2 == 0 && rows <= 32u * 32u) {
       g = g1;
       G = cols_pad / g1;
@@ -1421,12 +1416,11 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // blocks (7.30 vs 7.23 ms) and is 2x slower on a single matrix (the L2 latency of
   // streaming X twice per step is not hidden at 8 warps per SM). RK_JACOBI_WARP=0/1
   // forces it off/on.
-  const char* we = std::getenv("RK_JACOBI_WARP");
+  const Tuning& tn = tuning();
   const bool warp_default = rows >= 512 && !latency;  // a function of the shape only (see latency)
-  bool use_warp = (we ? we[0] == '1' : warp_default) && !with_v && cols_pad % 16 == 0;
+  bool use_warp = (tn.jacobi_warp >= 0 ? tn.jacobi_warp == 1 : warp_default) && !with_v && cols_pad % 16 == 0;
   if (use_warp) {
-    const char* ce0 = std::getenv("RK_JACOBI_CHECK");
-    WarpParams WP{nullptr, cols_pad / kWG, ce0 ? std::strtod(ce0, nullptr) : 1e-7};
+    WarpParams WP{nullptr, cols_pad / kWG, tn.jacobi_check >= 0 ? tn.jacobi_check : 1e-7};
     DBuf<JacobiJob> djw(jobs.size(), s);
     to_device(djw.get(), jobs.data(), jobs.size(), s);
     WP.jobs = djw.get();
@@ -1443,13 +1437,12 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
   cl = p2;
-  if (const char* ce2 = std::getenv("RK_JACOBI_CLUSTER")) {  // tuning override
-    const unsigned v = (unsigned)std::strtoul(ce2, nullptr, 10);
+  if (tn.jacobi_cluster) {  // tuning override
+    const unsigned v = (unsigned)tn.jacobi_cluster;
     if (v >= 1 && v <= 16 && v <= G / 2) cl = v;
   }
   DBuf<JacobiJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
-  const char* ce = std::getenv("RK_JACOBI_CHECK");
   // the convergence check (tail_check) takes over once a sweep's max ratio is
   // below check_ratio. Measured on c2: batched blocks 6.41 ms at 1e-7, 6.07 ms
   // anywhere in 3e-6 .. 1e-4 (one full sweep fewer; a check that finds too many
@@ -1457,15 +1450,15 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // merge is best at 1e-7 (1.71 vs 1.76 ms). A check certifies with the
   // reference's rule whatever the threshold.
   const double check_default = latency ? 1e-7 : 1e-5;
-  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, ce ? std::strtod(ce, nullptr) : check_default, use_warp ? 1 : 0,
-                 std::getenv("RK_JACOBI_DEBUG") ? 1 : 0};
+  JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, tn.jacobi_check >= 0 ? tn.jacobi_check : check_default,
+                 use_warp ? 1 : 0, tn.jacobi_debug ? 1 : 0};
   void* kargs[] = {&P};
   // lanes per pair: enough lane groups for the g pairs of a round; E = column
   // elements per lane held in registers by the cross rounds (0: shared-memory path)
   int Q = 32;
   while (Q > 8 && (kJThreads / Q) < (int)g) Q /= 2;
-  if (const char* qe = std::getenv("RK_JACOBI_Q")) {  // tuning override (must give >= g lane groups)
-    const int qv = (int)std::strtol(qe, nullptr, 10);
+  if (tn.jacobi_q) {  // tuning override (must give >= g lane groups)
+    const int qv = tn.jacobi_q;
     if ((qv == 8 || qv == 16 || qv == 32) && kJThreads / qv >= (int)g) Q = qv;
   }
   int E = 1;
@@ -1494,8 +1487,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
     case 32: exact ? launch(jacobi_cluster_kernel<QQ, 32, true>) : launch(jacobi_cluster_kernel<QQ, 32, false>); break; \
     default: launch(jacobi_cluster_kernel<QQ, 0, false>); break;                       \
   }
-  const char* ue = std::getenv("RK_JACOBI_UNROLL");
-  const bool unroll = !(ue && ue[0] == '0');
+  const bool unroll = tn.jacobi_unroll;
   if (unroll && Q == 16 && E == 16 && exact && g == 16) {
     launch(jacobi_cluster_kernel<16, 16, true, 16>);  // c2's blocks: compile-time group count
   } else if (unroll && Q == 32 && E == 8 && exact && g == 8) {

@@ -32,6 +32,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+#ifdef RK_EXPERIMENTS  // not kept (measured): the row-pair merge-join Gram, RK_GRAM_PAIRS=1
 // one thread per (block, r >= s) pair: G[r + s M] = G[s + r M] = sum_c A[r,c] A[s,c]
 __global__ void sparse_gram_kernel(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
                                    const double* __restrict__ val, uint32_t M, Partition p, uint64_t d_lo,
@@ -74,6 +75,7 @@ __global__ void sparse_gram_kernel(const uint64_t* __restrict__ row_ptr, const u
     g[s + (uint64_t)r * M] = acc;
   }
 }
+#endif  // RK_EXPERIMENTS
 
 // The same Gram from the other side: one thread per (block, row r). Row r's block
 // entries are visited in ascending column c; for each, the column's entries in
@@ -266,6 +268,7 @@ __global__ void diag_gather_kernel(const double* __restrict__ G, uint64_t stride
 
 constexpr int kCT = 256;
 
+#ifdef RK_EXPERIMENTS  // not kept (measured): the right-looking kernel, RK_CHOL=r
 // kCB: panel width (32; 16 for tall matrices, so the M x kCB panel fits shared memory)
 template <int kCB>
 __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restrict__ mats, uint32_t M,
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(kCT, 1) cholesky_kernel(double* const* __restr
     diag_ratio[blockIdx.x] = s_bad ? INFINITY : s_dmax / s_dmin;
   }
 }
+#endif  // RK_EXPERIMENTS
 
 // the nb x nb diagonal block at P (column-major, ld ldp) factored in place by one
 // warp: lane i holds row i in registers. FP64 latency sets the speed here (DFMA
@@ -657,14 +661,15 @@ void sparse_gram(const DevMatrix& m, const Partition& p, uint64_t d_lo, uint64_t
   const DevCsr& a = m.csr;
   const uint32_t M = (uint32_t)a.rows;
   if (!M || !nblk) return;
-  const char* e = std::getenv("RK_GRAM_PAIRS");
-  if (e && e[0] == '1') {  // the row-pair merge-join kernel (A/B)
+#ifdef RK_EXPERIMENTS
+  if (tuning().gram_pairs) {  // the row-pair merge-join kernel (A/B; experiments build)
     const uint64_t total = (uint64_t)M * (M + 1) / 2 * nblk;
     sparse_gram_kernel<<<grid_for(total), 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), M, p, d_lo, nblk, G,
                                                        stride);
     RK_LAUNCH_CHECK();
     return;
   }
+#endif
   // G is zero on entry (the caller's slot buffer)
   // 64 threads per CTA: one thread per (block, row) is only M x nblk threads
   sparse_gram_rows_kernel<<<grid_for((uint64_t)M * nblk * 4), 64, 0, s>>>(
@@ -717,10 +722,7 @@ void diag_order(const double* G, uint64_t stride, uint32_t M, uint64_t nb, uint3
   RK_LAUNCH_CHECK();
 }
 
-bool diag_order_enabled() {
-  const char* e = std::getenv("RK_DIAG_ORDER");
-  return !(e && e[0] == '0');
-}
+bool diag_order_enabled() { return tuning().diag_order; }
 
 void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s) {
   const uint64_t mm = (uint64_t)M * M;
@@ -784,6 +786,7 @@ void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, 
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
                       cudaStream_t s) {
   if (!n_mats) return;
+#ifdef RK_EXPERIMENTS
   auto launch = [&](auto kern, int cb) {
     const size_t smem = ((size_t)cb * cb + (size_t)M * cb) * sizeof(double);
     if (smem > 200 * 1024) fail(RK_RUNTIME, "cholesky_batched: M too large for the panel buffer");
@@ -792,8 +795,10 @@ void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32
     kern<<<n_mats, kCT, smem, s>>>(d_mats, M, d_status, d_ratio);
     RK_LAUNCH_CHECK();
   };
-  const char* ce = std::getenv("RK_CHOL");
-  const bool ll = !(ce && ce[0] == 'r');  // RK_CHOL=r: the right-looking kernel (A/B)
+  const bool ll = !tuning().chol_right;  // RK_CHOL=r: the right-looking kernel (A/B; experiments build)
+#else
+  const bool ll = true;
+#endif
   auto launch_ll = [&](auto kern, int cb) {
     const size_t smem = (size_t)ll_ld<16>(M) * cb * sizeof(double);
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -809,19 +814,23 @@ void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32
     launch_ll(cholesky_ll_kernel<16, 16>, 16);
   } else if (ll && M <= 1280) {
     launch_ll(cholesky_ll_kernel<16, 20>, 16);
-  } else if (M <= 640) {
+  }
+#ifdef RK_EXPERIMENTS
+  else if (M <= 640) {
     launch(cholesky_kernel<32>, 32);
   } else {
     launch(cholesky_kernel<16>, 16);
   }
+#else
+  else {
+    fail(RK_RUNTIME, "cholesky_batched: M above the panel cap");
+  }
+#endif
 }
 
 uint32_t cholesky_max_rows() { return 1280; }  // the panel buffer (M x 16 doubles) must fit shared memory
 
-bool gram_route_enabled() {
-  const char* e = std::getenv("RK_BLOCK_ROUTE");
-  return !(e && std::string(e) == "householder");
-}
+bool gram_route_enabled() { return !tuning().householder_only; }
 
 double kappa_max(uint32_t M) {
   // every sigma moves by < 1e-11 relative when M eps kappa^2 / 2 < 1e-11

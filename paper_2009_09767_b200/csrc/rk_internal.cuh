@@ -38,6 +38,34 @@ struct Error : std::runtime_error {
 // can report how many of its kernels ran (bench.py "gpu_launches")
 extern thread_local uint64_t* g_launch_counter;
 // RK_TRACE=1: synchronize after every launch and log it to stderr (debugging hangs)
+// Tuning and debug switches (RK_* environment variables).
+// Read once per process on first use -- never on the hot path -- and re-read only by
+// rk_reload_tuning() (tests flip them; no other API call may be in flight then).
+// Defaults are the measured best.
+struct Tuning {
+  bool trace = false;             // RK_TRACE=1: synchronise and log every launch
+  bool hostprof = false;          // RK_HOSTPROF=1: host/device segment times
+  bool meminfo_exact = false;     // RK_MEMINFO=x: cudaMemGetInfo on every budget query
+  int jacobi_gmax = 16;           // RK_JACOBI_GMAX: group-size cap
+  int jacobi_single_g = 8;        // RK_JACOBI_SINGLE_G: the merge's group size
+  int jacobi_warp = -1;           // RK_JACOBI_WARP=0/1 (-1: by shape)
+  double jacobi_check = -1.0;     // RK_JACOBI_CHECK: tail-check ratio (<0: by workload; 0 off)
+  int jacobi_cluster = 0;         // RK_JACOBI_CLUSTER: cluster size override (0: planned)
+  bool jacobi_debug = false;      // RK_JACOBI_DEBUG=1
+  int jacobi_q = 0;               // RK_JACOBI_Q: lanes per pair override (0: planned)
+  bool jacobi_unroll = true;      // RK_JACOBI_UNROLL=0: no compile-time group counts
+  bool gram_pairs = false;        // RK_GRAM_PAIRS=1: row-pair Gram kernel (experiments build)
+  bool diag_order = true;         // RK_DIAG_ORDER=0: no descending-diagonal ordering
+  bool chol_right = false;        // RK_CHOL=r: right-looking Cholesky (experiments build)
+  bool householder_only = false;  // RK_BLOCK_ROUTE=householder: no Gram route
+  bool precond = false;           // RK_PRECOND=1: FP32-preconditioned Jacobi (experiments build)
+  float precond_stop = 1e-5f;     // RK_PRECOND_STOP
+  bool spmm_warp = false;         // RK_SPMM_WARP=1: warp-per-column V SpMM
+};
+const Tuning& tuning();
+void reload_tuning();
+int device_sms(int device);  // cached per device
+
 void trace_launch(const char* file, int line);
 #define RK_LAUNCH_CHECK()                                                                    \
   do {                                                                                      \

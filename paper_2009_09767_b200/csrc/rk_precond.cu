@@ -26,6 +26,10 @@
 // A numpy replay on c2 blocks (tournament order): 10 FP64 sweeps directly vs 8
 // FP32 sweeps + 2 FP64 sweeps + the check, sigma within 7e-14 of LAPACK.
 // The GEMMs (steps 2-4, n x n x n each) run on the FP64 tensor cores (DMMA).
+// Measured and not kept: compiled only in the experiments build
+// (RK_EXPERIMENTS=1 python -m paper_2009_09767_b200._build --force).
+#include "rk_internal.cuh"
+#ifdef RK_EXPERIMENTS
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -462,8 +466,7 @@ bool precondition_eligible(const JacobiJob& j) {
   // ones -- a round is bound by its dependent chain (shuffle reduction, angle,
   // barrier), not by the FP64 latency of its arithmetic -- so the FP64 sweeps it
   // saves (12 -> 5) do not pay for it and the GEMMs (blocks 7.1 -> 8.6 ms)
-  const char* e = std::getenv("RK_PRECOND");
-  if (!(e && e[0] == '1')) return false;
+  if (!tuning().precond) return false;
   return j.gram_ok && j.v == nullptr && j.rows == j.cols && j.cols == j.cols_pad && j.rows % 64 == 0 &&
          j.rows >= 64 && j.rows <= 512;
 }
@@ -502,9 +505,7 @@ void precondition_fp32(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, si
   unsigned p2 = 1;
   while (p2 * 2 <= cl) p2 *= 2;
   cl = p2;
-  const char* se = std::getenv("RK_PRECOND_STOP");
-  J32Params P{dj.get(), n, n, g, G, se ? (float)std::strtod(se, nullptr) : 1e-5f, 20,
-              std::getenv("RK_JACOBI_DEBUG") ? 1 : 0};
+  J32Params P{dj.get(), n, n, g, G, tuning().precond_stop, 20, tuning().jacobi_debug ? 1 : 0};
   void* kargs[] = {&P};
   auto launch = [&](auto kern) {
     RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -544,3 +545,9 @@ void precondition_fp32(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, si
 }
 
 }  // namespace rk
+#else
+namespace rk {
+bool precondition_eligible(const JacobiJob&) { return false; }
+void precondition_fp32(std::vector<JacobiJob>&, cudaStream_t, int, size_t, uint32_t, uint32_t, int) {}
+}  // namespace rk
+#endif  // RK_EXPERIMENTS

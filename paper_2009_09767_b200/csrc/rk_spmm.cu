@@ -156,16 +156,16 @@ void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const u
   unsigned g1 = (unsigned)std::min<uint64_t>(ceil_div(tot ? tot : 1, 256), 65535);
   gather_u<<<g1, 256, 0, s>>>(u, (uint32_t)a.rows, u_cols, retained, r, sigma, u_ret.get(), inv.get());
   RK_LAUNCH_CHECK();
-  int dev = 0, sms = 148;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms(dev);
   const uint64_t cols = col_hi - col_lo;
   unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(cols * 32, 256), (uint64_t)sms * 16);
   if (grid == 0) grid = 1;
-  const char* se = std::getenv("RK_SPMM_WARP");
+
   // half a warp per column up to r = 256 (at r = 512 its 32 double2 accumulators
   // per lane cost occupancy: c3 9.3 ms vs 3.9 ms for the warp-per-column kernel)
-  if (!(se && se[0] == '1') && r % 32 == 0 && r <= 256 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+  if (!tuning().spmm_warp && r % 32 == 0 && r <= 256 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
     spmm_half_kernel<8><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
                                              col_hi, v);
   } else if ((r & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0)

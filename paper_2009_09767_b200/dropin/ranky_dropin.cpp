@@ -48,16 +48,28 @@ static_assert(sizeof(ranky::Entry) == sizeof(rk_entry), "ranky::Entry must match
 namespace ranky {
 namespace {
 
+// The reference's functions are reentrant and may run concurrently (proj/src/pipeline.cpp
+// runs run_block_task on a thread pool); an rk_ctx is not thread-safe (include/ranky_b200.h),
+// so every calling thread gets its own context (own stream, pinned arena and launch
+// counter), created on first use and destroyed when the thread exits.
+struct ThreadContext {
+  rk_ctx* ctx = nullptr;
+  ~ThreadContext() {
+    if (ctx) rk_ctx_destroy(ctx);
+  }
+};
+
 rk_ctx* context() {
-  static std::once_flag once;
-  static rk_ctx* ctx = nullptr;
-  std::call_once(once, [] {
+  thread_local ThreadContext tc;
+  if (!tc.ctx) {
     int dev = 0;
     if (const char* e = std::getenv("RANKY_DEVICE")) dev = std::atoi(e);
-    if (rk_ctx_create(dev, &ctx) != RK_OK)
+    if (rk_ctx_create(dev, &tc.ctx) != RK_OK) {
+      tc.ctx = nullptr;
       throw std::runtime_error(std::string("ranky B200 drop-in: ") + rk_last_error());
-  });
-  return ctx;
+    }
+  }
+  return tc.ctx;
 }
 
 void check(rk_status st) {

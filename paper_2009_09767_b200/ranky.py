@@ -183,6 +183,7 @@ def lib():
         pu64, pdbl = C.POINTER(C.c_uint64), C.POINTER(C.c_double)
         sig = {
             "rk_last_error": ([], C.c_char_p), "rk_last_residual": ([], dbl), "rk_abi_version": ([], i32),
+            "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32),
             "rk_ctx_create": ([i32, C.POINTER(vp)], i32), "rk_ctx_destroy": ([vp], i32),
             "rk_ctx_set_stream": ([vp, vp], i32), "rk_ctx_synchronize": ([vp], i32),
             "rk_ctx_kernel_launches": ([vp], u64),
@@ -231,6 +232,16 @@ def lib():
             f.restype = res
         _lib = L
         return L
+
+
+def reload_tuning() -> None:
+    """Re-read the RK_* tuning switches (the library reads them once per process)."""
+    lib().rk_reload_tuning()
+
+
+def experiments_built() -> bool:
+    """True when libranky_b200.so is the experiments build (RK_EXPERIMENTS=1)."""
+    return bool(lib().rk_build_flags() & 1)
 
 
 def _check(status: int):
@@ -332,17 +343,19 @@ class SparseMatrix:
         order = np.lexsort((e["col"], e["row"]))
         e = e[order]
         if len(e):
-            bad = (e["row"] >= self._rows) | (e["col"] >= self._cols)
+            # the reference checks entry by entry in sorted order (sparse_matrix.cpp:15-29):
+            # the first entry that violates any rule decides which error is raised
+            out = (e["row"] >= self._rows) | (e["col"] >= self._cols)
+            zero = e["value"] == 0.0
+            dup = np.zeros(len(e), dtype=bool)
+            dup[1:] = (e["row"][1:] == e["row"][:-1]) & (e["col"][1:] == e["col"][:-1])
+            bad = out | zero | dup
             if bad.any():
                 i = int(np.argmax(bad))
-                raise InvalidArgument(f"sparse entry ({e['row'][i]}, {e['col'][i]}) outside {rows}x{cols}")
-            z = e["value"] == 0.0
-            if z.any():
-                i = int(np.argmax(z))
-                raise InvalidArgument(f"sparse entry ({e['row'][i]}, {e['col'][i]}) stores zero")
-            dup = (e["row"][1:] == e["row"][:-1]) & (e["col"][1:] == e["col"][:-1])
-            if dup.any():
-                i = int(np.argmax(dup)) + 1
+                if out[i]:
+                    raise InvalidArgument(f"sparse entry ({e['row'][i]}, {e['col'][i]}) outside {rows}x{cols}")
+                if zero[i]:
+                    raise InvalidArgument(f"sparse entry ({e['row'][i]}, {e['col'][i]}) stores zero")
                 raise InvalidArgument(f"duplicate sparse entry ({e['row'][i]}, {e['col'][i]})")
         self._e = np.ascontiguousarray(e)
 

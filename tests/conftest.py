@@ -39,6 +39,20 @@ def ref():
     return Oracle("reference") if available("reference") else Oracle("port")
 
 
+@pytest.fixture
+def tuning_env(monkeypatch):
+    """set(name, value): an RK_* tuning switch for this test (the library reads the
+    switches once per process; rk_reload_tuning re-reads them, here and at teardown)."""
+    import paper_2009_09767_b200.ranky as R
+
+    def set_(name, value):
+        monkeypatch.setenv(name, value)
+        R.reload_tuning()
+    yield set_
+    monkeypatch.undo()
+    R.reload_tuning()
+
+
 def golden_matrix(garrays, name, prefix="in_"):
     r = garrays[f"{prefix}{name}_r"]
     c = garrays[f"{prefix}{name}_c"]

@@ -12,7 +12,7 @@ import pytest
 
 import paper_2009_09767_b200 as rk
 from paper_2009_09767_b200 import configs
-from test_gpu_svd import compare
+from parity import compare
 
 pytestmark = pytest.mark.gpu
 

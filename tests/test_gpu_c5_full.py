@@ -18,7 +18,7 @@ import pytest
 import paper_2009_09767_b200 as rk
 from paper_2009_09767_b200 import configs
 from paper_2009_09767_b200.ranky import dev_outputs_tensors, dev_residual
-from test_gpu_svd import compare
+from parity import compare
 from test_gpu_scale import coo_of
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow,

@@ -25,7 +25,7 @@ import scipy.sparse as sp
 import paper_2009_09767_b200 as rk
 from paper_2009_09767_b200 import configs
 from paper_2009_09767_b200.ranky import dev_outputs_tensors
-from test_gpu_svd import compare
+from parity import check_sigma, check_u, check_v_rows, compare
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -41,6 +41,15 @@ def sample_blocks(D, n, seed):
     rng = np.random.default_rng(seed)
     mid = rng.choice(np.arange(1, D - 1), size=n - 2, replace=False)
     return sorted({0, D - 1, *mid.tolist()})
+
+
+def load_golden(name):
+    import os
+    for f in (f"{name}_reference.npz", f"{name}_merge_reference.npz"):
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f)
+        if os.path.exists(p):
+            return dict(np.load(p))
+    return None
 
 
 def gram(a):
@@ -94,6 +103,14 @@ def test_full_scale_config(name, n_blocks, ref):
         assert out.contents.n_edges == len(report.added_edges)
         sigma, u = sig_d.cpu().numpy(), u_d.cpu().numpy()
         assert sigma.shape == (M,) and u.shape == (M, M)
+        gold = load_golden(name)
+        if gold is not None:
+            # the reference's own final sigma / U: c3 from its full run_pipeline, c4 from its
+            # proxy_from_records + proxy_svd on the GPU's block records (tests/golden/make_*_golden.py)
+            k = gold["u"].shape[1]
+            check_sigma(sigma, gold["sigma"], f"{name} sigma vs reference")
+            check_u(u, gold["u"], gold["sigma"], f"{name} U vs reference", cols=k)
+            mark(f"sigma/U checked against the reference ({k} U columns)")
         lam, q = np.linalg.eigh(gram(rep))
         lam, q = lam[::-1], q[:, ::-1]
         s_ref = np.sqrt(np.clip(lam, 0, None))
@@ -127,6 +144,11 @@ def test_full_scale_config(name, n_blocks, ref):
         vr = ref.recover_right_vectors(coo_of(views[d]), u, sigma, rk.K_RANK_TOL)
         got = v_d[rng_d.begin:rng_d.end].cpu().numpy()
         assert np.array_equal(got, vr), (name, d, float(np.abs(got - vr).max()))
+        if gold is not None:
+            # and against the reference's own V (its U, sigma) on the golden's slice of rows
+            lo = int(gold["v_begin"])
+            vg = gold["v_rows"]
+            check_v_rows(v_d[lo:lo + vg.shape[0]].cpu().numpy(), vg, gold["sigma"], f"{name} V rows vs reference")
         mark("V checked")
     finally:
         rk.dev_outputs_free(out)

@@ -15,7 +15,7 @@ import pytest
 import paper_2009_09767_b200 as rk
 from paper_2009_09767_b200 import configs, shard
 from paper_2009_09767_b200 import ranky as R
-from test_gpu_svd import compare
+from parity import compare
 
 pytestmark = pytest.mark.gpu
 
@@ -146,10 +146,10 @@ def test_sharded_gram_route(name):
         assert held, "c2's merge is well conditioned: the Gram route must hold"
 
 
-def test_sharded_gram_not_applicable(monkeypatch):
+def test_sharded_gram_not_applicable(tuning_env):
     """RK_BLOCK_ROUTE=householder turns the Gram routes off: factor_gram reports
     RK_GRAM_REJECTED (no shard) and the protocol takes the TSQR path."""
-    monkeypatch.setenv("RK_BLOCK_ROUTE", "householder")
+    tuning_env("RK_BLOCK_ROUTE", "householder")
     cfg = configs.CONFIGS["c1"]
     dm = rk.DeviceMatrix(cfg.generate())
     outs, held = run_sharded(dm, cfg, 2, "gram")

@@ -12,8 +12,7 @@ from paper_2009_09767_b200 import configs
 
 pytestmark = pytest.mark.gpu
 
-SIGMA_REL = 1e-10
-OVERLAP = 1 - 1e-8
+from parity import compare, SIGMA_REL, OVERLAP  # noqa: F401  (re-exported for the other tests)
 
 
 def orth_defect(u):
@@ -28,22 +27,6 @@ def check_contract(a, s):
     assert np.all(np.diff(s.sigma) <= 0) and np.all(s.sigma >= 0)
     res = np.linalg.norm(a - (s.u * s.sigma) @ s.v.T)
     assert res <= 1e-10 * max(1.0, np.linalg.norm(a))
-
-
-def compare(s, ref_sigma, ref_u, what=""):
-    sig = np.asarray(s.sigma)
-    assert sig.shape == ref_sigma.shape, what
-    smax = ref_sigma.max() if ref_sigma.size else 0.0
-    big = ref_sigma > 1e-8 * smax
-    if big.any():
-        rel = np.abs(sig[big] - ref_sigma[big]) / ref_sigma[big]
-        assert rel.max() <= SIGMA_REL, (what, rel.max())
-    assert np.all(np.abs(sig[~big] - ref_sigma[~big]) <= 1e-8 * max(smax, 1e-300)), what
-    for j in np.nonzero(big)[0]:
-        gaps = [abs(ref_sigma[j] - ref_sigma[i]) for i in (j - 1, j + 1) if 0 <= i < len(ref_sigma)]
-        if min(gaps, default=np.inf) <= 1e-9 * smax:
-            continue  # degenerate cluster: compared by subspace elsewhere
-        assert abs(float(s.u[:, j] @ ref_u[:, j])) >= OVERLAP, (what, j)
 
 
 def test_closed_forms():

@@ -23,6 +23,14 @@ def test_sparse_matrix_validation():
         rk.SparseMatrix(2, 2, [(0, 0, 1.0), (0, 0, 2.0)])
     with pytest.raises(rk.OutOfRange):
         a.row_entries(5)
+    # the first violating entry in sorted order decides (sparse_matrix.cpp:15-29): an early
+    # stored zero is reported before a later out-of-range entry, and vice versa
+    with pytest.raises(rk.InvalidArgument, match=r"\(0, 1\) stores zero"):
+        rk.SparseMatrix(2, 2, [(5, 0, 1.0), (0, 1, 0.0)])
+    with pytest.raises(rk.InvalidArgument, match=r"\(0, 7\) outside"):
+        rk.SparseMatrix(2, 2, [(0, 7, 1.0), (1, 1, 0.0)])
+    with pytest.raises(rk.InvalidArgument, match=r"duplicate sparse entry \(0, 1\)"):
+        rk.SparseMatrix(2, 2, [(1, 1, 0.0), (0, 1, 2.0), (0, 1, 3.0)])
 
 
 def test_partition_columns():

@@ -7,7 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import numpy as np
 import paper_2009_09767_b200 as rk
 from paper_2009_09767_b200 import configs
-from test_gpu_svd import compare
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from parity import compare
 cfg = configs.CONFIGS["c5"]
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 t = time.time()
