@@ -253,6 +253,32 @@ RK_API rk_status rk_dev_outputs_free(rk_dev_outputs* o);
 RK_API rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
                                  double* a_norm);
 
+/* ---- evaluation metrics (proj/include/ranky/metrics.hpp, proj/src/metrics.cpp) ----
+ * Matrices are row-major (DenseMatrix layout). The rk_dev_* forms take device
+ * pointers (e.g. rk_dev_outputs' d_u / d_sigma) and return scalars to the host;
+ * the plain forms take host pointers (upload, compute on the device, download).
+ *   sigma_error        metrics.cpp:32-42   sum |a_i - b_i|, the shorter list zero-padded
+ *   align_signs        metrics.cpp:44-93   sign flips; Procrustes on clusters of sigma_ref
+ *                                          (n_sigma = 0: no sigma, flips only)
+ *   left_vector_error  metrics.cpp:95-103  sum |align_signs(u_hat) - u_ref|
+ *   numerical_rank     metrics.cpp:105-114 #{sigma > tol sigma_max} of dense_svd(a) */
+RK_API rk_status rk_dev_sigma_error(rk_ctx* ctx, const double* d_sigma_hat, uint64_t n_hat,
+                                    const double* d_sigma_ref, uint64_t n_ref, double* out);
+RK_API rk_status rk_dev_align_signs(rk_ctx* ctx, const double* d_u_hat, const double* d_u_ref, uint64_t rows,
+                                    uint64_t cols, const double* d_sigma_ref, uint64_t n_sigma, double* d_out);
+RK_API rk_status rk_dev_left_vector_error(rk_ctx* ctx, const double* d_u_hat, const double* d_u_ref, uint64_t rows,
+                                          uint64_t cols, const double* d_sigma_ref, uint64_t n_sigma, double* out);
+RK_API rk_status rk_dev_numerical_rank(rk_ctx* ctx, const double* d_a, uint64_t rows, uint64_t cols, double tol,
+                                       uint64_t* out);
+RK_API rk_status rk_sigma_error(rk_ctx* ctx, const double* sigma_hat, uint64_t n_hat, const double* sigma_ref,
+                                uint64_t n_ref, double* out);
+RK_API rk_status rk_align_signs(rk_ctx* ctx, const double* u_hat, const double* u_ref, uint64_t rows, uint64_t cols,
+                                const double* sigma_ref, uint64_t n_sigma, double* out);
+RK_API rk_status rk_left_vector_error(rk_ctx* ctx, const double* u_hat, const double* u_ref, uint64_t rows,
+                                      uint64_t cols, const double* sigma_ref, uint64_t n_sigma, double* out);
+RK_API rk_status rk_numerical_rank(rk_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double tol,
+                                   uint64_t* out);
+
 /* ---- sharded path (one process per GPU) --------------------------------------
  * Column blocks are sharded over G ranks by merge-tree leaves. Rank g repairs the
  * whole matrix (the replay is deterministic, so every rank holds the same repaired

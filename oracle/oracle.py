@@ -238,6 +238,44 @@ class Oracle:
                                                          self._p(flat, C.c_double)))
 
 
+    # ---- evaluation metrics (reference only): proj/src/metrics.cpp:32-114 ----
+    def sigma_error(self, a, b) -> float:
+        a = np.ascontiguousarray(a, dtype=np.float64); b = np.ascontiguousarray(b, dtype=np.float64)
+        fn = self.lib.ref_sigma_error
+        fn.restype = C.c_double
+        fn.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.POINTER(C.c_double), C.c_uint64]
+        return float(fn(self._p(a, C.c_double), len(a), self._p(b, C.c_double), len(b)))
+
+    def align_signs(self, u_hat, u_ref, sigma=None) -> np.ndarray:
+        h = np.ascontiguousarray(u_hat, dtype=np.float64); r = np.ascontiguousarray(u_ref, dtype=np.float64)
+        s = np.ascontiguousarray(np.zeros(0) if sigma is None else sigma, dtype=np.float64)
+        out = np.zeros_like(h)
+        fn = self.lib.ref_align_signs
+        fn.restype = C.c_int
+        pd = C.POINTER(C.c_double)
+        fn.argtypes = [pd, pd, C.c_uint64, C.c_uint64, pd, C.c_uint64, pd]
+        if fn(self._p(h, C.c_double), self._p(r, C.c_double), h.shape[0], h.shape[1], self._p(s, C.c_double),
+              len(s), self._p(out, C.c_double)):
+            raise OracleError(1, "align_signs: invalid argument")
+        return out
+
+    def left_vector_error(self, u_hat, u_ref, sigma=None) -> float:
+        h = np.ascontiguousarray(u_hat, dtype=np.float64); r = np.ascontiguousarray(u_ref, dtype=np.float64)
+        s = np.ascontiguousarray(np.zeros(0) if sigma is None else sigma, dtype=np.float64)
+        fn = self.lib.ref_left_vector_error
+        fn.restype = C.c_double
+        pd = C.POINTER(C.c_double)
+        fn.argtypes = [pd, pd, C.c_uint64, C.c_uint64, pd, C.c_uint64]
+        return float(fn(self._p(h, C.c_double), self._p(r, C.c_double), h.shape[0], h.shape[1],
+                        self._p(s, C.c_double), len(s)))
+
+    def numerical_rank(self, a, tol) -> int:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        fn = self.lib.ref_numerical_rank
+        fn.restype = C.c_uint64
+        fn.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint64, C.c_double]
+        return int(fn(self._p(a, C.c_double), a.shape[0], a.shape[1], tol))
+
     def sampled_pipeline(self, a, D, method, keep, seed, workers, sample, slice_cols, phase) -> np.ndarray:
         """ref_sampled_pipeline (reference only): per-stage std::chrono times of the
         reference's run_pipeline stages on a block sample (see ref_capi.cpp)."""

@@ -18,6 +18,7 @@
 #include "ranky/block_record.hpp"
 #include "ranky/dense_matrix.hpp"
 #include "ranky/errors.hpp"
+#include "ranky/metrics.hpp"
 #include "ranky/partition.hpp"
 #include "ranky/pipeline.hpp"
 #include "ranky/proxy.hpp"
@@ -320,6 +321,32 @@ int ref_read_block_record(const char* path, uint32_t* index, uint32_t* rows, uin
   } catch (const std::exception&) {
     return 2;
   }
+}
+
+// ---- evaluation metrics -- proj/src/metrics.cpp:32-114 ----
+double ref_sigma_error(const double* a, uint64_t na, const double* b, uint64_t nb) {
+  return sigma_error(std::span<const double>(a, na), std::span<const double>(b, nb));
+}
+int ref_align_signs(const double* hat, const double* ref, uint64_t rows, uint64_t cols, const double* sigma,
+                    uint64_t n_sigma, double* out) {
+  try {
+    DenseMatrix h(rows, cols, std::vector<double>(hat, hat + rows * cols));
+    DenseMatrix r(rows, cols, std::vector<double>(ref, ref + rows * cols));
+    DenseMatrix o = align_signs(h, r, std::span<const double>(sigma, n_sigma));
+    std::memcpy(out, o.values().data(), rows * cols * sizeof(double));
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+double ref_left_vector_error(const double* hat, const double* ref, uint64_t rows, uint64_t cols,
+                             const double* sigma, uint64_t n_sigma) {
+  DenseMatrix h(rows, cols, std::vector<double>(hat, hat + rows * cols));
+  DenseMatrix r(rows, cols, std::vector<double>(ref, ref + rows * cols));
+  return left_vector_error(h, r, std::span<const double>(sigma, n_sigma));
+}
+uint64_t ref_numerical_rank(const double* a, uint64_t rows, uint64_t cols, double tol) {
+  return numerical_rank(DenseMatrix(rows, cols, std::vector<double>(a, a + rows * cols)), tol);
 }
 
 // ---- the reference arm's bounded sample (bench.py --impl reference) ----------

@@ -6,7 +6,8 @@ from .ranky import (BlockPartition, BlockResultRecord, BlockTask, ColumnRange, C
                     DeviceMatrix, InvalidArgument, OutOfRange, PipelineResult, ProxyMatrix, RankyRuntimeError,
                     RepairMethod, RepairReport, SparseMatrix, SvdResult, block_svd, block_view, build_proxy,
                     dense_svd, find_lonely_rows, partition_columns, proxy_from_records, proxy_svd,
-                    recover_right_vectors, repair, run_block_task, run_block_tasks, run_pipeline, sparse_of)
+                    recover_right_vectors, repair, run_block_task, run_block_tasks, run_pipeline, sparse_of,
+                    sigma_error, align_signs, left_vector_error, numerical_rank)
 
 __all__ = [
     "BlockPartition", "BlockResultRecord", "BlockTask", "ColumnRange", "ConvergenceError", "Context", "DeviceMatrix",
@@ -14,4 +15,5 @@ __all__ = [
     "RepairReport", "SparseMatrix", "SvdResult", "block_svd", "block_view", "build_proxy", "dense_svd",
     "find_lonely_rows", "partition_columns", "proxy_from_records", "proxy_svd", "recover_right_vectors", "repair",
     "run_block_task", "run_block_tasks", "run_pipeline", "sparse_of",
+    "sigma_error", "align_signs", "left_vector_error", "numerical_rank",
 ]

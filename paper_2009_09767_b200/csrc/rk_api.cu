@@ -975,6 +975,116 @@ rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outp
   });
 }
 
+// ---- evaluation metrics (rk_eval.cu) ----
+rk_status rk_dev_sigma_error(rk_ctx* ctx, const double* d_sigma_hat, uint64_t n_hat, const double* d_sigma_ref,
+                             uint64_t n_ref, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (n_hat && !d_sigma_hat) || (n_ref && !d_sigma_ref)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    *out = sigma_error_device(d_sigma_hat, n_hat, d_sigma_ref, n_ref, ctx->c.stream);
+  });
+}
+
+rk_status rk_dev_align_signs(rk_ctx* ctx, const double* d_u_hat, const double* d_u_ref, uint64_t rows, uint64_t cols,
+                             const double* d_sigma_ref, uint64_t n_sigma, double* d_out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (rows * cols && (!d_u_hat || !d_u_ref || !d_out)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    align_signs_device(ctx->c, d_u_hat, d_u_ref, rows, cols, d_sigma_ref, n_sigma, d_out);
+    sync(ctx->c.stream);
+  });
+}
+
+rk_status rk_dev_left_vector_error(rk_ctx* ctx, const double* d_u_hat, const double* d_u_ref, uint64_t rows,
+                                   uint64_t cols, const double* d_sigma_ref, uint64_t n_sigma, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (rows * cols && (!d_u_hat || !d_u_ref))) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    *out = left_vector_error_device(ctx->c, d_u_hat, d_u_ref, rows, cols, d_sigma_ref, n_sigma);
+  });
+}
+
+rk_status rk_dev_numerical_rank(rk_ctx* ctx, const double* d_a, uint64_t rows, uint64_t cols, double tol,
+                                uint64_t* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (rows * cols && !d_a)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    *out = numerical_rank_device(ctx->c, d_a, rows, cols, tol);
+  });
+}
+
+rk_status rk_sigma_error(rk_ctx* ctx, const double* sigma_hat, uint64_t n_hat, const double* sigma_ref,
+                         uint64_t n_ref, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (n_hat && !sigma_hat) || (n_ref && !sigma_ref)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    DBuf<double> a(n_hat + 1, s), b(n_ref + 1, s);
+    to_device(a.get(), sigma_hat, n_hat, s);
+    to_device(b.get(), sigma_ref, n_ref, s);
+    *out = sigma_error_device(a.get(), n_hat, b.get(), n_ref, s);
+  });
+}
+
+namespace {
+void check_align_shapes(uint64_t n_sigma, uint64_t cols) {
+  if (n_sigma && n_sigma != cols) fail(RK_INVALID_ARGUMENT, "align_signs: sigma length mismatch");
+}
+}  // namespace
+
+rk_status rk_align_signs(rk_ctx* ctx, const double* u_hat, const double* u_ref, uint64_t rows, uint64_t cols,
+                         const double* sigma_ref, uint64_t n_sigma, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (rows * cols && (!u_hat || !u_ref || !out)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    check_align_shapes(n_sigma, cols);
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    const uint64_t n = rows * cols;
+    DBuf<double> h(n + 1, s), r(n + 1, s), o(n + 1, s), sg(n_sigma + 1, s);
+    to_device(h.get(), u_hat, n, s);
+    to_device(r.get(), u_ref, n, s);
+    to_device(sg.get(), sigma_ref, n_sigma, s);
+    align_signs_device(ctx->c, h.get(), r.get(), rows, cols, n_sigma ? sg.get() : nullptr, n_sigma, o.get());
+    if (n) RK_CUDA_CHECK(cudaMemcpyAsync(out, o.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+rk_status rk_left_vector_error(rk_ctx* ctx, const double* u_hat, const double* u_ref, uint64_t rows, uint64_t cols,
+                               const double* sigma_ref, uint64_t n_sigma, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (rows * cols && (!u_hat || !u_ref))) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    check_align_shapes(n_sigma, cols);
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    const uint64_t n = rows * cols;
+    DBuf<double> h(n + 1, s), r(n + 1, s), sg(n_sigma + 1, s);
+    to_device(h.get(), u_hat, n, s);
+    to_device(r.get(), u_ref, n, s);
+    to_device(sg.get(), sigma_ref, n_sigma, s);
+    *out = left_vector_error_device(ctx->c, h.get(), r.get(), rows, cols, n_sigma ? sg.get() : nullptr, n_sigma);
+  });
+}
+
+rk_status rk_numerical_rank(rk_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double tol, uint64_t* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!out || (rows * cols && !a)) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ctx->c);
+    cudaStream_t s = ctx->c.stream;
+    DBuf<double> d(rows * cols + 1, s);
+    to_device(d.get(), a, rows * cols, s);
+    *out = numerical_rank_device(ctx->c, d.get(), rows, cols, tol);
+  });
+}
+
 uint64_t rk_merge_tree_leaves(uint64_t rows, uint64_t cols, uint64_t block_count, uint64_t keep) {
   try {
     Partition p = make_partition(cols, block_count);

@@ -100,6 +100,14 @@ double kappa_max(uint32_t M);
 uint32_t cholesky_max_rows();
 bool gram_route_enabled();
 
+// rk_eval.cu: the reference's evaluation metrics (proj/src/metrics.cpp:32-114) on the device
+double sigma_error_device(const double* a, uint64_t na, const double* b, uint64_t nb, cudaStream_t s);
+void align_signs_device(Ctx& c, const double* hat, const double* ref, uint64_t rows, uint64_t cols,
+                        const double* sigma_ref, uint64_t n_sigma, double* out);
+double left_vector_error_device(Ctx& c, const double* hat, const double* ref, uint64_t rows, uint64_t cols,
+                                const double* sigma_ref, uint64_t n_sigma);
+uint64_t numerical_rank_device(Ctx& c, const double* a, uint64_t rows, uint64_t cols, double tol);
+
 // small launch helpers
 void sign_rows(double* u, uint32_t rows, uint32_t k, double* v, uint32_t vrows, cudaStream_t s);
 void check_finite_or_throw(const double* x, uint64_t n, const char* what, cudaStream_t s);

@@ -184,6 +184,14 @@ def lib():
         sig = {
             "rk_last_error": ([], C.c_char_p), "rk_last_residual": ([], dbl), "rk_abi_version": ([], i32),
             "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32),
+            "rk_sigma_error": ([vp, pdbl, u64, pdbl, u64, pdbl], i32),
+            "rk_align_signs": ([vp, pdbl, pdbl, u64, u64, pdbl, u64, pdbl], i32),
+            "rk_left_vector_error": ([vp, pdbl, pdbl, u64, u64, pdbl, u64, pdbl], i32),
+            "rk_numerical_rank": ([vp, pdbl, u64, u64, dbl, pu64], i32),
+            "rk_dev_sigma_error": ([vp, vp, u64, vp, u64, pdbl], i32),
+            "rk_dev_align_signs": ([vp, vp, vp, u64, u64, vp, u64, vp], i32),
+            "rk_dev_left_vector_error": ([vp, vp, vp, u64, u64, vp, u64, pdbl], i32),
+            "rk_dev_numerical_rank": ([vp, vp, u64, u64, dbl, pu64], i32),
             "rk_ctx_create": ([i32, C.POINTER(vp)], i32), "rk_ctx_destroy": ([vp], i32),
             "rk_ctx_set_stream": ([vp, vp], i32), "rk_ctx_synchronize": ([vp], i32),
             "rk_ctx_kernel_launches": ([vp], u64),
@@ -751,6 +759,72 @@ def recover_right_vectors(a: SparseMatrix, u: np.ndarray, sigma, tol: float = K_
         return _svd_of(out).v
     finally:
         L.rk_svd_free(C.byref(out))
+
+
+# ---------------------------------------------------------------------------
+# evaluation metrics -- proj/include/ranky/metrics.hpp, proj/src/metrics.cpp:32-114 (rk_eval.cu)
+
+def _pd(x):
+    return x.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def sigma_error(sigma_hat, sigma_ref, ctx: Context | None = None) -> float:
+    """Sum of |sigma_hat_i - sigma_ref_i|, the shorter list zero-padded (metrics.cpp:32-42)."""
+    a = np.ascontiguousarray(sigma_hat, dtype=np.float64)
+    b = np.ascontiguousarray(sigma_ref, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().rk_sigma_error(_ctx(ctx), _pd(a), len(a), _pd(b), len(b), C.byref(out)))
+    return out.value
+
+
+def align_signs(u_hat, u_ref, sigma_ref=None, ctx: Context | None = None) -> np.ndarray:
+    """Sign flips per column; with sigma_ref, Procrustes on degenerate clusters (metrics.cpp:44-93)."""
+    h = np.ascontiguousarray(u_hat, dtype=np.float64)
+    r = np.ascontiguousarray(u_ref, dtype=np.float64)
+    if h.shape != r.shape:
+        raise InvalidArgument("align_signs: shape mismatch")
+    sg = np.ascontiguousarray(np.zeros(0) if sigma_ref is None else sigma_ref, dtype=np.float64)
+    out = np.empty_like(h)
+    _check(lib().rk_align_signs(_ctx(ctx), _pd(h), _pd(r), h.shape[0], h.shape[1], _pd(sg), len(sg), _pd(out)))
+    return out
+
+
+def left_vector_error(u_hat, u_ref, sigma_ref, ctx: Context | None = None) -> float:
+    """Sum of |align_signs(u_hat) - u_ref| (metrics.cpp:95-103)."""
+    h = np.ascontiguousarray(u_hat, dtype=np.float64)
+    r = np.ascontiguousarray(u_ref, dtype=np.float64)
+    if h.shape != r.shape:
+        raise InvalidArgument("align_signs: shape mismatch")
+    sg = np.ascontiguousarray(sigma_ref, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().rk_left_vector_error(_ctx(ctx), _pd(h), _pd(r), h.shape[0], h.shape[1], _pd(sg), len(sg),
+                                      C.byref(out)))
+    return out.value
+
+
+def numerical_rank(a, tol: float, ctx: Context | None = None) -> int:
+    """Count of singular values above tol * sigma_max (metrics.cpp:105-114)."""
+    d = np.ascontiguousarray(a, dtype=np.float64)
+    out = C.c_uint64()
+    _check(lib().rk_numerical_rank(_ctx(ctx), _pd(d), d.shape[0], d.shape[1], tol, C.byref(out)))
+    return int(out.value)
+
+
+def dev_left_vector_error(u_hat_t, u_ref_t, sigma_ref_t=None, ctx: Context | None = None) -> float:
+    """left_vector_error on device tensors (torch, float64, row-major contiguous)."""
+    out = C.c_double()
+    ns = 0 if sigma_ref_t is None else int(sigma_ref_t.numel())
+    _check(lib().rk_dev_left_vector_error(_ctx(ctx), C.c_void_p(u_hat_t.data_ptr()), C.c_void_p(u_ref_t.data_ptr()),
+                                          u_hat_t.shape[0], u_hat_t.shape[1],
+                                          C.c_void_p(sigma_ref_t.data_ptr() if ns else 0), ns, C.byref(out)))
+    return out.value
+
+
+def dev_sigma_error(a_t, b_t, ctx: Context | None = None) -> float:
+    out = C.c_double()
+    _check(lib().rk_dev_sigma_error(_ctx(ctx), C.c_void_p(a_t.data_ptr()), a_t.numel(), C.c_void_p(b_t.data_ptr()),
+                                    b_t.numel(), C.byref(out)))
+    return out.value
 
 
 # ---------------------------------------------------------------------------

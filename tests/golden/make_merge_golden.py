@@ -42,6 +42,9 @@ def main(name, out_dir, scale=None):
 
     R = Oracle("reference")
     cfg = configs.CONFIGS[name]
+    if scale:  # dry run: the config's block width, scale // width blocks
+        import dataclasses
+        cfg = dataclasses.replace(cfg, cols=scale, blocks=scale // (cfg.cols // cfg.blocks))
     a = cfg.generate(scale)
     M = a.rows()
     mark("generated")
@@ -59,7 +62,7 @@ def main(name, out_dir, scale=None):
     del recs
     mark("reference proxy_from_records + proxy_svd")
     p = rk.partition_columns(rep.cols(), cfg.blocks)
-    rng = p.range(V_BLOCK[name])
+    rng = p.range(min(V_BLOCK[name], cfg.blocks - 1))
     lo = rng.begin
     rr, rc, rv = rep.coo()
     m = (rc >= lo) & (rc < lo + V_COLS)

@@ -14,6 +14,9 @@
 * a cluster of >1 columns is compared by the largest principal angle between the
   two column spans (proj/tests/test_support.hpp:71-79), computed from its sine
   ||(I - Ã Ãᵀ) B||₂ for accuracy at small angles; bound 1e-6.
+* columns of numerically zero sigma (<= 1e-10·sigma_max) are any basis of part of
+  the null space; they are compared (as a span) only when U is square and they
+  form its tail, where the span is the complement of the rest.
 """
 from __future__ import annotations
 
@@ -84,10 +87,20 @@ def check_u(u, ref_u, ref_sigma, what="", cols: int | None = None):
     k = ref_u.shape[1] if cols is None else cols
     assert u.shape[0] == ref_u.shape[0] and u.shape[1] >= k, (what, u.shape, ref_u.shape)
     min_ov, max_sin = 1.0, 0.0
+    smax = float(np.max(ref_sigma)) if len(ref_sigma) else 0.0
+    square = ref_u.shape[1] == ref_u.shape[0]
     for lo, hi in clusters(ref_sigma[:ref_u.shape[1]]):
         if lo >= k:
             break
         hi_c = min(hi, k)
+        if np.all(ref_sigma[lo:hi] <= SIGMA_SPLIT * smax):
+            # numerically zero sigma: the columns span part of the null space, which fixes them
+            # only when U is a full basis and the cluster is its tail (the complement of the rest)
+            if square and hi == ref_u.shape[1]:
+                s = sin_largest_angle(u[:, lo:hi_c], ref_u[:, lo:hi])
+                max_sin = max(max_sin, s)
+                assert s <= ANGLE, (what, "null-space tail", lo, hi, s)
+            continue
         if hi - lo == 1:
             ov = float(u[:, lo] @ ref_u[:, lo])
             if ov < OVERLAP and sign_ambiguous(ref_u[:, lo]):

@@ -78,3 +78,15 @@ def test_near_tie_sign_exempt():
     flipped = u.copy()
     flipped[:, 0] *= -1
     check_u(flipped, u, s)
+
+
+def test_null_space_columns():
+    rng = np.random.default_rng(4)
+    u, _ = np.linalg.qr(rng.standard_normal((9, 9)))
+    s = np.array([5.0, 2.0] + [1e-16] * 7)
+    other = u.copy()
+    q, _ = np.linalg.qr(rng.standard_normal((7, 7)))
+    other[:, 2:] = u[:, 2:] @ q          # another basis of the same null space: passes
+    check_u(other, u, s)
+    trunc_ref, trunc = u[:, :4], other[:, :4]   # truncated: the null columns are not determined
+    check_u(trunc, trunc_ref, s[:4])
