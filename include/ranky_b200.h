@@ -253,6 +253,29 @@ RK_API rk_status rk_dev_outputs_free(rk_dev_outputs* o);
 RK_API rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
                                  double* a_norm);
 
+/* ---- RepairWorkspace (proj/include/ranky/repair.hpp:56-87, proj/src/repair.cpp:52-160) ----
+ * The single-row checker API on a device workspace: the matrix (device CSR + CSC)
+ * plus the edges inserted so far. Partitions are partition_columns(cols, block_count).
+ * The draws stay with the caller's KeyedRng, where the reference makes them:
+ *   apply_random(d, row, rng):   col = begin(d) + rng.below(width(d)); rk_workspace_insert
+ *   apply_neighbor(d, row, rng): rk_workspace_neighbor_columns -> n; n == 0: no edge and no
+ *                                draw; else col = cols[rng.below(n)]; rk_workspace_insert
+ * rk_workspace_neighbor_columns writes the ascending distinct columns of block d held by
+ * rows sharing a column with `row` outside block d (the row itself included), as
+ * repair.cpp:107-125 builds neighbor_cols; `cols` must hold width(d) entries.
+ * Insertion is idempotent. rk_workspace_to_matrix: original values kept, inserted 1.0. */
+typedef struct rk_workspace rk_workspace;
+RK_API rk_status rk_workspace_create(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count,
+                                     rk_workspace** out);
+RK_API rk_status rk_workspace_destroy(rk_workspace* ws);
+RK_API rk_status rk_workspace_has_entry(rk_workspace* ws, uint64_t row, uint64_t col, int32_t* out);
+RK_API rk_status rk_workspace_row_lonely_in_block(rk_workspace* ws, uint64_t d, uint64_t row, int32_t* out);
+RK_API rk_status rk_workspace_lonely_rows(rk_workspace* ws, uint64_t d, uint64_t* rows_out, uint64_t* n_out);
+RK_API rk_status rk_workspace_neighbor_columns(rk_workspace* ws, uint64_t d, uint64_t row, uint64_t* cols_out,
+                                               uint64_t* n_out);
+RK_API rk_status rk_workspace_insert(rk_workspace* ws, uint64_t row, uint64_t col);
+RK_API rk_status rk_workspace_to_matrix(rk_workspace* ws, rk_sparse* out);
+
 /* ---- evaluation metrics (proj/include/ranky/metrics.hpp, proj/src/metrics.cpp) ----
  * Matrices are row-major (DenseMatrix layout). The rk_dev_* forms take device
  * pointers (e.g. rk_dev_outputs' d_u / d_sigma) and return scalars to the host;

@@ -975,6 +975,94 @@ rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outp
   });
 }
 
+// ---- RepairWorkspace (rk_workspace.cu) ----
+struct rk_workspace {
+  rk_ctx* owner;
+  Workspace* w;
+};
+
+rk_status rk_workspace_create(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_count, rk_workspace** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    check_view(a);
+    if (!out) fail(RK_INVALID_ARGUMENT, "out is NULL");
+    CallScope sc(&ctx->c);
+    auto h = std::make_unique<rk_workspace>();
+    h->owner = ctx;
+    h->w = workspace_create(ctx->c, *a, block_count);
+    *out = h.release();
+  });
+}
+
+rk_status rk_workspace_destroy(rk_workspace* ws) {
+  if (!ws) return RK_OK;
+  return guarded([&] {
+    CallScope sc(&ws->owner->c);
+    workspace_destroy(ws->w);
+    delete ws;
+  });
+}
+
+rk_status rk_workspace_has_entry(rk_workspace* ws, uint64_t row, uint64_t col, int32_t* out) {
+  return guarded([&] {
+    if (!ws || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    *out = workspace_has_entry(*ws->w, row, col) ? 1 : 0;
+  });
+}
+
+rk_status rk_workspace_row_lonely_in_block(rk_workspace* ws, uint64_t d, uint64_t row, int32_t* out) {
+  return guarded([&] {
+    if (!ws || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    std::vector<uint64_t> r;
+    workspace_lonely(*ws->w, d, row, row + 1, r);
+    *out = r.empty() ? 0 : 1;
+  });
+}
+
+rk_status rk_workspace_lonely_rows(rk_workspace* ws, uint64_t d, uint64_t* rows_out, uint64_t* n_out) {
+  return guarded([&] {
+    if (!ws || !n_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    std::vector<uint64_t> r;
+    workspace_lonely(*ws->w, d, 0, UINT64_MAX, r);
+    if (!r.empty() && !rows_out) fail(RK_INVALID_ARGUMENT, "rows_out is NULL");
+    std::copy(r.begin(), r.end(), rows_out);
+    *n_out = r.size();
+  });
+}
+
+rk_status rk_workspace_neighbor_columns(rk_workspace* ws, uint64_t d, uint64_t row, uint64_t* cols_out,
+                                        uint64_t* n_out) {
+  return guarded([&] {
+    if (!ws || !n_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    std::vector<uint64_t> cols;
+    workspace_neighbor_columns(*ws->w, d, row, cols);
+    if (!cols.empty() && !cols_out) fail(RK_INVALID_ARGUMENT, "cols_out is NULL");
+    std::copy(cols.begin(), cols.end(), cols_out);
+    *n_out = cols.size();
+  });
+}
+
+rk_status rk_workspace_insert(rk_workspace* ws, uint64_t row, uint64_t col) {
+  return guarded([&] {
+    if (!ws) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    workspace_insert(*ws->w, row, col);
+  });
+}
+
+rk_status rk_workspace_to_matrix(rk_workspace* ws, rk_sparse* out) {
+  return guarded([&] {
+    if (!ws || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    CallScope sc(&ws->owner->c);
+    std::memset(out, 0, sizeof *out);
+    workspace_to_matrix(*ws->w, *out);
+  });
+}
+
 // ---- evaluation metrics (rk_eval.cu) ----
 rk_status rk_dev_sigma_error(rk_ctx* ctx, const double* d_sigma_hat, uint64_t n_hat, const double* d_sigma_ref,
                              uint64_t n_ref, double* out) {

@@ -327,6 +327,16 @@ struct DevEdges {  // repair edges in report order
 };
 void apply_edges(const DevMatrix& a, const DevEdges& e, DevMatrix& out, cudaStream_t s);
 
+// rk_workspace.cu: RepairWorkspace's single-row API on the device
+struct Workspace;
+Workspace* workspace_create(Ctx& c, const rk_sparse_view& a, uint64_t block_count);
+void workspace_destroy(Workspace* w);
+bool workspace_has_entry(Workspace& w, uint64_t row, uint64_t col);
+void workspace_lonely(Workspace& w, uint64_t d, uint64_t r_lo, uint64_t r_hi, std::vector<uint64_t>& out);
+void workspace_neighbor_columns(Workspace& w, uint64_t d, uint64_t row, std::vector<uint64_t>& out);
+void workspace_insert(Workspace& w, uint64_t row, uint64_t col);
+void workspace_to_matrix(Workspace& w, rk_sparse& out);
+
 // rk_repair.cu
 struct RepairOut {
   DevEdges edges;

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <map>
+
 #include "rk_pipeline.cuh"
 
 namespace rk {
@@ -57,20 +59,41 @@ __global__ void stack_r(const double* ra, uint32_t ha, const double* rb, uint32_
 }
 
 // leaf = records [r0, r1) of P^T stacked: column-major h x n
-__global__ void gather_leaf(const double* payload, const uint64_t* off, const uint32_t* kept, uint32_t r0,
-                            uint32_t r1, uint32_t n, uint32_t h, double* out) {
+// the leaf's stacked P^T rows: the first eff[rec] columns of each record (row-major
+// n x kept[rec]); the columns past eff are exactly zero (see record_effective_cols)
+__global__ void gather_leaf(const double* payload, const uint64_t* off, const uint32_t* kept, const uint32_t* eff,
+                            uint32_t r0, uint32_t r1, uint32_t n, uint32_t h, double* out) {
   uint32_t base = 0;
   for (uint32_t rec = r0; rec < r1; ++rec) {
-    const uint32_t k = kept[rec];
+    const uint32_t k = kept[rec], e = eff[rec];
     const double* src = payload + off[rec];
-    const uint64_t total = (uint64_t)k * n;
+    const uint64_t total = (uint64_t)e * n;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
-      const uint32_t j = (uint32_t)(t % k), col = (uint32_t)(t / k);  // payload: row-major n x k
+      const uint32_t j = (uint32_t)(t % e), col = (uint32_t)(t / e);  // payload: row-major n x k
       out[(base + j) + (uint64_t)col * h] = src[(uint64_t)col * k + j];
     }
-    base += k;
+    base += e;
   }
+}
+
+// eff[rec] = 1 + the last column of record rec holding a nonzero (0: none). The
+// finalize writes a record's columns in descending sigma, and a column of sigma 0
+// is exactly zero, so the columns past eff are zero: rows of P^T that change
+// neither P P^T nor its R factor (c3: ~385 of every block's 512). One CTA per record.
+__global__ void record_effective_cols(const double* payload, const uint64_t* off, const uint32_t* kept, uint32_t n,
+                                      uint32_t r0, uint32_t* eff) {
+  __shared__ uint32_t s_max;
+  const uint32_t rec = r0 + blockIdx.x, k = kept[rec];
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  const double* src = payload + off[rec];
+  uint32_t m = 0;
+  for (uint64_t t = threadIdx.x; t < (uint64_t)n * k; t += blockDim.x)
+    if (src[t] != 0.0) m = max(m, (uint32_t)(t % k) + 1);
+  if (m) atomicMax(&s_max, m);
+  __syncthreads();
+  if (threadIdx.x == 0) eff[rec] = s_max;
 }
 
 // row-major rows x k (payload) -> column-major rows x k at dst (ld rows)
@@ -263,6 +286,18 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   std::vector<char> done(nblk, 0);
   for (uint64_t i = 0; i < nblk; ++i) done[i] = skip[i];
 
+  // the Jacobi width for a wide block of n < M real columns: planned for n rounded up
+  // to 32 (few distinct widths, so few launches)
+  std::map<uint32_t, uint32_t> pad_cache;
+  auto narrow_pad = [&](uint32_t n) {
+    const uint32_t r = std::min<uint32_t>(M, (n + 31) & ~31u);
+    auto it = pad_cache.find(r);
+    if (it != pad_cache.end()) return it->second;
+    const uint32_t pd = std::min<uint32_t>(cols_pad_full, jacobi_cols_pad(M, r, false, c.smem_optin));
+    pad_cache[r] = pd;
+    return pd;
+  };
+
   // Jacobi + finalize of a set of W slots; records stats and writes payloads
   std::vector<double> sigma_host;  // sorted sigma of the Gram-route slots (read with the Jacobi stats)
   auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
@@ -274,19 +309,27 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     DBuf<uint32_t> order((uint64_t)nb * cols_pad_full, s);
     DBuf<double> fscratch((uint64_t)nb * cols_pad_full, s);
     stats.zero();
-    std::vector<JacobiJob> jj(nb);
+    // A wide block (n_d < M real columns: the compacted Householder route) runs its
+    // tournament over a width planned for its own n_d, not over M: the columns past
+    // n_d are zero and would only lengthen every sweep (c3: ~130 of 512). The width
+    // is a function of the block's own data, so results do not depend on batching.
+    // Jobs of one width share a launch; the finalize still sees cols_pad_full
+    // columns (the slot's tail is zero: sigma 0, deficient).
+    std::map<uint32_t, std::vector<JacobiJob>> by_pad;
     for (size_t q = 0; q < nb; ++q) {
-      jj[q].w = slots[q];
-      jj[q].v = nullptr;
-      jj[q].rows = M;
-      jj[q].cols = std::max<uint32_t>(cols[q], 1);
-      jj[q].cols_pad = cols_pad_full;
-      jj[q].alpha = alpha.get() + (uint64_t)q * cols_pad_full;
-      jj[q].stats = stats.get() + 8 * q;
-      jj[q].gram_ok = gram_ok ? 1u : 0u;
+      JacobiJob j{};
+      j.w = slots[q];
+      j.v = nullptr;
+      j.rows = M;
+      j.cols = std::max<uint32_t>(cols[q], 1);
+      j.cols_pad = j.cols >= M ? cols_pad_full : narrow_pad(j.cols);
+      j.alpha = alpha.get() + (uint64_t)q * cols_pad_full;
+      j.stats = stats.get() + 8 * q;
+      j.gram_ok = gram_ok ? 1u : 0u;
+      by_pad[j.cols_pad].push_back(j);
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
-    jacobi_batched(jj, s, c.num_sms, c.smem_optin);
+    for (auto& kv : by_pad) jacobi_batched(kv.second, s, c.num_sms, c.smem_optin);
     RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
     prof_mark(s, "blk jacobi");
     std::vector<FinalJob> fj(nb);
@@ -634,15 +677,32 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   DBuf<uint32_t> dkept(kept.size(), s);
   to_device(doff.get(), offset.data(), offset.size(), s);
   to_device(dkept.get(), kept.data(), kept.size(), s);
+  // the leaves keep the record grouping of `kept` (data-independent, so a shard's
+  // subtree is a node of the whole tree), but stack only each record's nonzero columns
+  const uint32_t rec_lo = leaves[leaf_lo].r0, rec_hi = leaves[leaf_hi - 1].r1;
+  DBuf<uint32_t> deff(kept.size(), s);
+  if (rec_hi > rec_lo) {
+    record_effective_cols<<<rec_hi - rec_lo, 256, 0, s>>>(payload, doff.get(), dkept.get(), M, rec_lo, deff.get());
+    RK_LAUNCH_CHECK();
+  }
+  std::vector<uint32_t> heff;
+  to_host(heff, deff.get(), kept.size(), s);
+  sync(s);
   std::vector<DBuf<double>> bufs;
   std::vector<std::vector<LeafRef>> tree(1);
   for (size_t l = leaf_lo; l < leaf_hi; ++l) {
     const TreeLeaf& L = leaves[l];
-    bufs.emplace_back((uint64_t)L.height * M, s);
-    gather_leaf<<<grid_for((uint64_t)L.height * M), 256, 0, s>>>(payload, doff.get(), dkept.get(), L.r0, L.r1, M,
-                                                                 L.height, bufs.back().get());
-    RK_LAUNCH_CHECK();
-    tree[0].push_back({bufs.back().get(), L.height, L.height, 0u});
+    uint32_t h = 0;
+    for (uint32_t r = L.r0; r < L.r1; ++r) h += heff[r];
+    const uint32_t hb = std::max<uint32_t>(h, 1);  // an all-zero leaf: one zero row
+    bufs.emplace_back((uint64_t)hb * M, s);
+    if (h == 0) bufs.back().zero();
+    else {
+      gather_leaf<<<grid_for((uint64_t)h * M), 256, 0, s>>>(payload, doff.get(), dkept.get(), deff.get(), L.r0, L.r1,
+                                                            M, h, bufs.back().get());
+      RK_LAUNCH_CHECK();
+    }
+    tree[0].push_back({bufs.back().get(), hb, hb, 0u});
   }
   std::vector<DBuf<double>> roots;
   tsqr_forest(c, M, tree, roots);

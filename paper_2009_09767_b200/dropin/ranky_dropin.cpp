@@ -21,15 +21,15 @@
 //   pipeline.cpp:11-16 run_block_task                             -> rk_run_block_tasks
 //   pipeline.cpp:18-59 proxy_from_records                         (host concatenation)
 //   pipeline.cpp:61-121 run_pipeline                              -> rk_run_pipeline
-// RepairWorkspace's single-row methods (repair.cpp:52-160) are an interactive,
-// host-side API; the drop-in does not reimplement them on the CPU and throws
-// std::logic_error instead (ranky::repair is the supported entry point).
+//   repair.cpp:52-160  RepairWorkspace                            -> rk_workspace_* (device
+//                      adjacency + inserted edges; the caller's KeyedRng draws on the host)
 #include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "ranky/block_record.hpp"
@@ -145,9 +145,40 @@ RepairReport report_of(const rk_repair_report& r) {
   return rep;
 }
 
-[[noreturn]] void no_workspace() {
-  throw std::logic_error(
-      "RepairWorkspace's single-row API is not part of the B200 drop-in; call ranky::repair");
+// RepairWorkspace's state lives in a device workspace (rk_workspace_*). The class
+// layout is the reference's (repair.hpp:80-86: no destructor hook, no spare member),
+// so the handle is kept in a registry keyed by the object's address: created by the
+// constructor, replaced when a new workspace is constructed at the same address (the
+// old object is then necessarily dead), released at exit. The reference members
+// origin_ / partition_ are set as in repair.cpp:52-63; row_cols_ / col_rows_ stay
+// empty (the adjacency is on the device). A copied workspace has no handle of its
+// own and reports std::logic_error. Each workspace owns its context (any thread may
+// use it; calls on one workspace must not overlap, as for the reference object).
+// Handles still registered at exit are left to process teardown.
+struct WsHandle {
+  rk_ctx* ctx = nullptr;
+  rk_workspace* ws = nullptr;
+};
+struct WorkspaceRegistry {
+  std::mutex mu;
+  std::unordered_map<const void*, WsHandle> map;
+};
+WorkspaceRegistry& registry() {
+  static WorkspaceRegistry* r = new WorkspaceRegistry;  // never destroyed: see above
+  return *r;
+}
+void release(WsHandle& h) {
+  rk_workspace_destroy(h.ws);
+  rk_ctx_destroy(h.ctx);
+  h = WsHandle{};
+}
+rk_workspace* workspace_of(const void* self) {
+  WorkspaceRegistry& r = registry();
+  std::lock_guard<std::mutex> lk(r.mu);
+  auto it = r.map.find(self);
+  if (it == r.map.end())
+    throw std::logic_error("RepairWorkspace: no device workspace for this object (copies are not supported)");
+  return it->second.ws;
 }
 
 }  // namespace
@@ -192,16 +223,85 @@ std::vector<std::size_t> find_lonely_rows(const SparseMatrix& a, const BlockPart
   return std::vector<std::size_t>(out.begin(), out.begin() + n);
 }
 
-RepairWorkspace::RepairWorkspace(const SparseMatrix&, const BlockPartition&) { no_workspace(); }
-std::size_t RepairWorkspace::apply_random(std::size_t, std::size_t, KeyedRng&) { no_workspace(); }
-std::optional<std::size_t> RepairWorkspace::apply_neighbor(std::size_t, std::size_t, KeyedRng&) { no_workspace(); }
-std::vector<std::size_t> RepairWorkspace::apply_neighbor_random(std::size_t, std::size_t, KeyedRng&) {
-  no_workspace();
+// ---- RepairWorkspace (repair.cpp:52-160) on rk_workspace_* ----------------------
+RepairWorkspace::RepairWorkspace(const SparseMatrix& a, const BlockPartition& p) : origin_(&a), partition_(&p) {
+  if (p.total_cols() != a.cols()) throw std::invalid_argument("partition does not match matrix columns");
+  require_uniform(p);
+  const rk_sparse_view v = view_of(a);
+  WsHandle h;
+  int dev = 0;
+  if (const char* e = std::getenv("RANKY_DEVICE")) dev = std::atoi(e);
+  check(rk_ctx_create(dev, &h.ctx));
+  const rk_status st = rk_workspace_create(h.ctx, &v, p.block_count(), &h.ws);
+  if (st != RK_OK) {
+    rk_ctx_destroy(h.ctx);
+    check(st);  // rk_last_error() still holds the create's message
+  }
+  WorkspaceRegistry& r = registry();
+  std::lock_guard<std::mutex> lk(r.mu);
+  auto it = r.map.find(this);
+  if (it != r.map.end()) release(it->second);
+  r.map[this] = h;
 }
-bool RepairWorkspace::has_entry(std::size_t, std::size_t) const { no_workspace(); }
-bool RepairWorkspace::row_lonely_in_block(std::size_t, std::size_t) const { no_workspace(); }
-std::vector<std::size_t> RepairWorkspace::lonely_rows(std::size_t) const { no_workspace(); }
-SparseMatrix RepairWorkspace::to_matrix() const { no_workspace(); }
+
+void RepairWorkspace::insert(std::size_t row, std::size_t col) { check(rk_workspace_insert(workspace_of(this), row, col)); }
+
+std::size_t RepairWorkspace::apply_random(std::size_t d, std::size_t row, KeyedRng& rng) {
+  const ColumnRange& range = partition_->range(d);
+  const std::size_t col = range.begin + rng.below(range.width());
+  insert(row, col);
+  return col;
+}
+
+std::optional<std::size_t> RepairWorkspace::apply_neighbor(std::size_t d, std::size_t row, KeyedRng& rng) {
+  const ColumnRange& range = partition_->range(d);
+  std::vector<uint64_t> cols(range.width() ? range.width() : 1);
+  uint64_t n = 0;
+  check(rk_workspace_neighbor_columns(workspace_of(this), d, row, cols.data(), &n));
+  if (n == 0) return std::nullopt;  // no draw on an empty set (repair.cpp:127)
+  const std::size_t col = cols[rng.below(n)];
+  insert(row, col);
+  return col;
+}
+
+std::vector<std::size_t> RepairWorkspace::apply_neighbor_random(std::size_t d, std::size_t row, KeyedRng& rng) {
+  std::vector<std::size_t> added;
+  if (auto col = apply_neighbor(d, row, rng)) added.push_back(*col);
+  const std::size_t random_col = apply_random(d, row, rng);
+  if (added.empty() || added.front() != random_col) added.push_back(random_col);
+  return added;
+}
+
+bool RepairWorkspace::has_entry(std::size_t row, std::size_t col) const {
+  int32_t f = 0;
+  check(rk_workspace_has_entry(workspace_of(this), row, col, &f));
+  return f != 0;
+}
+
+bool RepairWorkspace::row_lonely_in_block(std::size_t d, std::size_t row) const {
+  int32_t f = 0;
+  check(rk_workspace_row_lonely_in_block(workspace_of(this), d, row, &f));
+  return f != 0;
+}
+
+std::vector<std::size_t> RepairWorkspace::lonely_rows(std::size_t d) const {
+  std::vector<uint64_t> rows(origin_->rows() ? origin_->rows() : 1);
+  uint64_t n = 0;
+  check(rk_workspace_lonely_rows(workspace_of(this), d, rows.data(), &n));
+  return std::vector<std::size_t>(rows.begin(), rows.begin() + n);
+}
+
+SparseMatrix RepairWorkspace::to_matrix() const {
+  rk_sparse rs{};
+  const rk_status st = rk_workspace_to_matrix(workspace_of(this), &rs);
+  if (st != RK_OK) {
+    rk_sparse_free(&rs);
+    check(st);
+  }
+  SparseMatrix m = sparse_of_rk(rs);
+  rk_sparse_free(&rs);
+  return m;
+}
 
 std::pair<SparseMatrix, RepairReport> repair(const SparseMatrix& a, const BlockPartition& p, RepairMethod method,
                                              std::uint64_t seed) {

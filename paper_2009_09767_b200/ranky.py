@@ -184,6 +184,14 @@ def lib():
         sig = {
             "rk_last_error": ([], C.c_char_p), "rk_last_residual": ([], dbl), "rk_abi_version": ([], i32),
             "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32),
+            "rk_workspace_create": ([vp, C.POINTER(_View), u64, C.POINTER(vp)], i32),
+            "rk_workspace_destroy": ([vp], i32),
+            "rk_workspace_has_entry": ([vp, u64, u64, C.POINTER(C.c_int32)], i32),
+            "rk_workspace_row_lonely_in_block": ([vp, u64, u64, C.POINTER(C.c_int32)], i32),
+            "rk_workspace_lonely_rows": ([vp, u64, pu64, pu64], i32),
+            "rk_workspace_neighbor_columns": ([vp, u64, u64, pu64, pu64], i32),
+            "rk_workspace_insert": ([vp, u64, u64], i32),
+            "rk_workspace_to_matrix": ([vp, C.POINTER(_Sparse)], i32),
             "rk_sigma_error": ([vp, pdbl, u64, pdbl, u64, pdbl], i32),
             "rk_align_signs": ([vp, pdbl, pdbl, u64, u64, pdbl, u64, pdbl], i32),
             "rk_left_vector_error": ([vp, pdbl, pdbl, u64, u64, pdbl, u64, pdbl], i32),
@@ -617,6 +625,127 @@ def keyed_rng_below(seed: int, block, row, bound, ctx: Context | None = None) ->
     _check(lib().rk_keyed_rng_below(_ctx(ctx), len(b), seed, b.ctypes.data_as(p), r.ctypes.data_as(p),
                                     bd.ctypes.data_as(p), out.ctypes.data_as(p)))
     return out
+
+
+_M64 = (1 << 64) - 1
+
+
+def _mix(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+class KeyedRng:
+    """The reference's generator object (proj/include/ranky/rng.hpp:11-25,
+    proj/src/rng.cpp:8-38): a caller-owned splitmix64 stream keyed by (seed, block,
+    row). RepairWorkspace draws from it on the host, as the reference does; the
+    batch repair evaluates the same streams on the device (keyed_rng_*)."""
+
+    def __init__(self, seed: int, block: int, row: int):
+        st = _mix((seed + 0x9E3779B97F4A7C15) & _M64)
+        st = _mix(st ^ ((block + 0xBF58476D1CE4E5B9) & _M64))
+        self.state = _mix(st ^ ((row + 0x94D049BB133111EB) & _M64))
+
+    def next(self) -> int:
+        self.state = (self.state + 0x9E3779B97F4A7C15) & _M64
+        return _mix(self.state)
+
+    def below(self, bound: int) -> int:
+        threshold = ((1 << 64) - bound) % bound
+        while True:
+            r = self.next()
+            if r >= threshold:
+                return r % bound
+
+    def unit(self) -> float:
+        return (self.next() >> 11) * 2.0 ** -53
+
+
+class RepairWorkspace:
+    """RepairWorkspace (proj/include/ranky/repair.hpp:56-87, proj/src/repair.cpp:52-160)
+    on a device workspace (rk_workspace_*: the matrix's CSR + CSC in HBM plus the
+    inserted edges). The neighbor scan runs on the device; the draws come from the
+    caller's KeyedRng on the host, where the reference makes them."""
+
+    def __init__(self, a: SparseMatrix, p: BlockPartition, ctx: Context | None = None):
+        if p.total_cols() != a.cols():
+            raise InvalidArgument("partition does not match matrix columns")
+        _uniform_or_raise(a, p)
+        self._a, self._p, self._ctx = a, p, ctx
+        self._h = C.c_void_p()
+        v = a._view()
+        _check(lib().rk_workspace_create(_ctx(ctx), C.byref(v), p.block_count(), C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib is not None:
+            _lib.rk_workspace_destroy(h)
+            self._h = C.c_void_p()
+
+    def _insert(self, row: int, col: int) -> None:
+        _check(lib().rk_workspace_insert(self._h, row, col))
+
+    def apply_random(self, d: int, row: int, rng: KeyedRng) -> int:
+        """repair.cpp:95-101"""
+        rg = self._p.range(d)
+        col = rg.begin + rng.below(rg.end - rg.begin)
+        self._insert(row, col)
+        return col
+
+    def neighbor_columns(self, d: int, row: int) -> np.ndarray:
+        """The NeighborChecker's candidate columns before the draw (repair.cpp:107-125)."""
+        rg = self._p.range(d)
+        out = np.zeros(max(1, rg.end - rg.begin), dtype=np.uint64)
+        n = C.c_uint64()
+        p = C.POINTER(C.c_uint64)
+        _check(lib().rk_workspace_neighbor_columns(self._h, d, row, out.ctypes.data_as(p), C.byref(n)))
+        return out[:n.value].astype(np.int64)
+
+    def apply_neighbor(self, d: int, row: int, rng: KeyedRng):
+        """repair.cpp:103-135: None (no draw, no edge) when no candidate column exists."""
+        cols = self.neighbor_columns(d, row)
+        if len(cols) == 0:
+            return None
+        col = int(cols[rng.below(len(cols))])
+        self._insert(row, col)
+        return col
+
+    def apply_neighbor_random(self, d: int, row: int, rng: KeyedRng) -> list[int]:
+        """repair.cpp:137-145"""
+        added = []
+        c = self.apply_neighbor(d, row, rng)
+        if c is not None:
+            added.append(c)
+        rc = self.apply_random(d, row, rng)
+        if not added or added[0] != rc:
+            added.append(rc)
+        return added
+
+    def has_entry(self, row: int, col: int) -> bool:
+        out = C.c_int32()
+        _check(lib().rk_workspace_has_entry(self._h, row, col, C.byref(out)))
+        return bool(out.value)
+
+    def row_lonely_in_block(self, d: int, row: int) -> bool:
+        out = C.c_int32()
+        _check(lib().rk_workspace_row_lonely_in_block(self._h, d, row, C.byref(out)))
+        return bool(out.value)
+
+    def lonely_rows(self, d: int) -> list[int]:
+        out = np.zeros(max(1, self._a.rows()), dtype=np.uint64)
+        n = C.c_uint64()
+        _check(lib().rk_workspace_lonely_rows(self._h, d, out.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(n)))
+        return [int(x) for x in out[:n.value]]
+
+    def to_matrix(self) -> SparseMatrix:
+        out = _Sparse()
+        st = lib().rk_workspace_to_matrix(self._h, C.byref(out))
+        try:
+            _check(st)
+            return _sparse_of(out)
+        finally:
+            lib().rk_sparse_free(C.byref(out))
 
 
 # ---------------------------------------------------------------------------

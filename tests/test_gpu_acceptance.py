@@ -25,3 +25,15 @@ def test_reference_acceptance_suite_on_b200_dropin():
     assert not failed, failed
     assert len(passed) == 8, text
     assert out.returncode == 0
+
+
+def test_reference_workspace_tests_on_b200_dropin():
+    """proj/tests/repair_test.cpp's RepairWorkspace cases (tests/c/workspace_dropin_test.cpp)
+    through the drop-in's RepairWorkspace (rk_workspace_* device workspace)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ranky_workspace_b200")
+    if not os.path.exists(exe):
+        pytest.skip("workspace drop-in test not built (needs the reference sources)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout + out.stderr)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout

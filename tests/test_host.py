@@ -141,3 +141,14 @@ def test_planted_generator_spectrum():
     z1 = configs.planted(64, 8192, 0.01, 64, 0.9, 1e-6, 3)
     assert np.array_equal(z0.coo()[1], z1.coo()[1])
     assert 0.5e-6 < np.std(z1.coo()[2] - z0.coo()[2]) < 2e-6
+
+
+def test_keyed_rng_host_object_kat():
+    # KeyedRng(0,0,0)'s first draws as the reference library produces them (SURVEY.md §8(c)
+    # lists the same three values, last first); repair_test.cpp:77-88
+    from paper_2009_09767_b200.ranky import KeyedRng
+    g = KeyedRng(0, 0, 0)
+    assert [g.next() for _ in range(3)] == [0x060599146f06297d, 0x0bc1da82f6532f86, 0x9cd8ff1831b74722]
+    assert 0 <= KeyedRng(42, 0, 8).below(1024) < 1024
+    u = KeyedRng(1, 2, 3).unit()
+    assert 0.0 <= u < 1.0
