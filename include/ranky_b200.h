@@ -361,6 +361,45 @@ RK_API rk_status rk_read_block_record(const char* path, uint32_t* block_index, u
 /* every record of `records` to "<path_prefix><block index>.rnky", payload CRCs on the GPU */
 RK_API rk_status rk_write_records(rk_ctx* ctx, const rk_records* records, const char* path_prefix);
 
+/* ---- library-owned multi-GPU runs --------------------------------------------
+ * The sharded protocol above, orchestrated by the library (DESIGN.md (e)):
+ *
+ * rk_multi_*: one process drives several devices (`devices` may repeat one device:
+ * its shards then share it). rk_multi_run_pipeline is rk_run_pipeline over the whole
+ * box -- every device uploads the matrix, factors its leaves; the M x M factors are
+ * exchanged by peer copies (NVLink with peer access), every shard finishes the same
+ * tree top; V rows and records are copied back from their owners concurrently.
+ * Results are bitwise those of one process per GPU with the same shard count.
+ *
+ * rk_dist_*: one process per GPU with the library's own NCCL communicator (NCCL
+ * opened at run time from libnccl.so.2). rank 0 makes the id (rk_nccl_unique_id),
+ * the caller ships it to the other ranks. rk_dist_full_svd returns this rank's
+ * outputs (sigma, U and V rows [col_lo, col_hi)).
+ *
+ * rk_dev_sharded_full_svd: the same with the caller's all-gather: allgather(user,
+ * d_mine, d_all, count) must gather `count` doubles from every rank into d_all in
+ * rank order (device pointers on the context's device, the context's stream
+ * synchronized before the call; the data must be in d_all when it returns). */
+typedef struct rk_multi rk_multi;
+typedef struct rk_dist rk_dist;
+typedef void (*rk_allgather_fn)(void* user, const double* d_mine, double* d_all, uint64_t count);
+RK_API rk_status rk_multi_create(const int32_t* devices, uint32_t n, rk_multi** out);
+RK_API rk_status rk_multi_destroy(rk_multi* m);
+RK_API rk_status rk_multi_run_pipeline(rk_multi* m, const rk_sparse_view* a, uint64_t block_count,
+                                       rk_method method, uint64_t keep, uint64_t seed, uint32_t flags,
+                                       uint64_t top_k, rk_pipeline_result* out);
+RK_API rk_status rk_nccl_unique_id(uint8_t id_out[128]);
+RK_API rk_status rk_dist_create(rk_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128], rk_dist** out);
+RK_API rk_status rk_dist_destroy(rk_dist* d);
+RK_API rk_status rk_dist_full_svd(rk_dist* d, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
+                                  uint64_t keep, uint64_t seed, uint32_t flags, uint64_t top_k,
+                                  rk_dev_outputs** out, rk_timing* timing, uint64_t* col_lo, uint64_t* col_hi);
+RK_API rk_status rk_dev_sharded_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count,
+                                         rk_method method, uint64_t keep, uint64_t seed, uint32_t flags,
+                                         uint64_t top_k, int32_t world, int32_t rank, rk_allgather_fn allgather,
+                                         void* user, rk_dev_outputs** out, rk_timing* timing, uint64_t* col_lo,
+                                         uint64_t* col_hi);
+
 #ifdef __cplusplus
 }
 #endif

@@ -198,6 +198,8 @@ struct rk_dev_shard {
   BlockStageResult blocks;
   std::vector<TreeLeaf> local;  // the shard's leaves, block indices relative to its first block
   bool has_records = false;
+  RepairOut repair_out;         // the (whole-matrix) repair report
+  uint64_t d_lo = 0;            // the shard's first block
 };
 
 namespace {
@@ -1196,7 +1198,7 @@ namespace {
 // (gram = false) or the Gram partial of the subtree (gram = true, records kept)
 void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method, uint64_t keep,
                   uint64_t seed, uint64_t leaf_lo, uint64_t leaf_hi, double* d_out, rk_dev_shard** shard_out,
-                  rk_timing* timing, bool gram) {
+                  rk_timing* timing, bool gram, bool keep_records = false) {
   check_ctx(ctx);
   if (!a || !shard_out || !d_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
   CallScope sc(&ctx->c);
@@ -1221,10 +1223,10 @@ void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_
   std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
   if (leaf_lo >= leaf_hi || leaf_hi > leaves.size()) fail(RK_OUT_OF_RANGE, "leaf range outside the merge tree");
   RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
-  RepairOut rep;
-  sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, rep);
+  sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, sh->repair_out);
   RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
   const uint64_t d_lo = leaves[leaf_lo].r0, d_hi = leaves[leaf_hi - 1].r1;
+  sh->d_lo = d_lo;
   BlockStageResult& br = sh->blocks;
   block_stage(c, *sh->rep(), sh->p, d_lo, d_hi, keep, br, nullptr);
   if (any_failure(br)) throw_block_failure(br, d_lo);
@@ -1241,7 +1243,8 @@ void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_
     DBuf<double> R;
     merge_subtree(c, br.payload.get(), br.offset, br.kept, M, sh->local, 0, sh->local.size(), R);
     RK_CUDA_CHECK(cudaMemcpyAsync(d_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice, s));
-    br.payload.release();
+    if (keep_records) sh->has_records = true;
+    else br.payload.release();
   }
   RK_CUDA_CHECK(cudaEventRecord(c.ev[6], s));
   sync(s);
@@ -1416,6 +1419,479 @@ rk_status rk_dev_shard_destroy(rk_dev_shard* shard) {
     CallScope sc(&shard->owner->c);
     sync(shard->owner->c.stream);
     delete shard;
+  });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Library-owned multi-GPU runs. One orchestration of the sharded protocol
+// (DESIGN.md (e)) with three exchanges for its one collective (the all-gather of
+// the ranks' M x M factors):
+//   rk_multi_*                one process drives several devices: a host barrier,
+//                             then every shard pulls the others' factors with peer
+//                             copies (NVLink when peer access is available)
+//   rk_dist_*                 one process per GPU: the library's own NCCL
+//                             communicator (libnccl.so.2 opened at run time),
+//                             ncclAllGather on the context's stream
+//   rk_dev_sharded_full_svd   one process per GPU, the caller's all-gather (e.g.
+//                             torch.distributed) as a callback
+// Per rank: factor its leaves (Gram partial; the TSQR factor when the Gram route
+// does not apply), exchange, finish; when the kappa guard rejects the summed Gram
+// (identically on every rank) the TSQR factors are exchanged and finished instead.
+
+#include <condition_variable>
+#include <dlfcn.h>
+#include <functional>
+#include <thread>
+
+#include <nccl.h>
+
+namespace {
+
+using Exchange = std::function<void(double* d_mine, double* d_all)>;  // all-gather of M*M doubles per rank
+
+struct ShardPlan {
+  uint64_t leaf_lo, leaf_hi, col_lo, col_hi;
+};
+
+ShardPlan plan_shard(uint64_t M, uint64_t cols, uint64_t D, uint64_t keep, int world, int rank) {
+  Partition p = make_partition(cols, D);
+  std::vector<uint32_t> kept(D);
+  for (uint64_t d = 0; d < D; ++d) {
+    const uint64_t w = p.end(d) - p.begin(d), k_full = std::min<uint64_t>(M, w);
+    kept[d] = (uint32_t)(keep == 0 ? k_full : std::min(keep, k_full));
+  }
+  const std::vector<TreeLeaf> leaves = merge_leaves(kept, (uint32_t)M);
+  const uint64_t n = leaves.size();
+  if (world < 1 || (uint64_t)world > n || rank < 0 || rank >= world)
+    fail(RK_INVALID_ARGUMENT, "cannot shard " + std::to_string(n) + " merge-tree leaves over " +
+                                  std::to_string(world) + " ranks");
+  const uint64_t per = n / world;
+  ShardPlan sp;
+  sp.leaf_lo = rank * per;
+  sp.leaf_hi = rank + 1 == world ? n : (rank + 1) * per;
+  sp.col_lo = p.begin(leaves[sp.leaf_lo].r0);
+  sp.col_hi = p.end(leaves[sp.leaf_hi - 1].r1 - 1);
+  return sp;
+}
+
+[[noreturn]] void rethrow_status(rk_status st) { fail(st, g_error); }
+void chk(rk_status st) {
+  if (st != RK_OK) rethrow_status(st);
+}
+
+struct RankRun {
+  rk_dev_shard* shard = nullptr;
+  rk_dev_outputs* out = nullptr;
+  rk_timing tf{}, tfin{};
+  ShardPlan plan{};
+  ~RankRun() {
+    if (out) rk_dev_outputs_free(out);
+    if (shard) rk_dev_shard_destroy(shard);
+  }
+};
+
+void sharded_run(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t D, rk_method method, uint64_t keep, uint64_t seed,
+                 uint32_t flags, uint64_t top_k, int world, int rank, const Exchange& ex, bool keep_records,
+                 RankRun& r) {
+  const uint64_t M = a->m.csr.rows;
+  r.plan = plan_shard(M, a->m.csr.cols, D, keep, world, rank);
+  const uint64_t mm = M * M;
+  DBuf<double> mine, all;
+  {
+    CallScope sc(&ctx->c);
+    mine.alloc(mm ? mm : 1, ctx->c.stream);
+    all.alloc(world * mm ? world * mm : 1, ctx->c.stream);
+    sync(ctx->c.stream);
+  }
+  bool gram = gram_merge_eligible((uint32_t)M);
+  try {
+    shard_factor(ctx, a, D, method, keep, seed, r.plan.leaf_lo, r.plan.leaf_hi, mine.get(), &r.shard, &r.tf, gram,
+                 keep_records);
+  } catch (const Error& e) {
+    if (e.code != RK_GRAM_REJECTED) throw;
+    gram = false;
+    shard_factor(ctx, a, D, method, keep, seed, r.plan.leaf_lo, r.plan.leaf_hi, mine.get(), &r.shard, &r.tf, false,
+                 keep_records);
+  }
+  ex(mine.get(), all.get());
+  if (gram) {
+    const rk_status st = rk_dev_shard_finish_gram(ctx, r.shard, all.get(), world, flags, top_k, r.plan.col_lo,
+                                                  r.plan.col_hi, &r.out, &r.tfin);
+    if (st != RK_GRAM_REJECTED) {
+      chk(st);
+      return;
+    }
+    chk(rk_dev_shard_tsqr(ctx, r.shard, mine.get()));
+    ex(mine.get(), all.get());
+  }
+  chk(rk_dev_shard_finish(ctx, r.shard, all.get(), world, flags, top_k, r.plan.col_lo, r.plan.col_hi, &r.out,
+                          &r.tfin));
+}
+
+void add_timing(rk_timing& t, const RankRun& r) {
+  t.repair_ms = std::max(t.repair_ms, r.tf.repair_ms);
+  t.blocks_ms = std::max(t.blocks_ms, r.tf.blocks_ms);
+  t.merge_ms = std::max(t.merge_ms, r.tf.merge_ms + r.tfin.merge_ms);
+  t.recover_ms = std::max(t.recover_ms, r.tfin.recover_ms);
+  t.total_ms = std::max(t.total_ms, r.tf.total_ms + r.tfin.total_ms);
+  t.qr_ms = std::max(t.qr_ms, (double)r.tf.qr_ms);
+  t.jacobi_ms = std::max(t.jacobi_ms, (double)r.tf.jacobi_ms);
+  t.jacobi_sweeps_max = std::max(t.jacobi_sweeps_max, r.tf.jacobi_sweeps_max);
+  t.jacobi_rotations += r.tf.jacobi_rotations;
+  t.kernel_launches += r.tf.kernel_launches + r.tfin.kernel_launches;
+  t.jacobi_sweeps_sum += r.tf.jacobi_sweeps_sum;
+  t.qr_flops += r.tf.qr_flops;
+  t.jacobi_flops += r.tf.jacobi_flops;
+  t.merge_sweeps = r.tfin.merge_sweeps;
+  t.merge_rotations = r.tfin.merge_rotations;
+  t.merge_flops = std::max(t.merge_flops, r.tfin.merge_flops);
+}
+
+// a host barrier that a failing shard can break (the others then fail too instead of waiting)
+struct Barrier {
+  std::mutex m;
+  std::condition_variable cv;
+  int n, count = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  explicit Barrier(int n_) : n(n_) {}
+  void wait() {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) fail(RK_RUNTIME, "another shard failed");
+    const uint64_t g = gen;
+    if (++count == n) {
+      count = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    cv.wait(lk, [&] { return gen != g || broken; });
+    if (gen == g) fail(RK_RUNTIME, "another shard failed");
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
+// ---- NCCL, opened at run time ----
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("libnccl.so.2 not found: ") + dlerror();
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.comm_destroy || !api.error_string)
+      err = "libnccl.so.2 lacks a required symbol";
+  });
+  if (!err.empty()) fail(RK_RUNTIME, err);
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(RK_RUNTIME, std::string(what) + ": " + nccl().error_string(r));
+}
+
+}  // namespace
+
+struct rk_multi {
+  std::vector<int> devices;
+  std::vector<rk_ctx*> ctx;
+};
+
+struct rk_dist {
+  rk_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int world = 0, rank = 0;
+};
+
+extern "C" {
+
+rk_status rk_multi_create(const int32_t* devices, uint32_t n, rk_multi** out) {
+  return guarded([&] {
+    if (!devices || !n || !out) fail(RK_INVALID_ARGUMENT, "rk_multi_create: no devices");
+    auto m = std::make_unique<rk_multi>();
+    for (uint32_t g = 0; g < n; ++g) {
+      rk_ctx* c = nullptr;
+      const rk_status st = rk_ctx_create(devices[g], &c);
+      if (st != RK_OK) {
+        for (rk_ctx* x : m->ctx) rk_ctx_destroy(x);
+        rethrow_status(st);
+      }
+      m->ctx.push_back(c);
+      m->devices.push_back(devices[g]);
+    }
+    // peer access between distinct devices (the factor exchange then runs over NVLink)
+    for (uint32_t i = 0; i < n; ++i)
+      for (uint32_t j = 0; j < n; ++j) {
+        const int a = devices[i], b = devices[j];
+        int can = 0;
+        if (a == b || cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) continue;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(a);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        cudaGetLastError();
+        cudaSetDevice(prev);
+      }
+    *out = m.release();
+  });
+}
+
+rk_status rk_multi_destroy(rk_multi* m) {
+  if (!m) return RK_OK;
+  for (rk_ctx* c : m->ctx) rk_ctx_destroy(c);
+  delete m;
+  return RK_OK;
+}
+
+rk_status rk_multi_run_pipeline(rk_multi* m, const rk_sparse_view* a, uint64_t block_count, rk_method method,
+                                uint64_t keep, uint64_t seed, uint32_t flags, uint64_t top_k,
+                                rk_pipeline_result* out) {
+  return guarded([&] {
+    if (!m || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    check_view(a);
+    std::memset(out, 0, sizeof *out);
+    const int G = (int)m->ctx.size();
+    const uint64_t M = a->rows;
+    const uint64_t mm = M * M;
+    std::vector<rk_dev_matrix*> dms(G, nullptr);
+    std::vector<std::unique_ptr<RankRun>> runs(G);
+    std::vector<double*> mines(G, nullptr);
+    std::vector<rk_status> status(G, RK_OK);
+    std::vector<std::string> errors(G);
+    Barrier bar(G);
+    auto worker = [&](int g) {
+      try {
+        rk_ctx* ctx = m->ctx[g];
+        chk(rk_dev_matrix_create(ctx, a, &dms[g]));
+        runs[g] = std::make_unique<RankRun>();
+        Exchange ex = [&, g, ctx](double* mine, double* all) {
+          mines[g] = mine;
+          bar.wait();  // every shard's factor is written (each synchronized its stream)
+          {
+            CallScope sc(&ctx->c);
+            for (int h = 0; h < G; ++h) {
+              if (m->devices[h] == m->devices[g])
+                RK_CUDA_CHECK(cudaMemcpyAsync(all + h * mm, mines[h], mm * 8, cudaMemcpyDeviceToDevice,
+                                              ctx->c.stream));
+              else
+                RK_CUDA_CHECK(cudaMemcpyPeerAsync(all + h * mm, m->devices[g], mines[h], m->devices[h], mm * 8,
+                                                  ctx->c.stream));
+            }
+            sync(ctx->c.stream);
+          }
+          bar.wait();  // nobody rewrites its factor (the TSQR fallback) while another copies it
+        };
+        sharded_run(ctx, dms[g], block_count, method, keep, seed, flags, top_k, G, g, ex,
+                    (flags & RK_WANT_RECORDS) != 0, *runs[g]);
+      } catch (const Error& e) {
+        status[g] = e.code;
+        errors[g] = e.what();
+        bar.abort();
+      } catch (const std::exception& e) {
+        status[g] = RK_RUNTIME;
+        errors[g] = e.what();
+        bar.abort();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) th.emplace_back(worker, g);
+    for (auto& t : th) t.join();
+    auto cleanup = [&] {
+      runs.clear();
+      for (int g = 0; g < G; ++g)
+        if (dms[g]) rk_dev_matrix_destroy(dms[g]);
+    };
+    for (int g = 0; g < G; ++g)
+      if (status[g] != RK_OK && errors[g] != "another shard failed") {
+        cleanup();
+        fail(status[g], errors[g]);
+      }
+    for (int g = 0; g < G; ++g)
+      if (status[g] != RK_OK) {
+        cleanup();
+        fail(status[g], errors[g]);
+      }
+    try {
+      // host outputs: sigma, U from shard 0 (every shard holds the same), V rows and
+      // records from their owners, copied concurrently on every device's stream
+      RankRun& r0 = *runs[0];
+      Ctx& c0 = m->ctx[0]->c;
+      const rk_dev_outputs* o0 = r0.out;
+      const uint64_t k = o0->k_sigma, r = o0->k_v;
+      out->svd.u_rows = M;
+      out->svd.u_cols = k;
+      out->svd.n_sigma = k;
+      {
+        CallScope sc(&c0);
+        out->svd.u = host_copy(o0->d_u, M * k, c0.stream);
+        out->svd.sigma = host_copy(o0->d_sigma, k, c0.stream);
+        report_to_host(r0.shard->repair_out, r0.shard->p, &out->report, c0.stream);
+        if (flags & RK_WANT_REPAIRED) csr_to_entries_host(r0.shard->rep()->csr, out->repaired, c0.stream);
+        sync(c0.stream);
+      }
+      if (flags & RK_WANT_V) {
+        out->svd.has_v = 1;
+        out->svd.v_rows = a->cols;
+        out->svd.v_cols = r;
+        out->svd.v = host_alloc<double>(a->cols * r);
+      }
+      std::vector<uint32_t> kept_all;
+      std::vector<uint64_t> off_all;
+      if (flags & RK_WANT_RECORDS) {
+        const Partition p = make_partition(a->cols, block_count);
+        for (uint64_t d = 0; d < block_count; ++d) {
+          const uint64_t w = p.end(d) - p.begin(d), kf = std::min<uint64_t>(M, w);
+          kept_all.push_back((uint32_t)(keep == 0 ? kf : std::min(keep, kf)));
+        }
+        uint64_t tot = 0;
+        for (uint32_t kk : kept_all) {
+          off_all.push_back(tot);
+          tot += M * kk;
+        }
+        out->records.n_records = block_count;
+        out->records.rows = M;
+        out->records.kept = host_alloc<uint32_t>(block_count);
+        out->records.offset = host_alloc<uint64_t>(block_count);
+        std::copy(kept_all.begin(), kept_all.end(), out->records.kept);
+        std::copy(off_all.begin(), off_all.end(), out->records.offset);
+        out->records.payload = host_alloc<double>(tot ? tot : 1);
+      }
+      for (int g = 0; g < G; ++g) {
+        RankRun& rr = *runs[g];
+        Ctx& c = m->ctx[g]->c;
+        CallScope sc(&c);
+        if ((flags & RK_WANT_V) && r && rr.out->d_v)
+          RK_CUDA_CHECK(cudaMemcpyAsync(out->svd.v + rr.plan.col_lo * r, rr.out->d_v,
+                                        (rr.plan.col_hi - rr.plan.col_lo) * r * 8, cudaMemcpyDeviceToHost, c.stream));
+        if (flags & RK_WANT_RECORDS) {
+          const BlockStageResult& br = rr.shard->blocks;
+          const uint64_t d0 = rr.shard->d_lo;
+          if (!br.offset.empty()) {
+            const uint64_t n = br.offset.back() + M * br.kept.back();
+            RK_CUDA_CHECK(cudaMemcpyAsync(out->records.payload + off_all[d0], br.payload.get(), n * 8,
+                                          cudaMemcpyDeviceToHost, c.stream));
+          }
+        }
+      }
+      for (int g = 0; g < G; ++g) {
+        CallScope sc(&m->ctx[g]->c);
+        sync(m->ctx[g]->c.stream);
+        add_timing(out->timing, *runs[g]);
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+rk_status rk_nccl_unique_id(uint8_t id_out[128]) {
+  return guarded([&] {
+    if (!id_out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    static_assert(sizeof id == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id_out, &id, 128);
+  });
+}
+
+rk_status rk_dist_create(rk_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128], rk_dist** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) fail(RK_INVALID_ARGUMENT, "bad rank / world");
+    CallScope sc(&ctx->c);
+    auto d = std::make_unique<rk_dist>();
+    d->ctx = ctx;
+    d->world = world;
+    d->rank = rank;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    nccl_check(nccl().comm_init_rank(&d->comm, world, uid, rank), "ncclCommInitRank");
+    *out = d.release();
+  });
+}
+
+rk_status rk_dist_destroy(rk_dist* d) {
+  if (!d) return RK_OK;
+  return guarded([&] {
+    if (d->comm) nccl().comm_destroy(d->comm);
+    delete d;
+  });
+}
+
+rk_status rk_dist_full_svd(rk_dist* d, const rk_dev_matrix* a, uint64_t block_count, rk_method method, uint64_t keep,
+                           uint64_t seed, uint32_t flags, uint64_t top_k, rk_dev_outputs** out, rk_timing* timing,
+                           uint64_t* col_lo, uint64_t* col_hi) {
+  return guarded([&] {
+    if (!d || !a || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    const uint64_t mm = a->m.csr.rows * a->m.csr.rows;
+    Exchange ex = [&](double* mine, double* all) {
+      CallScope sc(&d->ctx->c);
+      nccl_check(nccl().all_gather(mine, all, mm, ncclFloat64, d->comm, d->ctx->c.stream), "ncclAllGather");
+      sync(d->ctx->c.stream);
+    };
+    RankRun r;
+    sharded_run(d->ctx, a, block_count, method, keep, seed, flags, top_k, d->world, d->rank, ex, false, r);
+    if (timing) {
+      std::memset(timing, 0, sizeof *timing);
+      add_timing(*timing, r);
+    }
+    if (col_lo) *col_lo = r.plan.col_lo;
+    if (col_hi) *col_hi = r.plan.col_hi;
+    *out = r.out;
+    r.out = nullptr;
+  });
+}
+
+rk_status rk_dev_sharded_full_svd(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_method method,
+                                  uint64_t keep, uint64_t seed, uint32_t flags, uint64_t top_k, int32_t world,
+                                  int32_t rank, rk_allgather_fn allgather, void* user, rk_dev_outputs** out,
+                                  rk_timing* timing, uint64_t* col_lo, uint64_t* col_hi) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!a || !out || !allgather) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    const uint64_t mm = a->m.csr.rows * a->m.csr.rows;
+    Exchange ex = [&](double* mine, double* all) {
+      {
+        CallScope sc(&ctx->c);
+        sync(ctx->c.stream);
+      }
+      allgather(user, mine, all, mm);
+    };
+    RankRun r;
+    sharded_run(ctx, a, block_count, method, keep, seed, flags, top_k, world, rank, ex, false, r);
+    if (timing) {
+      std::memset(timing, 0, sizeof *timing);
+      add_timing(*timing, r);
+    }
+    if (col_lo) *col_lo = r.plan.col_lo;
+    if (col_hi) *col_hi = r.plan.col_hi;
+    *out = r.out;
+    r.out = nullptr;
   });
 }
 

@@ -11,7 +11,8 @@
 // block. Cholesky squares the condition number, so the result is accepted only
 // when the block's kappa = sigma_max/sigma_min is small enough that the Gram's
 // rounding (~ M eps sigma_max^2) moves every singular value by less than
-// 1e-11 relative (kappa_max(M) = sqrt(2e-11 / (M eps))); otherwise -- and for a
+// 3e-11 relative, a third of the 1e-10 parity tolerance (kappa_max(M) =
+// sqrt(6e-11 / (M eps)): 46 at M = 256, 32 at 512); otherwise -- and for a
 // non-positive pivot -- the block is redone on the Householder path. The same
 // kernels give the merge's R_P from P P^T (SYRK over the records).
 #include <cooperative_groups.h>
@@ -680,6 +681,44 @@ void sparse_gram(const DevMatrix& m, const Partition& p, uint64_t d_lo, uint64_t
   RK_LAUNCH_CHECK();
 }
 
+namespace {
+// eff[rec] = 1 + the last column of record rec holding a nonzero (0: none). The
+// finalize writes a record's columns in descending sigma, and a column of sigma 0
+// is exactly zero, so the columns past eff are zero: rows of P^T that change
+// neither P P^T nor its R factor (c3: ~385 of every block's 512). One CTA per record.
+__global__ void record_effective_cols(const double* payload, const uint64_t* off, const uint32_t* kept, uint32_t n,
+                                      uint32_t r0, uint32_t* eff) {
+  __shared__ uint32_t s_max;
+  const uint32_t rec = r0 + blockIdx.x, k = kept[rec];
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  const double* src = payload + off[rec];
+  uint32_t m = 0;
+  for (uint64_t t = threadIdx.x; t < (uint64_t)n * k; t += blockDim.x)
+    if (src[t] != 0.0) m = max(m, (uint32_t)(t % k) + 1);
+  if (m) atomicMax(&s_max, m);
+  __syncthreads();
+  if (threadIdx.x == 0) eff[rec] = s_max;
+}
+}  // namespace
+
+std::vector<uint32_t> record_eff_cols(const double* payload, const std::vector<uint64_t>& offset,
+                                      const std::vector<uint32_t>& kept, uint32_t M, uint32_t r_lo, uint32_t r_hi,
+                                      cudaStream_t s) {
+  std::vector<uint32_t> eff(kept.size(), 0);
+  if (r_hi <= r_lo || !M) return eff;
+  DBuf<uint64_t> doff(offset.size(), s);
+  DBuf<uint32_t> dkept(kept.size(), s), deff(kept.size(), s);
+  to_device(doff.get(), offset.data(), offset.size(), s);
+  to_device(dkept.get(), kept.data(), kept.size(), s);
+  deff.zero();
+  record_effective_cols<<<r_hi - r_lo, 256, 0, s>>>(payload, doff.get(), dkept.get(), M, r_lo, deff.get());
+  RK_LAUNCH_CHECK();
+  to_host(eff, deff.get(), kept.size(), s);
+  sync(s);
+  return eff;
+}
+
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
                   uint32_t M, double* G, cudaStream_t s) {
   if (M % 8) fail(RK_RUNTIME, "records_gram: M must be a multiple of 8");
@@ -687,11 +726,14 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
   // M x M partial, so the chunk width grows with M to bound that buffer (c4:
   // 1024 records x 1024 columns -> 1024 partials of 8 MiB, not 4096)
   const uint32_t kChunk = M <= 256 ? 256u : 1024u;
+  // only each record's leading nonzero columns (record_eff_cols): the zero ones add
+  // nothing to P P^T (c3: ~385 of 512 per record)
+  const std::vector<uint32_t> eff = record_eff_cols(payload, offset, kept, M, 0, (uint32_t)kept.size(), s);
   std::vector<SyrkChunk> ch;
   for (size_t d = 0; d < kept.size(); ++d) {
-    if (!kept[d]) continue;
-    for (uint32_t j0 = 0; j0 < kept[d]; j0 += kChunk)
-      ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + kChunk)});
+    if (!eff[d]) continue;
+    for (uint32_t j0 = 0; j0 < eff[d]; j0 += kChunk)
+      ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(eff[d], j0 + kChunk)});
   }
   if (ch.empty()) {
     RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * M * M, s));
@@ -833,9 +875,9 @@ uint32_t cholesky_max_rows() { return 1280; }  // the panel buffer (M x 16 doubl
 bool gram_route_enabled() { return !tuning().householder_only; }
 
 double kappa_max(uint32_t M) {
-  // every sigma moves by < 1e-11 relative when M eps kappa^2 / 2 < 1e-11
+  // every sigma moves by < 3e-11 relative when M eps kappa^2 / 2 < 3e-11
   const double eps = 1.1102230246251565e-16;
-  return sqrt(2e-11 / ((double)std::max<uint32_t>(M, 1) * eps));
+  return sqrt(6e-11 / ((double)std::max<uint32_t>(M, 1) * eps));
 }
 
 }  // namespace rk

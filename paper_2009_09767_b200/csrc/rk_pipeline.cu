@@ -77,24 +77,6 @@ __global__ void gather_leaf(const double* payload, const uint64_t* off, const ui
   }
 }
 
-// eff[rec] = 1 + the last column of record rec holding a nonzero (0: none). The
-// finalize writes a record's columns in descending sigma, and a column of sigma 0
-// is exactly zero, so the columns past eff are zero: rows of P^T that change
-// neither P P^T nor its R factor (c3: ~385 of every block's 512). One CTA per record.
-__global__ void record_effective_cols(const double* payload, const uint64_t* off, const uint32_t* kept, uint32_t n,
-                                      uint32_t r0, uint32_t* eff) {
-  __shared__ uint32_t s_max;
-  const uint32_t rec = r0 + blockIdx.x, k = kept[rec];
-  if (threadIdx.x == 0) s_max = 0;
-  __syncthreads();
-  const double* src = payload + off[rec];
-  uint32_t m = 0;
-  for (uint64_t t = threadIdx.x; t < (uint64_t)n * k; t += blockDim.x)
-    if (src[t] != 0.0) m = max(m, (uint32_t)(t % k) + 1);
-  if (m) atomicMax(&s_max, m);
-  __syncthreads();
-  if (threadIdx.x == 0) eff[rec] = s_max;
-}
 
 // row-major rows x k (payload) -> column-major rows x k at dst (ld rows)
 __global__ void rowmajor_to_colmajor(const double* src, uint32_t rows, uint32_t k, double* dst) {
@@ -380,6 +362,15 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   const uint64_t budget = std::max<uint64_t>((uint64_t)(device_free_bytes(c, need_all * 3) * 0.4), 256ull << 20);
   prof_mark(s, "blk budget");
 
+  // compacted row counts (multi-entry columns, merged single-entry rows) of every block:
+  // the Householder route's plan, and a rank bound for route 1 (rank <= n_rows)
+  DBuf<uint32_t> counts(2 * nblk, s);
+  DBuf<double> single(nblk * (uint64_t)M, s);
+  compaction_counts(a, p, d_lo, d_hi, counts.get(), single.get(), s);
+  std::vector<uint32_t> hc;
+  to_host(hc, counts.get(), 2 * nblk, s);
+  sync(s);
+
   // ---- route 1: W = chol(A_d A_d^T), accepted when kappa <= kappa_max(M) ----
   if (gram_route_enabled() && M <= cholesky_max_rows()) {
     const double kmax = kappa_max(M);
@@ -387,6 +378,11 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     const uint64_t chunk = std::max<uint64_t>(1, budget / per_block);
     for (uint64_t i0 = 0; i0 < nblk; i0 += chunk) {
       const uint64_t i1 = std::min(nblk, i0 + chunk), nb = i1 - i0;
+      // a block whose compacted height is below M is rank-deficient: its Gram is singular
+      // and the Cholesky would only reject it (c3: every block, rank ~127 of 512)
+      bool any = false;
+      for (uint64_t i = i0; i < i1 && !any; ++i) any = !skip[i] && hc[2 * i] + hc[2 * i + 1] >= M;
+      if (!any) continue;
       DBuf<double> W(nb * M * cols_pad_full, s);
       W.zero();
       RK_CUDA_CHECK(cudaEventRecord(c.ev[8], s));
@@ -453,12 +449,6 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   for (uint64_t i = 0; i < nblk; ++i)
     if (!done[i]) todo.push_back(i);
   if (todo.empty()) return;
-  DBuf<uint32_t> counts(2 * nblk, s);
-  DBuf<double> single(nblk * (uint64_t)M, s);
-  compaction_counts(a, p, d_lo, d_hi, counts.get(), single.get(), s);
-  std::vector<uint32_t> hc;
-  to_host(hc, counts.get(), 2 * nblk, s);
-  sync(s);
   const uint64_t aux_sz = 2 * (uint64_t)M + (ceil_div(M, 16) + 1) * 256;
   // TSQR leaf height of the tall blocks: at least 2M, so every leaf is tall (a wide
   // leaf makes the pairwise combines, ~4/3 M^3 each, dominate: c5 3x the flops)
@@ -680,14 +670,9 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   // the leaves keep the record grouping of `kept` (data-independent, so a shard's
   // subtree is a node of the whole tree), but stack only each record's nonzero columns
   const uint32_t rec_lo = leaves[leaf_lo].r0, rec_hi = leaves[leaf_hi - 1].r1;
+  const std::vector<uint32_t> heff = record_eff_cols(payload, offset, kept, M, rec_lo, rec_hi, s);
   DBuf<uint32_t> deff(kept.size(), s);
-  if (rec_hi > rec_lo) {
-    record_effective_cols<<<rec_hi - rec_lo, 256, 0, s>>>(payload, doff.get(), dkept.get(), M, rec_lo, deff.get());
-    RK_LAUNCH_CHECK();
-  }
-  std::vector<uint32_t> heff;
-  to_host(heff, deff.get(), kept.size(), s);
-  sync(s);
+  to_device(deff.get(), heff.data(), heff.size(), s);
   std::vector<DBuf<double>> bufs;
   std::vector<std::vector<LeafRef>> tree(1);
   for (size_t l = leaf_lo; l < leaf_hi; ++l) {

@@ -79,6 +79,12 @@ void dense_svd_dev(Ctx& c, const double* a, uint32_t rows, uint32_t cols, DenseS
 // rk_gram.cu: Gram + Cholesky route (see the file header)
 void sparse_gram(const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
                  cudaStream_t s);
+// eff[d] for records [r_lo, r_hi) (0 elsewhere): 1 + the last column of record d with
+// a nonzero; the finalize writes columns by descending sigma and a sigma-0 column is
+// exactly zero, so the columns past eff[d] are zero
+std::vector<uint32_t> record_eff_cols(const double* payload, const std::vector<uint64_t>& offset,
+                                      const std::vector<uint32_t>& kept, uint32_t M, uint32_t r_lo, uint32_t r_hi,
+                                      cudaStream_t s);
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
                   uint32_t M, double* G, cudaStream_t s);
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
