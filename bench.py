@@ -386,7 +386,6 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, cfg)
 
-    import ctypes as C
 
     import numpy as np
     import torch
@@ -437,52 +436,25 @@ def main():
         from paper_2009_09767_b200 import shard as SH
         sp = SH.plan(M, cfg.cols, cfg.blocks, cfg.keep, ws, rank)
         lo, hi, c_lo, c_hi = sp.leaf_lo, sp.leaf_hi, sp.col_lo, sp.col_hi
-        roots = torch.empty((ws, M, M), dtype=torch.float64, device="cuda")
-        mine = torch.empty((M, M), dtype=torch.float64, device="cuda")
-
-        def gather():
+        def allgather(mine, alls):
+            """the library's one collective, on the caller's communicator (NCCL)"""
             if args.backend == "nccl":
-                torch.distributed.all_gather_into_tensor(roots, mine)
+                torch.distributed.all_gather_into_tensor(alls, mine)
             else:
-                parts = [torch.empty((M, M), dtype=torch.float64) for _ in range(ws)]
+                parts = [torch.empty(mine.numel(), dtype=torch.float64) for _ in range(ws)]
                 torch.distributed.all_gather(parts, mine.cpu())
-                roots.copy_(torch.stack(parts))
+                alls.copy_(torch.cat(parts).to(alls.device))
 
         def sharded(dmx, sink=None):
-            """this rank's share: factor its leaves, all-gather the subtree's Gram
-            partial (NCCL), finish the merge, V for its columns; the TSQR factors
-            instead when the Gram route is rejected (identically on every rank);
-            `sink(out)` sees the outputs"""
-            shard = C.c_void_p()
-            t = R.Timing()
-            fargs = (ctx.handle, dmx.handle, cfg.blocks, R._method(cfg.method), cfg.keep, cfg.seed, lo, hi,
-                     C.c_void_p(mine.data_ptr()), C.byref(shard), C.byref(t))
-            st = L.rk_dev_shard_factor_gram(*fargs)
-            gram = st == 0
-            if st == R.GRAM_REJECTED:
-                R._check(L.rk_dev_shard_factor(*fargs))
-            else:
-                R._check(st)
-            gather()
-            out = C.POINTER(R.DevOutputs)()
-            t2 = R.Timing()
-            gargs = (ctx.handle, shard, C.c_void_p(roots.data_ptr()), ws, R.WANT_V, cfg.top_k, c_lo, c_hi,
-                     C.byref(out), C.byref(t2))
-            st = L.rk_dev_shard_finish_gram(*gargs) if gram else L.rk_dev_shard_finish(*gargs)
-            if gram and st == R.GRAM_REJECTED:
-                R._check(L.rk_dev_shard_tsqr(ctx.handle, shard, C.c_void_p(mine.data_ptr())))
-                gather()
-                st = L.rk_dev_shard_finish(*gargs)
-            R._check(st)
+            """this rank's share, orchestrated by the library (rk_dev_sharded_full_svd):
+            factor its leaves, all-gather the subtree factors, finish the tree top
+            (the TSQR factors when the kappa guard rejects the Gram route), V for its
+            columns; `sink(out)` sees the outputs"""
+            out, t, _, _ = R.dev_sharded_full_svd(dmx, cfg.blocks, cfg.method, cfg.keep, cfg.seed, ws, rank,
+                                                  allgather, True, cfg.top_k)
             if sink:
                 sink(out)
             R.dev_outputs_free(out)
-            L.rk_dev_shard_destroy(shard)
-            t.merge_ms += t2.merge_ms
-            t.merge_flops += t2.merge_flops
-            t.merge_sweeps = t2.merge_sweeps
-            t.recover_ms = t2.recover_ms
-            t.kernel_launches += t2.kernel_launches
             return t
 
         def step():
@@ -601,8 +573,9 @@ def main():
         e2e = {"value": a.nnz() / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": a.nnz() * R.ENTRY_DTYPE.itemsize, "d2h_bytes_per_step": moved.get("d2h", 0),
                "ms_median": statistics.median(e2e_ms),
-               "path": "per rank: rk_dev_matrix_create(pinned host entries) + rk_dev_shard_factor + NCCL "
-                       "all_gather + rk_dev_shard_finish + D2H of sigma, U and the rank's V rows; max over ranks",
+               "path": "per rank: rk_dev_matrix_create(pinned host entries) + rk_dev_sharded_full_svd (the "
+                       "library's factor / NCCL all-gather / finish) + D2H of sigma, U and the rank's V rows; max "
+                       "over ranks",
                "bytes_note": "per rank"}
     if not args.no_e2e and ws == 1:
         pinned = torch.empty(a.nnz() * R.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)

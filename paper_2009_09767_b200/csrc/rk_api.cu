@@ -395,21 +395,32 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
     const uint64_t rmax = std::max<uint64_t>(1, top_k ? std::min<uint64_t>(top_k, M) : M);
     fr.v.alloc(a.csr.cols * rmax, s);
   }
+  RK_NVTX("rk.full_svd");
   RK_CUDA_CHECK(cudaEventRecord(ev0, s));
   prof_mark(s, "start");
-  fr.repaired = repair_and_apply(c, a, p, method, seed, fr.rep);
+  {
+    RK_NVTX("rk.repair");
+    fr.repaired = repair_and_apply(c, a, p, method, seed, fr.rep);
+  }
   prof_mark(s, "repair");
   const DevMatrix& rep = fr.repaired ? *fr.repaired : a;
   RK_CUDA_CHECK(cudaEventRecord(ev1, s));
-  block_stage(c, rep, p, 0, p.blocks, keep, fr.blocks, nullptr);
+  {
+    RK_NVTX("rk.blocks");
+    block_stage(c, rep, p, 0, p.blocks, keep, fr.blocks, nullptr);
+  }
   if (any_failure(fr.blocks)) throw_block_failure(fr.blocks, 0);
   RK_CUDA_CHECK(cudaEventRecord(ev2, s));
   prof_mark(s, "blocks (end)");
-  merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
+  {
+    RK_NVTX("rk.merge");
+    merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
+  }
   RK_CUDA_CHECK(cudaEventRecord(ev3, s));
   prof_mark(s, "merge (end)");
   if (!(flags & RK_WANT_RECORDS)) fr.blocks.payload.release();  // P is not an output: make room for V
   if (flags & RK_WANT_V) {
+    RK_NVTX("rk.recover_v");
     const uint32_t k = fr.merge.k;
     const uint32_t kk = (top_k && top_k < k) ? (uint32_t)top_k : k;
     std::vector<double> sig;
@@ -1222,6 +1233,7 @@ void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_
   }
   std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
   if (leaf_lo >= leaf_hi || leaf_hi > leaves.size()) fail(RK_OUT_OF_RANGE, "leaf range outside the merge tree");
+  RK_NVTX("rk.shard_factor");
   RK_CUDA_CHECK(cudaEventRecord(c.ev[3], s));
   sh->repaired = repair_and_apply(c, a->m, sh->p, method, seed, sh->repair_out);
   RK_CUDA_CHECK(cudaEventRecord(c.ev[4], s));
@@ -1495,6 +1507,7 @@ struct RankRun {
 void sharded_run(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t D, rk_method method, uint64_t keep, uint64_t seed,
                  uint32_t flags, uint64_t top_k, int world, int rank, const Exchange& ex, bool keep_records,
                  RankRun& r) {
+  RK_NVTX("rk.sharded_run");
   const uint64_t M = a->m.csr.rows;
   r.plan = plan_shard(M, a->m.csr.cols, D, keep, world, rank);
   const uint64_t mm = M * M;
@@ -1515,7 +1528,10 @@ void sharded_run(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t D, rk_method meth
     shard_factor(ctx, a, D, method, keep, seed, r.plan.leaf_lo, r.plan.leaf_hi, mine.get(), &r.shard, &r.tf, false,
                  keep_records);
   }
-  ex(mine.get(), all.get());
+  {
+    RK_NVTX("rk.exchange");
+    ex(mine.get(), all.get());
+  }
   if (gram) {
     const rk_status st = rk_dev_shard_finish_gram(ctx, r.shard, all.get(), world, flags, top_k, r.plan.col_lo,
                                                   r.plan.col_hi, &r.out, &r.tfin);

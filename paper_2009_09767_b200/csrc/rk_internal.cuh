@@ -1,6 +1,7 @@
 // rk_internal.cuh -- shared internals of libranky_b200 (not part of the ABI).
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -67,6 +68,18 @@ void reload_tuning();
 int device_sms(int device);  // cached per device
 
 void trace_launch(const char* file, int line);
+
+// NVTX stage ranges (nvtx3, header-only: free unless a tool such as nsys / ncu
+// --nvtx is attached): RK_NVTX("rk.blocks") opens a range for the enclosing scope
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+#define RK_NVTX_CAT2(a, b) a##b
+#define RK_NVTX_CAT(a, b) RK_NVTX_CAT2(a, b)
+#define RK_NVTX(name) ::rk::NvtxScope RK_NVTX_CAT(rk_nvtx_, __LINE__)(name)
 #define RK_LAUNCH_CHECK()                                                                    \
   do {                                                                                      \
     if (::rk::g_launch_counter) ++*::rk::g_launch_counter;                                   \

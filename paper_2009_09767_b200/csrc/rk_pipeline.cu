@@ -311,7 +311,10 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       by_pad[j.cols_pad].push_back(j);
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
-    for (auto& kv : by_pad) jacobi_batched(kv.second, s, c.num_sms, c.smem_optin);
+    {
+      RK_NVTX("rk.blocks.jacobi");
+      for (auto& kv : by_pad) jacobi_batched(kv.second, s, c.num_sms, c.smem_optin);
+    }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
     prof_mark(s, "blk jacobi");
     std::vector<FinalJob> fj(nb);
@@ -373,6 +376,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
 
   // ---- route 1: W = chol(A_d A_d^T), accepted when kappa <= kappa_max(M) ----
   if (gram_route_enabled() && M <= cholesky_max_rows()) {
+    RK_NVTX("rk.blocks.gram_route");
     const double kmax = kappa_max(M);
     const uint64_t per_block = (uint64_t)M * cols_pad_full * 8 * 2;
     const uint64_t chunk = std::max<uint64_t>(1, budget / per_block);
@@ -454,6 +458,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   // leaf makes the pairwise combines, ~4/3 M^3 each, dominate: c5 3x the flops)
   const uint32_t kLeafRows = std::max<uint32_t>(768, std::min<uint32_t>(2 * M, qr_max_rows()));
 
+  RK_NVTX("rk.blocks.householder_route");
   size_t t0 = 0;
   while (t0 < todo.size()) {
     std::vector<BlockPlan> plans;

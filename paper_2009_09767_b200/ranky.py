@@ -167,6 +167,8 @@ class DevOutputs(C.Structure):
 WANT_V, WANT_REPAIRED, WANT_RECORDS = 1, 2, 4
 
 _lib = None
+# rk_allgather_fn: (user, const double* d_mine, double* d_all, uint64_t count)
+ALLGATHER_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
 _lib_lock = threading.Lock()
 
 
@@ -184,6 +186,17 @@ def lib():
         sig = {
             "rk_last_error": ([], C.c_char_p), "rk_last_residual": ([], dbl), "rk_abi_version": ([], i32),
             "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32),
+            "rk_multi_create": ([C.POINTER(C.c_int32), u32, C.POINTER(vp)], i32),
+            "rk_multi_destroy": ([vp], i32),
+            "rk_multi_run_pipeline": ([vp, C.POINTER(_View), u64, i32, u64, u64, u32, u64, C.POINTER(_Pipeline)],
+                                      i32),
+            "rk_nccl_unique_id": ([C.POINTER(C.c_uint8)], i32),
+            "rk_dist_create": ([vp, i32, i32, C.POINTER(C.c_uint8), C.POINTER(vp)], i32),
+            "rk_dist_destroy": ([vp], i32),
+            "rk_dist_full_svd": ([vp, vp, u64, i32, u64, u64, u32, u64, C.POINTER(C.POINTER(DevOutputs)),
+                                  C.POINTER(Timing), pu64, pu64], i32),
+            "rk_dev_sharded_full_svd": ([vp, vp, u64, i32, u64, u64, u32, u64, i32, i32, ALLGATHER_FN, vp,
+                                         C.POINTER(C.POINTER(DevOutputs)), C.POINTER(Timing), pu64, pu64], i32),
             "rk_workspace_create": ([vp, C.POINTER(_View), u64, C.POINTER(vp)], i32),
             "rk_workspace_destroy": ([vp], i32),
             "rk_workspace_has_entry": ([vp, u64, u64, C.POINTER(C.c_int32)], i32),
@@ -1186,3 +1199,103 @@ def write_records(records, path_prefix, ctx: Context | None = None) -> None:
     rec = _Records(len(records), rows, kept.ctypes.data_as(C.POINTER(C.c_uint32)),
                    offset.ctypes.data_as(C.POINTER(C.c_uint64)), payload.ctypes.data_as(C.POINTER(C.c_double)))
     _check(lib().rk_write_records(_ctx(ctx), C.byref(rec), os.fsencode(str(path_prefix))))
+
+
+# ---------------------------------------------------------------------------
+# library-owned multi-GPU runs (rk_multi_*, rk_dist_*, rk_dev_sharded_full_svd)
+
+class Multi:
+    """Several devices driven from this process (rk_multi_*). `devices` may repeat a
+    device (its shards then share it) -- e.g. [0, 0] runs the two-shard protocol on
+    one GPU, bitwise the same as two processes on two GPUs."""
+
+    def __init__(self, devices):
+        d = (C.c_int32 * len(devices))(*devices)
+        self.handle = C.c_void_p()
+        _check(lib().rk_multi_create(d, len(devices), C.byref(self.handle)))
+        self.devices = list(devices)
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            lib().rk_multi_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run_pipeline(self, a: SparseMatrix, block_count: int, method, keep: int = 0, seed: int = 0,
+                     want_v: bool = False, top_k: int = 0, want_repaired: bool = True,
+                     want_records: bool = True) -> PipelineResult:
+        """run_pipeline (proj/src/pipeline.cpp:61-121) over all the devices."""
+        v = a._view()
+        out = _Pipeline()
+        flags = (WANT_V if want_v else 0) | (WANT_REPAIRED if want_repaired else 0) | \
+            (WANT_RECORDS if want_records else 0)
+        L = lib()
+        st = L.rk_multi_run_pipeline(self.handle, C.byref(v), block_count, _method(method), keep, seed, flags, top_k,
+                                     C.byref(out))
+        try:
+            _check(st)
+            svd = _svd_of(out.svd)
+            return PipelineResult(SvdResult(svd.u, svd.sigma, svd.v), _report_of(out.report),
+                                  _sparse_of(out.repaired) if want_repaired else None,
+                                  partition_columns(a.cols(), block_count),
+                                  _records_of(out.records) if want_records else [], out.timing.as_dict())
+        finally:
+            L.rk_pipeline_result_free(C.byref(out))
+
+
+def dev_sharded_full_svd(m: DeviceMatrix, block_count: int, method, keep: int, seed: int, world: int, rank: int,
+                         allgather, want_v: bool = True, top_k: int = 0):
+    """One rank's share of the library-orchestrated sharded run with the caller's
+    all-gather: allgather(mine, all) gets torch float64 CUDA tensors (count and
+    world*count doubles) and must fill `all` in rank order before returning.
+    Returns (DevOutputs ptr, Timing, col_lo, col_hi)."""
+    import torch
+
+    def cb(user, d_mine, d_all, count):
+        mine = torch.as_tensor(_CudaArray(d_mine, (count,)), device="cuda")
+        alls = torch.as_tensor(_CudaArray(d_all, (count * world,)), device="cuda")
+        allgather(mine, alls)
+
+    fn = ALLGATHER_FN(cb)
+    out = C.POINTER(DevOutputs)()
+    t = Timing()
+    lo, hi = C.c_uint64(), C.c_uint64()
+    _check(lib().rk_dev_sharded_full_svd(m.ctx.handle, m.handle, block_count, _method(method), keep, seed,
+                                         WANT_V if want_v else 0, top_k, world, rank, fn, None, C.byref(out),
+                                         C.byref(t), C.byref(lo), C.byref(hi)))
+    return out, t, lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().rk_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Dist:
+    """One process per GPU with the library's own NCCL communicator (rk_dist_*)."""
+
+    def __init__(self, ctx: Context, world: int, rank: int, uid: bytes):
+        buf = (C.c_uint8 * 128)(*uid)
+        self.handle = C.c_void_p()
+        _check(lib().rk_dist_create(ctx.handle, world, rank, buf, C.byref(self.handle)))
+
+    def full_svd(self, m: DeviceMatrix, block_count: int, method, keep: int = 0, seed: int = 0, want_v: bool = True,
+                 top_k: int = 0):
+        out = C.POINTER(DevOutputs)()
+        t = Timing()
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _check(lib().rk_dist_full_svd(self.handle, m.handle, block_count, _method(method), keep, seed,
+                                      WANT_V if want_v else 0, top_k, C.byref(out), C.byref(t), C.byref(lo),
+                                      C.byref(hi)))
+        return out, t, lo.value, hi.value
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            lib().rk_dist_destroy(self.handle)
+            self.handle = C.c_void_p()
