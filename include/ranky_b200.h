@@ -57,7 +57,8 @@ typedef enum rk_status {
   RK_CUDA = 5,             /* CUDA runtime failure or no usable device */
   RK_NOMEM = 6,            /* device or host allocation failed */
   RK_RECORD = 7,           /* ranky::RecordError: damaged or truncated block record file */
-  RK_GRAM_REJECTED = 8     /* sharded Gram route not applicable: take the TSQR path (rk_dev_shard_tsqr) */
+  RK_GRAM_REJECTED = 8,    /* sharded Gram route not applicable: take the TSQR path (rk_dev_shard_tsqr) */
+  RK_PARSE = 9             /* ranky::ParseError (errors.hpp:9-20); the line is rk_last_error_line() */
 } rk_status;
 
 /* RepairMethod -- proj/include/ranky/repair.hpp:15-20 (same numbering) */
@@ -141,6 +142,7 @@ typedef struct rk_pipeline_result {
 /* ---- errors & context ---------------------------------------------------- */
 RK_API const char* rk_last_error(void);
 RK_API double rk_last_residual(void);
+RK_API uint64_t rk_last_error_line(void); /* ParseError::line() of the last RK_PARSE */
 /* Re-read the RK_* tuning/debug environment switches (read once per process
  * otherwise). Not thread-safe against calls in flight. */
 RK_API void rk_reload_tuning(void);
@@ -252,6 +254,14 @@ RK_API rk_status rk_dev_outputs_free(rk_dev_outputs* o);
  * a_norm = ||A||_F. Requires RK_WANT_V. */
 RK_API rk_status rk_dev_residual(rk_ctx* ctx, const rk_dev_matrix* a, const rk_dev_outputs* out, double* residual,
                                  double* a_norm);
+
+/* ---- Matrix Market (proj/src/matrix_market.cpp:38-132) ----------------------------
+ * `%%MatrixMarket matrix coordinate real general`, 1-based. Loading validates as the
+ * reference (RK_PARSE with its messages and line numbers; the (row, col) sort that
+ * finds duplicates runs on the device) and returns the entries sorted; saving writes
+ * the reference's bytes (shortest round-trip values). Free with rk_sparse_free. */
+RK_API rk_status rk_load_matrix_market(rk_ctx* ctx, const char* path, rk_sparse* out);
+RK_API rk_status rk_save_matrix_market(const rk_sparse_view* a, const char* path);
 
 /* ---- RepairWorkspace (proj/include/ranky/repair.hpp:56-87, proj/src/repair.cpp:52-160) ----
  * The single-row checker API on a device workspace: the matrix (device CSR + CSC)

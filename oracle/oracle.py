@@ -238,6 +238,24 @@ class Oracle:
                                                          self._p(flat, C.c_double)))
 
 
+    # ---- Matrix Market (reference only): proj/src/matrix_market.cpp:38-132 ----
+    def load_matrix_market(self, path):
+        """-> (rows, cols, r, c, v); raises OracleError(6, "... (line L)", residual=L) on ParseError"""
+        fn = self.lib.ref_load_matrix_market
+        fn.restype = C.POINTER(_Res)
+        fn.argtypes = [C.c_char_p]
+        return self._take(fn(str(path).encode())).matrix
+
+    def save_matrix_market(self, a, path):
+        rows, cols, r, c, v = self._coo(a)
+        fn = self.lib.ref_save_matrix_market
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                       C.POINTER(C.c_double), C.c_char_p]
+        if fn(rows, cols, len(r), self._p(r, C.c_uint64), self._p(c, C.c_uint64), self._p(v, C.c_double),
+              str(path).encode()):
+            raise OracleError(4, "save_matrix_market failed")
+
     # ---- evaluation metrics (reference only): proj/src/metrics.cpp:32-114 ----
     def sigma_error(self, a, b) -> float:
         a = np.ascontiguousarray(a, dtype=np.float64); b = np.ascontiguousarray(b, dtype=np.float64)

@@ -18,6 +18,7 @@
 #include "ranky/block_record.hpp"
 #include "ranky/dense_matrix.hpp"
 #include "ranky/errors.hpp"
+#include "ranky/matrix_market.hpp"
 #include "ranky/metrics.hpp"
 #include "ranky/partition.hpp"
 #include "ranky/pipeline.hpp"
@@ -320,6 +321,31 @@ int ref_read_block_record(const char* path, uint32_t* index, uint32_t* rows, uin
     return 1;
   } catch (const std::exception&) {
     return 2;
+  }
+}
+
+// ---- Matrix Market -- proj/src/matrix_market.cpp:38-132 ----
+// load: res->matrix on success; status OR_RUNTIME + message "... (line L)" and
+// residual = L on a ParseError (status 6 marks a ParseError)
+or_result* ref_load_matrix_market(const char* path) {
+  or_result* res = fresh();
+  try {
+    put_sparse(res, load_matrix_market(path));
+  } catch (const ParseError& e) {
+    res->residual = (double)e.line();
+    fail(res, 6, e.what());
+  } catch (const std::exception& e) {
+    fail(res, OR_RUNTIME, e.what());
+  }
+  return res;
+}
+int ref_save_matrix_market(uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* r, const uint64_t* c,
+                           const double* v, const char* path) {
+  try {
+    save_matrix_market(make_sparse(rows, cols, nnz, r, c, v), path);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
   }
 }
 

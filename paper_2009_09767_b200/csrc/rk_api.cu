@@ -471,6 +471,30 @@ extern "C" {
 
 const char* rk_last_error(void) { return g_error.c_str(); }
 double rk_last_residual(void) { return g_residual; }
+uint64_t rk_last_error_line(void) { return (uint64_t)g_residual; }
+
+rk_status rk_load_matrix_market(rk_ctx* ctx, const char* path, rk_sparse* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!path || !out) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    std::memset(out, 0, sizeof *out);
+    CallScope sc(&ctx->c);
+    try {
+      load_matrix_market(path, *out, ctx->c.stream);
+    } catch (...) {
+      rk_sparse_free(out);
+      throw;
+    }
+  });
+}
+
+rk_status rk_save_matrix_market(const rk_sparse_view* a, const char* path) {
+  return guarded([&] {
+    check_view(a);
+    if (!path) fail(RK_INVALID_ARGUMENT, "NULL argument");
+    save_matrix_market(*a, path);
+  });
+}
 void rk_reload_tuning(void) { reload_tuning(); }
 uint32_t rk_build_flags(void) {
 #ifdef RK_EXPERIMENTS

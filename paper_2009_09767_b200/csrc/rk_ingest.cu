@@ -259,6 +259,47 @@ void merge_format(const DBuf<uint64_t>& old_ptr, const DBuf<uint32_t>& old_key, 
 
 }  // namespace
 
+namespace {
+__global__ void first_equal_adjacent(const uint64_t* key, uint64_t n, unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (key[i] == key[i - 1]) atomicMin(first, (unsigned long long)i);
+}
+}  // namespace
+
+void sort_entries_device(const rk_entry* host_in, uint64_t n, rk_entry* host_sorted, int64_t* dup_a, int64_t* dup_b,
+                         cudaStream_t s) {
+  *dup_a = *dup_b = -1;
+  if (n == 0) return;
+  DBuf<rk_entry> staged(n, s), sorted(n, s);
+  RK_CUDA_CHECK(cudaMemcpyAsync(staged.get(), host_in, n * sizeof(rk_entry), cudaMemcpyHostToDevice, s));
+  DBuf<uint64_t> k_in(n, s), k_out(n, s), i_in(n, s), i_out(n, s);
+  make_keys<<<blocks_for(n), kT, 0, s>>>(staged.get(), n, k_in.get(), i_in.get());
+  RK_LAUNCH_CHECK();
+  size_t tmp_bytes = 0;
+  RK_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in.get(), k_out.get(), i_in.get(), i_out.get(),
+                                                n, 0, 64, s));
+  DBuf<unsigned char> tmp(tmp_bytes ? tmp_bytes : 1, s);
+  RK_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, k_in.get(), k_out.get(), i_in.get(), i_out.get(),
+                                                n, 0, 64, s));
+  gather_entries<<<blocks_for(n), kT, 0, s>>>(staged.get(), i_out.get(), n, sorted.get());
+  RK_LAUNCH_CHECK();
+  DBuf<unsigned long long> first(1, s);
+  RK_CUDA_CHECK(cudaMemsetAsync(first.get(), 0xff, sizeof(unsigned long long), s));
+  first_equal_adjacent<<<blocks_for(n), kT, 0, s>>>(k_out.get(), n, first.get());
+  RK_LAUNCH_CHECK();
+  unsigned long long f = 0;
+  RK_CUDA_CHECK(cudaMemcpyAsync(&f, first.get(), sizeof f, cudaMemcpyDeviceToHost, s));
+  RK_CUDA_CHECK(cudaMemcpyAsync(host_sorted, sorted.get(), n * sizeof(rk_entry), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (f != ~0ull) {
+    uint64_t pair[2];
+    RK_CUDA_CHECK(cudaMemcpyAsync(pair, i_out.get() + f - 1, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    *dup_a = (int64_t)pair[0];
+    *dup_b = (int64_t)pair[1];
+  }
+}
+
 void upload_entries(const rk_sparse_view& a, DevMatrix& m, cudaStream_t s) {
   if (a.nnz && !a.entries) fail(RK_INVALID_ARGUMENT, "sparse view has entries == NULL");
   if (a.cols > 0xffffffffull || a.rows > 0xffffffffull)

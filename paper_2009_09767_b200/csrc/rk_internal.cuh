@@ -330,6 +330,10 @@ void exclusive_scan_u32to64(const uint32_t* in, uint64_t* out, uint64_t n, cudaS
 
 // rk_ingest.cu -- entries -> CSR, CSR -> CSC, CSC + edges -> repaired CSC/CSR
 void upload_entries(const rk_sparse_view& a, DevMatrix& m, cudaStream_t s);
+// stable device radix sort of host entries by (row, col) into host_sorted; dup_a / dup_b =
+// the input positions of the first adjacent equal pair in sorted order (-1: none)
+void sort_entries_device(const rk_entry* host_in, uint64_t n, rk_entry* host_sorted, int64_t* dup_a, int64_t* dup_b,
+                         cudaStream_t s);
 void csr_to_csc(const DevCsr& a, DevCsc& out, cudaStream_t s);
 void csr_to_entries_host(const DevCsr& a, rk_sparse& out, cudaStream_t s);
 
@@ -339,6 +343,10 @@ struct DevEdges {  // repair edges in report order
   DBuf<int32_t> mech;
 };
 void apply_edges(const DevMatrix& a, const DevEdges& e, DevMatrix& out, cudaStream_t s);
+
+// rk_mm.cu: Matrix Market files
+void load_matrix_market(const std::string& path, rk_sparse& out, cudaStream_t s);
+void save_matrix_market(const rk_sparse_view& a, const std::string& path);
 
 // rk_workspace.cu: RepairWorkspace's single-row API on the device
 struct Workspace;

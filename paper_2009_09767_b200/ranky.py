@@ -75,6 +75,14 @@ class GramRejected(RankyError):
     takes the TSQR path (rk_dev_shard_tsqr, all-gather, rk_dev_shard_finish)."""
 
 
+class ParseError(RankyError, RuntimeError):
+    """ranky::ParseError (proj/include/ranky/errors.hpp:9-20): message "... (line L)", .line"""
+
+    def __init__(self, message: str, line: int = 0):
+        super().__init__(message)
+        self.line = line
+
+
 class RecordError(RankyError, RuntimeError):
     """ranky::RecordError (proj/include/ranky/errors.hpp:23-26): damaged block record"""
 
@@ -185,7 +193,9 @@ def lib():
         pu64, pdbl = C.POINTER(C.c_uint64), C.POINTER(C.c_double)
         sig = {
             "rk_last_error": ([], C.c_char_p), "rk_last_residual": ([], dbl), "rk_abi_version": ([], i32),
-            "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32),
+            "rk_reload_tuning": ([], None), "rk_build_flags": ([], u32), "rk_last_error_line": ([], u64),
+            "rk_load_matrix_market": ([vp, C.c_char_p, C.POINTER(_Sparse)], i32),
+            "rk_save_matrix_market": ([C.POINTER(_View), C.c_char_p], i32),
             "rk_multi_create": ([C.POINTER(C.c_int32), u32, C.POINTER(vp)], i32),
             "rk_multi_destroy": ([vp], i32),
             "rk_multi_run_pipeline": ([vp, C.POINTER(_View), u64, i32, u64, u64, u32, u64, C.POINTER(_Pipeline)],
@@ -294,6 +304,8 @@ def _check(status: int):
         raise RecordError(msg)
     if status == GRAM_REJECTED:
         raise GramRejected(msg)
+    if status == 9:
+        raise ParseError(msg, int(L.rk_last_error_line()))
     raise RankyError(f"status {status}: {msg}")
 
 
@@ -901,6 +913,28 @@ def recover_right_vectors(a: SparseMatrix, u: np.ndarray, sigma, tol: float = K_
         return _svd_of(out).v
     finally:
         L.rk_svd_free(C.byref(out))
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market -- proj/src/matrix_market.cpp:38-132 (rk_mm.cu)
+
+def load_matrix_market(path, ctx: Context | None = None) -> SparseMatrix:
+    """The reference's loader: same header/dimension/entry rules and ParseError
+    messages with line numbers; entries sorted on the device."""
+    out = _Sparse()
+    L = lib()
+    st = L.rk_load_matrix_market(_ctx(ctx), str(path).encode(), C.byref(out))
+    try:
+        _check(st)
+        return _sparse_of(out)
+    finally:
+        L.rk_sparse_free(C.byref(out))
+
+
+def save_matrix_market(a: SparseMatrix, path) -> None:
+    """Byte-identical to the reference's writer (shortest round-trip values)."""
+    v = a._view()
+    _check(lib().rk_save_matrix_market(C.byref(v), str(path).encode()))
 
 
 # ---------------------------------------------------------------------------
