@@ -1318,7 +1318,20 @@ __global__ void __launch_bounds__(kCThreads) complete_kernel(double* u, uint32_t
 // apply_q: out(:, c) = H_0 ... H_{K-1} [x(:, c); 0] -- warp per column
 // ===========================================================================
 
+__device__ void apply_q_body(const QrJob& qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out);
+
 __global__ void apply_q_kernel(QrJob qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out) {
+  apply_q_body(qr, x, x_rows, ncols, out);
+}
+
+// one job per blockIdx.y (the wide blocks' reduced route: slot = Q [R V; 0])
+__global__ void apply_q_batched_kernel(const ApplyQJob* jobs) {
+  const ApplyQJob j = jobs[blockIdx.y];
+  apply_q_body(j.qr, j.x, j.x_rows, j.ncols, j.out);
+}
+
+// a warp per output column: the reflectors applied last to first (svd.cpp:111-132)
+__device__ void apply_q_body(const QrJob& qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out) {
   const int lane = threadIdx.x & 31;
   const uint32_t m = qr.m, K = qr.m < qr.n ? qr.m : qr.n;
   for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < ncols;
@@ -1532,6 +1545,18 @@ void complete_columns_device(double* u, uint32_t rows, uint32_t cols, const uint
   if (smem > 200 * 1024) fail(RK_RUNTIME, "orthonormal completion: matrix too large");
   RK_CUDA_CHECK(cudaFuncSetAttribute(complete_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   complete_kernel<<<1, kCThreads, smem, s>>>(u, rows, cols, deficient, d_fail);
+  RK_LAUNCH_CHECK();
+}
+
+void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  uint32_t cmax = 0;
+  for (const ApplyQJob& j : jobs) cmax = std::max(cmax, j.ncols);
+  if (!cmax) return;
+  DBuf<ApplyQJob> dj(jobs.size(), s);
+  to_device(dj.get(), jobs.data(), jobs.size(), s);
+  const unsigned gx = (unsigned)std::min<uint64_t>(ceil_div((uint64_t)cmax * 32, 256), 64);
+  apply_q_batched_kernel<<<dim3(gx, (unsigned)jobs.size()), 256, 0, s>>>(dj.get());
   RK_LAUNCH_CHECK();
 }
 

@@ -62,6 +62,7 @@ struct Tuning {
   bool precond = false;           // RK_PRECOND=1: FP32-preconditioned Jacobi (experiments build)
   float precond_stop = 1e-5f;     // RK_PRECOND_STOP
   bool spmm_warp = false;         // RK_SPMM_WARP=1: warp-per-column V SpMM
+  bool wide_reduce = true;        // RK_WIDE_REDUCE=0: wide blocks' Jacobi on X = T^T, not on its R
 };
 const Tuning& tuning();
 void reload_tuning();
@@ -448,6 +449,13 @@ uint32_t jacobi_cols_pad(uint32_t rows, uint32_t cols, bool with_v, size_t smem_
 // out (m x ncols col-major) = Q [x; 0] for a factored QrJob (svd.cpp:111-132)
 void apply_q_device(const QrJob& qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out,
                     cudaStream_t s);
+struct ApplyQJob {    // out (qr.m x ncols col-major, ld qr.m) = Q [x; 0], x x_rows x ncols (ld x_rows)
+  QrJob qr;
+  const double* x;
+  uint32_t x_rows, ncols;
+  double* out;
+};
+void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s);
 
 // rk_spmm.cu -- V = A^T U Sigma^-1 over the CSC
 void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const uint32_t* retained,

@@ -270,21 +270,33 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
 
   // the Jacobi width for a wide block of n < M real columns: planned for n rounded up
   // to 32 (few distinct widths, so few launches)
-  std::map<uint32_t, uint32_t> pad_cache;
-  auto narrow_pad = [&](uint32_t n) {
+  std::map<std::pair<uint32_t, uint32_t>, uint32_t> pad_cache;
+  auto narrow_pad = [&](uint32_t n, uint32_t rows) {
     const uint32_t r = std::min<uint32_t>(M, (n + 31) & ~31u);
-    auto it = pad_cache.find(r);
+    auto it = pad_cache.find({rows, r});
     if (it != pad_cache.end()) return it->second;
-    const uint32_t pd = std::min<uint32_t>(cols_pad_full, jacobi_cols_pad(M, r, false, c.smem_optin));
-    pad_cache[r] = pd;
+    const uint32_t pd = std::min<uint32_t>(cols_pad_full, jacobi_cols_pad(rows, r, false, c.smem_optin));
+    pad_cache[{rows, r}] = pd;
     return pd;
+  };
+
+  // Wide blocks (compacted height n_d < M) on the reduced route: X = T^T (M x n_d)
+  // = Q R by Householder QR, the Jacobi on R (n_d x n_d: columns of length n_d, not M),
+  // then the slot = Q [R V; 0] = U Sigma (svd_tall's own QR -> Jacobi -> apply_q,
+  // svd.cpp:316-332, applied to the tall X). Each slot has its Jacobi matrix (rows
+  // padded to a multiple of 32 with zero rows) and its factored QR.
+  struct Reduced {
+    std::vector<double*> mats;
+    std::vector<uint32_t> rows;
+    std::vector<QrJob> qr;
   };
 
   // Jacobi + finalize of a set of W slots; records stats and writes payloads
   std::vector<double> sigma_host;  // sorted sigma of the Gram-route slots (read with the Jacobi stats)
   auto jacobi_finalize = [&](std::vector<double*>& slots, std::vector<uint32_t>& cols, std::vector<uint64_t>& blocks,
                              bool gram_ok, double* sigma_all /* nullable: slots x cols_pad */,
-                             const std::vector<const uint32_t*>* row_perms = nullptr) {
+                             const std::vector<const uint32_t*>* row_perms = nullptr,
+                             const Reduced* red = nullptr /* per slot; mats[q] == nullptr: not reduced */) {
     const size_t nb = slots.size();
     DBuf<double> alpha((uint64_t)nb * cols_pad_full, s);
     DBuf<uint64_t> stats(8 * nb, s);
@@ -297,18 +309,23 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     // is a function of the block's own data, so results do not depend on batching.
     // Jobs of one width share a launch; the finalize still sees cols_pad_full
     // columns (the slot's tail is zero: sigma 0, deficient).
-    std::map<uint32_t, std::vector<JacobiJob>> by_pad;
+    std::map<std::pair<uint32_t, uint32_t>, std::vector<JacobiJob>> by_pad;
+    std::vector<uint32_t> jrows(nb, M);
+    std::vector<ApplyQJob> aq;
     for (size_t q = 0; q < nb; ++q) {
+      const bool reduced = red && red->mats[q];
       JacobiJob j{};
-      j.w = slots[q];
+      j.w = reduced ? red->mats[q] : slots[q];
       j.v = nullptr;
-      j.rows = M;
+      j.rows = reduced ? red->rows[q] : M;
       j.cols = std::max<uint32_t>(cols[q], 1);
-      j.cols_pad = j.cols >= M ? cols_pad_full : narrow_pad(j.cols);
+      j.cols_pad = (j.cols >= M && !reduced) ? cols_pad_full : narrow_pad(j.cols, j.rows);
       j.alpha = alpha.get() + (uint64_t)q * cols_pad_full;
       j.stats = stats.get() + 8 * q;
       j.gram_ok = gram_ok ? 1u : 0u;
-      by_pad[j.cols_pad].push_back(j);
+      jrows[q] = j.rows;
+      by_pad[{j.rows, j.cols_pad}].push_back(j);
+      if (reduced) aq.push_back({red->qr[q], red->mats[q], j.rows, cols[q], slots[q]});
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
     {
@@ -316,6 +333,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       for (auto& kv : by_pad) jacobi_batched(kv.second, s, c.num_sms, c.smem_optin);
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
+    apply_q_batched(aq, s);  // reduced slots: U Sigma = Q [R V; 0]
     prof_mark(s, "blk jacobi");
     std::vector<FinalJob> fj(nb);
     for (size_t q = 0; q < nb; ++q) {
@@ -348,7 +366,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       out.sweeps_max = std::max(out.sweeps_max, js[q].sweeps);
       out.sweeps_sum += js[q].sweeps;
       out.rotations += js[q].rotations;
-      const double cA = cols[q], Md = M;
+      const double cA = cols[q], Md = jrows[q];
       out.jacobi_flops += (double)js[q].sweeps * (cA * (cA - 1) / 2 * 2 * Md + 2 * Md * cA) +
                           (double)js[q].rotations * 6 * Md;
       if (js[q].failed) {
@@ -457,6 +475,9 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   // TSQR leaf height of the tall blocks: at least 2M, so every leaf is tall (a wide
   // leaf makes the pairwise combines, ~4/3 M^3 each, dominate: c5 3x the flops)
   const uint32_t kLeafRows = std::max<uint32_t>(768, std::min<uint32_t>(2 * M, qr_max_rows()));
+  // the reduced route pays when the padded R is clearly shorter than M (RK_WIDE_REDUCE=0: off)
+  const bool reduce_on = tuning().wide_reduce;
+  auto reduce_wide = [&](uint32_t n) { return reduce_on && n >= 2 && ((n + 31) & ~31u) * 4 <= 3 * M; };
 
   RK_NVTX("rk.blocks.householder_route");
   size_t t0 = 0;
@@ -473,14 +494,18 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       pl.n_rows = pl.n_multi + pl.n_single;
       pl.tall = pl.n_rows > M;
       // staging + the TSQR forest (leaf R factors, then stacked pairs and their R
-      // factors alive together: <= 3 M x M per leaf) + the Jacobi slot
+      // factors alive together: <= 3 M x M per leaf) + the Jacobi slot; a reduced
+      // wide block stages X = T^T (M x n_d) and its R (rows_pad x n_pad)
       const uint64_t n_leaves = pl.tall ? ceil_div(pl.n_rows, kLeafRows) : 0;
+      const bool red = !pl.tall && reduce_wide(pl.n_rows);
+      const uint64_t rp = ((uint64_t)pl.n_rows + 31) & ~31ull;
       const uint64_t need = (pl.tall ? (uint64_t)pl.n_rows * M + 3 * n_leaves * ((uint64_t)M * M + aux_sz) : 0) +
+                            (red ? (uint64_t)pl.n_rows * M + rp * rp + aux_sz : 0) +
                             (uint64_t)M * cols_pad_full + aux_sz;
       if (!plans.empty() && (planned + need) * 8 > budget) break;
       planned += need;
       pl.offset = staging;
-      staging += pl.tall ? (uint64_t)pl.n_rows * M : 0;
+      staging += (pl.tall || red) ? (uint64_t)pl.n_rows * M : 0;
       wdoubles += (uint64_t)M * cols_pad_full + aux_sz;
       plans.push_back(pl);
     }
@@ -494,8 +519,8 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     W.zero();
     std::vector<BlockPlan> fill_tall, fill_wide;
     for (size_t q = 0; q < nb; ++q) {
-      if (plans[q].tall) {
-        fill_tall.push_back(plans[q]);
+      if (plans[q].tall || reduce_wide(plans[q].n_rows)) {
+        fill_tall.push_back(plans[q]);  // staged (T for tall, X = T^T for reduced wide)
       } else {
         BlockPlan w = plans[q];
         w.offset = (uint64_t)q * M * cols_pad;  // W = T^T written straight into the Jacobi slot
@@ -533,6 +558,49 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         }
       }
     }
+    // reduced wide blocks: QR of X = T^T in the staging buffer, R into its Jacobi matrix
+    Reduced red;
+    red.mats.assign(nb, nullptr);
+    red.rows.assign(nb, 0);
+    red.qr.assign(nb, QrJob{});
+    DBuf<double> rmats, raux;
+    {
+      uint64_t rtot = 0, ntot = 0;
+      for (size_t q = 0; q < nb; ++q)
+        if (!plans[q].tall && reduce_wide(plans[q].n_rows)) {
+          const uint64_t rp = ((uint64_t)plans[q].n_rows + 31) & ~31ull;
+          rtot += rp * narrow_pad(plans[q].n_rows, (uint32_t)rp);
+          ++ntot;
+        }
+      if (ntot) {
+        rmats.alloc(rtot, s);
+        rmats.zero();
+        raux.alloc(ntot * aux_sz, s);
+        std::vector<QrJob> qj;
+        std::vector<RJob> rj;
+        uint64_t ro = 0, ao = 0;
+        for (size_t q = 0; q < nb; ++q) {
+          const uint32_t n = plans[q].n_rows;
+          if (plans[q].tall || !reduce_wide(n)) continue;
+          const uint32_t rp = (n + 31) & ~31u;
+          QrJob j;
+          j.a = st.get() + plans[q].offset; j.lda = M; j.m = M; j.n = n;
+          j.diag = raux.get() + ao; j.beta = j.diag + n; j.tmat = j.diag + 2 * (uint64_t)n;
+          ao += aux_sz;
+          qj.push_back(j);
+          red.qr[q] = j;
+          red.mats[q] = rmats.get() + ro;
+          red.rows[q] = rp;
+          ro += (uint64_t)rp * narrow_pad(n, rp);
+          RJob r;
+          r.a = j.a; r.lda = j.lda; r.diag = j.diag; r.m = M; r.n = n; r.w = red.mats[q]; r.ldw = rp;
+          rj.push_back(r);
+          out.qr_flops += 2.0 * M * (double)n * n - 2.0 / 3.0 * (double)n * n * n;
+        }
+        qr_batched(qj, s, c.num_sms);
+        r_extract_batched(rj, /*transpose=*/false, s);
+      }
+    }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[11], s));
     std::vector<double*> slots(nb);
     std::vector<uint32_t> cols(nb);
@@ -542,7 +610,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       cols[q] = std::min<uint32_t>(plans[q].n_rows, M);
       blocks[q] = plans[q].block - d_lo;
     }
-    jacobi_finalize(slots, cols, blocks, false, nullptr);
+    jacobi_finalize(slots, cols, blocks, false, nullptr, nullptr, &red);
     float ms_qr = 0;
     cudaEventElapsedTime(&ms_qr, c.ev[8], c.ev[11]);
     out.qr_ms += ms_qr;

@@ -172,3 +172,18 @@ def test_recover_reconstruction():
         r = v.shape[1]
         res = np.linalg.norm(d - (s.u[:, :r] * s.sigma[:r]) @ v.T)
         assert res <= 1e-10 * max(1.0, np.linalg.norm(d))
+
+
+@pytest.mark.parametrize("reduce", ["1", "0"])
+def test_wide_blocks_reduced_route(reduce, tuning_env, ref):
+    """Blocks whose compacted height n_d is well below M (the c3 shape: Zipf columns,
+    mostly empty or single-entry) take the reduced route -- QR of X = T^T, Jacobi
+    on its n_d x n_d R, slot = Q [R V; 0] -- or, with RK_WIDE_REDUCE=0, the Jacobi on
+    X itself; both match the reference's block_svd."""
+    tuning_env("RK_WIDE_REDUCE", reduce)
+    for seed in range(3):
+        for m, n, mean_deg in [(512, 8192, 1.024), (256, 4096, 0.6), (128, 2048, 2.0)]:
+            a = configs.zipf(m, n, mean_deg, 1.1, configs.VAL_UNIFORM_01, seed)
+            r, c, v = a.coo()
+            o = ref.block_svd((m, n, r, c, v), m)
+            compare(rk.block_svd(a, m), o.sigma, o.u, f"zipf {m}x{n} seed {seed} reduce {reduce}")
