@@ -393,6 +393,7 @@ RK_API rk_status rk_write_records(rk_ctx* ctx, const rk_records* records, const 
 typedef struct rk_multi rk_multi;
 typedef struct rk_dist rk_dist;
 typedef void (*rk_allgather_fn)(void* user, const double* d_mine, double* d_all, uint64_t count);
+RK_API int32_t rk_device_count(void); /* visible CUDA devices (0 when none) */
 RK_API rk_status rk_multi_create(const int32_t* devices, uint32_t n, rk_multi** out);
 RK_API rk_status rk_multi_destroy(rk_multi* m);
 RK_API rk_status rk_multi_run_pipeline(rk_multi* m, const rk_sparse_view* a, uint64_t block_count,

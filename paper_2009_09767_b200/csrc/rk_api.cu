@@ -1668,6 +1668,15 @@ struct rk_dist {
 
 extern "C" {
 
+int32_t rk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 rk_status rk_multi_create(const int32_t* devices, uint32_t n, rk_multi** out) {
   return guarded([&] {
     if (!devices || !n || !out) fail(RK_INVALID_ARGUMENT, "rk_multi_create: no devices");

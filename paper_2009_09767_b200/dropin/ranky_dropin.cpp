@@ -466,12 +466,58 @@ ProxyMatrix proxy_from_records(std::span<const BlockResultRecord> records, std::
   return proxy;
 }
 
+// The devices run_pipeline spreads its blocks over: RANKY_DEVICES ("0,1,2,3"; a device
+// may repeat). Unset (the default): one device, so results are bitwise the same for
+// every `workers` as the reference promises (acceptance_main.cpp:211-250); the sharded
+// merge agrees with the single-device one to the parity tolerance, and bitwise across
+// shard counts whose leaves / shards is a power of two.
+std::vector<int32_t> pipeline_devices() {
+  std::vector<int32_t> d;
+  if (const char* e = std::getenv("RANKY_DEVICES")) {
+    std::string s(e);
+    std::size_t pos = 0;
+    while (pos < s.size()) {
+      const std::size_t comma = s.find(',', pos);
+      const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+      if (!tok.empty()) d.push_back(std::atoi(tok.c_str()));
+      if (comma == std::string::npos) break;
+      pos = comma + 1;
+    }
+  }
+  return d;
+}
+
+struct ThreadMulti {
+  std::vector<int32_t> devices;
+  rk_multi* m = nullptr;
+  ~ThreadMulti() {
+    if (m) rk_multi_destroy(m);
+  }
+};
+
+rk_multi* multi_for(const std::vector<int32_t>& devices) {
+  thread_local ThreadMulti tm;
+  if (!tm.m || tm.devices != devices) {
+    if (tm.m) rk_multi_destroy(tm.m);
+    tm.m = nullptr;
+    check(rk_multi_create(devices.data(), (uint32_t)devices.size(), &tm.m));
+    tm.devices = devices;
+  }
+  return tm.m;
+}
+
 PipelineResult run_pipeline(const SparseMatrix& a, std::size_t block_count, RepairMethod method, std::size_t keep,
                             std::uint64_t seed, std::size_t workers) {
+  if (workers == 0) throw std::invalid_argument("workers must be >= 1");
   const rk_sparse_view v = view_of(a);
   rk_pipeline_result pr{};
-  const rk_status st = rk_run_pipeline(context(), &v, block_count, method_of(method), keep, seed, workers,
-                                       RK_WANT_REPAIRED | RK_WANT_RECORDS, 0, &pr);
+  const std::vector<int32_t> devices = pipeline_devices();
+  const uint64_t leaves = rk_merge_tree_leaves(a.rows(), a.cols(), block_count, keep);
+  const bool multi = devices.size() > 1 && leaves >= devices.size();
+  const rk_status st = multi ? rk_multi_run_pipeline(multi_for(devices), &v, block_count, method_of(method), keep,
+                                                     seed, RK_WANT_REPAIRED | RK_WANT_RECORDS, 0, &pr)
+                             : rk_run_pipeline(context(), &v, block_count, method_of(method), keep, seed, workers,
+                                               RK_WANT_REPAIRED | RK_WANT_RECORDS, 0, &pr);
   if (st != RK_OK) {
     rk_pipeline_result_free(&pr);
     check(st);
