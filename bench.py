@@ -192,7 +192,7 @@ def profiled_traffic(dominant):
     committed `ncu --set full` summary (profiles/*_kernels.json, written by
     profiles/summarize.py); None when there is none."""
     import glob
-    names = {"block_jacobi": "jacobi_", "block_qr": "qr_kernel"}
+    names = {"block_jacobi": "jacobi_", "block_qr": "qr_kernel", "merge": "jacobi_cluster_kernel<32, 8"}
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
     for f in reversed(files):
         try:
@@ -491,7 +491,8 @@ def main():
     # ---- roofline of the dominant kernel (by device time) --------------------------
     med = {k: statistics.median([t[k] for t in timings]) for k in timings[0]}
     peaks, peak_src = measured_peaks()
-    cand = {"block_jacobi": (med["jacobi_ms"], med["jacobi_flops"]), "block_qr": (med["qr_ms"], med["qr_flops"])}
+    cand = {"block_jacobi": (med["jacobi_ms"], med["jacobi_flops"]), "block_qr": (med["qr_ms"], med["qr_flops"]),
+            "merge": (med["merge_ms"], med["merge_flops"])}
     dom = max(cand, key=lambda k: cand[k][0])
     d_ms, d_flops = cand[dom]
     achieved = d_flops / (d_ms * 1e-3) / 1e12 if d_ms > 0 else 0.0
@@ -502,8 +503,9 @@ def main():
                 "peak_source": "measured in bench.py: cuBLAS DGEMM burst (torch.matmul f64 8192^3, best of 5); "
                                "FP64 is not in MEASURED_PEAKS.json",
                 "flops_per_launch": d_flops, "ms_per_launch": d_ms,
-                "flops_model": "QR: sum_d 2 n_d M^2 - 2/3 M^3; Jacobi: per block sweeps*(c(c-1)/2*2M + 2Mc) "
-                               "+ rotations*6M"}
+                "flops_model": "QR: sum_d 2 n_d M^2 - 2/3 M^3 (wide blocks: 2 M n_d^2 - 2/3 n_d^3); Jacobi: per "
+                               "block sweeps*(c(c-1)/2*2r + 2rc) + rotations*6r (r = the rows it runs on); merge: "
+                               "Gram route M(M+1) sum k + M^3/3 + its Jacobi, TSQR route 2 sum k M^2 + its Jacobi"}
     stages = {k: med[k] for k in ("repair_ms", "blocks_ms", "qr_ms", "jacobi_ms", "merge_ms", "recover_ms",
                                   "total_ms")}
     stages["jacobi_sweeps_max"] = med["jacobi_sweeps_max"]

@@ -37,3 +37,18 @@ def test_reference_workspace_tests_on_b200_dropin():
     print(out.stdout + out.stderr)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+
+
+def test_reference_acceptance_suite_on_two_shards():
+    """The same suite with RANKY_DEVICES=0,0: the drop-in's run_pipeline shards the
+    blocks over two device contexts (rk_multi_run_pipeline: concurrent shards, the
+    factor exchange by device copies, the shared tree top)."""
+    if not os.path.exists(BIN):
+        pytest.skip("relinked acceptance binary not built (needs the reference sources)")
+    env = dict(os.environ, RANKY_DEVICES="0,0")
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=900, env=env)
+    text = out.stdout + out.stderr
+    print(text)
+    assert not [l for l in text.splitlines() if l.startswith("FAIL")], text
+    assert len([l for l in text.splitlines() if l.startswith("PASS")]) == 8, text
+    assert out.returncode == 0
