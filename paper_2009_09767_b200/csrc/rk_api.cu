@@ -56,6 +56,7 @@ Tuning read_tuning() {
   t.precond_stop = (float)num("RK_PRECOND_STOP", 1e-5);
   t.spmm_warp = flag("RK_SPMM_WARP", '1');
   t.wide_reduce = !flag("RK_WIDE_REDUCE", '0');
+  t.repair_speculate = !flag("RK_REPAIR_SPECULATE", '0');
   return t;
 }
 std::mutex g_tuning_mu;

@@ -63,6 +63,7 @@ struct Tuning {
   float precond_stop = 1e-5f;     // RK_PRECOND_STOP
   bool spmm_warp = false;         // RK_SPMM_WARP=1: warp-per-column V SpMM
   bool wide_reduce = true;        // RK_WIDE_REDUCE=0: wide blocks' Jacobi on X = T^T, not on its R
+  bool repair_speculate = true;   // RK_REPAIR_SPECULATE=0: the neighbor replay without speculated sets
 };
 const Tuning& tuning();
 void reload_tuning();
@@ -364,6 +365,7 @@ struct RepairOut {
   DevEdges edges;
   std::vector<uint64_t> lonely_counts;
   uint64_t fallback = 0;
+  uint64_t recomputed = 0;  // neighbor replay: steps whose speculated sets were invalidated
 };
 void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uint64_t seed,
                    RepairOut& out, cudaStream_t s);

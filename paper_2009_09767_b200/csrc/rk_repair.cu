@@ -104,8 +104,82 @@ struct ReplayArgs {
   unsigned long long* nb;            // ceil(max width/64) words
   uint32_t* rowov; uint32_t rowov_cap;  // scratch: the lonely row's inserted columns
   uint32_t* e_block; uint32_t* e_row; uint32_t* e_col; int32_t* e_mech;  // capacity 2 * n_lonely
-  unsigned long long* out_counts;    // [0] edges, [1] fallbacks, [2] overflow flag
+  unsigned long long* out_counts;    // [0] edges, [1] fallbacks, [2] overflow flag, [3] steps recomputed
+  // speculation (null: off): every step's sets computed beforehand on the input alone
+  const unsigned long long* spec_cand;  // n_lonely x cand_words
+  const unsigned long long* spec_nb;    // n_lonely x nb_stride
+  uint64_t nb_stride;
+  const unsigned long long* spec_count;
+  const uint32_t* spec_col;
+  const uint64_t* spec_state;           // the step's KeyedRng state after its neighbor draw
 };
+
+// Speculation: step i's candidate rows and neighbor columns from the INPUT alone (no
+// inserted edges), the neighbor draw included -- one CTA per lonely (block, row), all
+// in parallel. The ordered replay then only checks whether the edges inserted before
+// step i could have changed its sets (see neighbor_replay) and recomputes the few
+// steps where they could.
+__global__ void __launch_bounds__(256) speculate_kernel(ReplayArgs a, unsigned long long* cand_all,
+                                                        unsigned long long* nb_all, unsigned long long* count_out,
+                                                        uint32_t* col_out, uint64_t* state_out) {
+  __shared__ unsigned long long s_red[8];
+  __shared__ unsigned long long s_k;
+  const uint64_t step = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t d = a.l_block[step], row = a.l_row[step];
+  const uint64_t b = a.p.begin(d), e = a.p.end(d), width = e - b;
+  const uint64_t cand_words = (a.rows + 63) / 64, nb_words = (width + 63) / 64;
+  unsigned long long* cand = cand_all + step * cand_words;
+  unsigned long long* nb = nb_all + step * a.nb_stride;
+  for (uint64_t i = a.row_ptr[row] + tid; i < a.row_ptr[row + 1]; i += 256) {
+    const uint64_t c = a.col_idx[i];
+    if (c >= b && c < e) continue;
+    for (uint64_t k = a.col_ptr[c]; k < a.col_ptr[c + 1]; ++k) {
+      const uint32_t m = a.row_idx[k];
+      atomicOr(&cand[m >> 6], 1ull << (m & 63));
+    }
+  }
+  __syncthreads();
+  for (uint64_t jj = tid; jj < width; jj += 256) {
+    const uint64_t c = b + jj;
+    for (uint64_t k = a.col_ptr[c], kend = a.col_ptr[c + 1]; k < kend; ++k) {
+      const uint32_t m = a.row_idx[k];
+      if ((cand[m >> 6] >> (m & 63)) & 1ull) {
+        atomicOr(&nb[jj >> 6], 1ull << (jj & 63));
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long mine = 0;
+  for (uint64_t w = tid; w < nb_words; w += 256) mine += __popcll(nb[w]);
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (lane == 0) s_red[warp] = mine;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+    KeyedRng g(a.seed, d, row);
+    s_k = t ? g.below(t) : 0;  // no draw when the set is empty (repair.cpp:130)
+    count_out[step] = t;
+    state_out[step] = g.state;
+    col_out[step] = 0xffffffffu;
+    // the k-th set bit, ascending (a serial scan: one thread, nb_words words)
+    if (t) {
+      unsigned long long k = s_k;
+      for (uint64_t w = 0; w < nb_words; ++w) {
+        unsigned long long bits = nb[w];
+        const unsigned long long pc = __popcll(bits);
+        if (k < pc) {
+          for (unsigned long long z = 0; z < k; ++z) bits &= bits - 1;
+          col_out[step] = (uint32_t)(b + w * 64 + (__ffsll((long long)bits) - 1));
+          break;
+        }
+        k -= pc;
+      }
+    }
+  }
+}
 
 __device__ __forceinline__ bool csr_has(const uint64_t* row_ptr, const uint32_t* col_idx, uint64_t r,
                                         uint32_t c) {
@@ -157,6 +231,45 @@ __global__ void __launch_bounds__(kReplayThreads, 1) neighbor_replay(ReplayArgs 
     }
     __syncthreads();
     const uint32_t rowov_n = min(s_rowov_n, a.rowov_cap);
+    // speculation check: step's sets from the input alone hold unless an earlier edge
+    //   (1) put a column c on `row` (c in rowov) one of whose rows (input or inserted) is
+    //       not already a candidate;
+    //   (2) is (m, c) with c in [b, e), m a candidate, c not already a neighbor column;
+    //   (3) is (m, c) with c outside [b, e) on one of `row`'s input columns, m not a candidate.
+    // Otherwise the candidate and neighbor sets -- and so the draw -- are the speculated ones.
+    bool spec_ok = false;  // uniform over the CTA
+    if (a.spec_cand) {
+      const unsigned long long* sc = a.spec_cand + step * cand_words;
+      const unsigned long long* sn = a.spec_nb + step * a.nb_stride;
+      auto in_cand = [&](uint32_t m) { return ((sc[m >> 6] >> (m & 63)) & 1ull) != 0ull; };
+      bool changed = false;
+      for (uint32_t q = tid; q < rowov_n && !changed; q += kReplayThreads) {
+        const uint32_t c = a.rowov[q];
+        for (uint64_t k = a.col_ptr[c]; k < a.col_ptr[c + 1] && !changed; ++k) changed = !in_cand(a.row_idx[k]);
+      }
+      for (uint32_t j = tid; j < n_edges && !changed; j += kReplayThreads) {
+        const uint32_t m = a.e_row[j], c = a.e_col[j];
+        if (c >= b && c < e) {
+          const uint64_t jj = c - b;
+          changed = in_cand(m) && !((sn[jj >> 6] >> (jj & 63)) & 1ull);
+        } else {
+          bool on_row = false;
+          for (uint32_t q = 0; q < rowov_n && !on_row; ++q) on_row = a.rowov[q] == c;
+          if (on_row || csr_has(a.row_ptr, a.col_idx, row, c)) changed = !in_cand(m);
+        }
+      }
+      if (__syncthreads_or(changed ? 1 : 0) == 0) {
+        if (tid == 0) {
+          s_found = a.spec_count[step] > 0;
+          s_col = a.spec_col[step];
+          s_state = a.spec_state[step];
+        }
+        spec_ok = true;
+      } else if (tid == 0) {
+        atomicAdd(&a.out_counts[3], 1ull);
+      }
+    }
+    if (!spec_ok) {
     // b1: rows sharing an input column with `row` outside [b, e) -- repair.cpp:111-117
     {
       const uint64_t lo = a.row_ptr[row], hi = a.row_ptr[row + 1];
@@ -249,6 +362,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) neighbor_replay(ReplayArgs 
         k -= pc;
       }
     }
+    }  // !spec_ok
     __syncthreads();
     // e: record edges -- repair.cpp:184-209
     if (tid == 0) {
@@ -368,7 +482,7 @@ void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uin
   }
   uint64_t max_w = p.end(D - 1) - p.begin(D - 1);
   if (p.width > max_w) max_w = p.width;
-  DBuf<unsigned long long> cand((rows + 63) / 64 + 1, s), nbm((max_w + 63) / 64 + 1, s), counts3(3, s);
+  DBuf<unsigned long long> cand((rows + 63) / 64 + 1, s), nbm((max_w + 63) / 64 + 1, s), counts3(4, s);
   const uint32_t rowov_cap = (uint32_t)std::min<uint64_t>(cap + 1, 1u << 24);
   DBuf<uint32_t> rowov(rowov_cap, s);
   counts3.zero();
@@ -382,14 +496,41 @@ void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uin
   ra.rowov = rowov.get(); ra.rowov_cap = rowov_cap;
   ra.e_block = E.block.get(); ra.e_row = E.row.get(); ra.e_col = E.col.get(); ra.e_mech = E.mech.get();
   ra.out_counts = counts3.get();
+  ra.spec_cand = nullptr;
+  // speculation: every step's sets on the input alone, in parallel (bitmaps of n_lonely x
+  // (rows + width) bits; skipped when they would not fit a modest buffer)
+  const uint64_t cand_words = (rows + 63) / 64, nb_words = (max_w + 63) / 64;
+  const uint64_t spec_bytes = n_lonely * (cand_words + nb_words) * 8;
+  DBuf<unsigned long long> spec_bits, spec_count;
+  DBuf<uint32_t> spec_col;
+  DBuf<uint64_t> spec_state;
+  if (tuning().repair_speculate && spec_bytes <= (uint64_t(1) << 30)) {
+    spec_bits.alloc(n_lonely * (cand_words + nb_words), s);
+    spec_bits.zero();
+    spec_count.alloc(n_lonely, s);
+    spec_col.alloc(n_lonely, s);
+    spec_state.alloc(n_lonely, s);
+    ra.nb_stride = nb_words;
+    unsigned long long* cand_all = spec_bits.get();
+    unsigned long long* nb_all = spec_bits.get() + n_lonely * cand_words;
+    speculate_kernel<<<(unsigned)n_lonely, 256, 0, s>>>(ra, cand_all, nb_all, spec_count.get(), spec_col.get(),
+                                                         spec_state.get());
+    RK_LAUNCH_CHECK();
+    ra.spec_cand = cand_all;
+    ra.spec_nb = nb_all;
+    ra.spec_count = spec_count.get();
+    ra.spec_col = spec_col.get();
+    ra.spec_state = spec_state.get();
+  }
   neighbor_replay<<<1, kReplayThreads, 0, s>>>(ra);
   RK_LAUNCH_CHECK();
-  unsigned long long c3[3];
+  unsigned long long c3[4];
   RK_CUDA_CHECK(cudaMemcpyAsync(c3, counts3.get(), sizeof c3, cudaMemcpyDeviceToHost, s));
   sync(s);
   if (c3[2]) fail(RK_RUNTIME, "neighbor replay: inserted-column scratch overflow");
   E.n = c3[0];
   out.fallback = method == RK_NEIGHBOR ? c3[1] : 0;
+  out.recomputed = ra.spec_cand ? c3[3] : n_lonely;
 }
 
 void lonely_rows_device(const DevMatrix& a, const Partition& p, uint64_t d, std::vector<uint64_t>& out,

@@ -148,3 +148,22 @@ def test_bad_arguments():
         rk.repair(a, rk.partition_columns(8, 2), "random", 0)
     with pytest.raises(rk.OutOfRange):
         rk.find_lonely_rows(a, rk.partition_columns(16, 2), 5)
+
+
+@pytest.mark.parametrize("method", ["neighbor", "neighbor-random"])
+def test_speculated_replay_is_exact(method, tuning_env, ref):
+    """The neighbor replay with speculated sets (every step's candidate and neighbor
+    sets from the input alone, recomputed only where an earlier edge could change
+    them) gives the reference's edges bit for bit -- on dense-collision cases (many
+    lonely rows per block, rows lonely in several blocks) as on sparse ones."""
+    cases = [(configs.synth_bipartite(16, 256, 0.03, s), 16) for s in range(4)]
+    cases += [(configs.synth_bipartite(64, 8192, 0.002, 7), 32), (configs.synth_bipartite(200, 4000, 0.004, 3), 40)]
+    for spec in ("1", "0"):
+        tuning_env("RK_REPAIR_SPECULATE", spec)
+        for a, D in cases:
+            p = rk.partition_columns(a.cols(), D)
+            rep, report = rk.repair(a, p, method, 11)
+            r, c, v = a.coo()
+            o = ref.repair((a.rows(), a.cols(), r, c, v), D, method, 11)
+            assert np.array_equal(report.edges_array(), o.edges), (spec, a.rows(), D)
+            assert report.fallback_count == o.fallback_count
