@@ -853,6 +853,8 @@ rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_c
     out->svd.u_rows = M;
     out->svd.u_cols = k;
     out->svd.n_sigma = k;
+    RK_NVTX("rk.results_to_host");
+    prof_mark(s, "out: start");
     out->svd.u = host_copy(fr.merge.u.get(), M * k, s);
     out->svd.sigma = host_copy(fr.merge.sigma.get(), k, s);
     if (flags & RK_WANT_V) {
@@ -860,9 +862,12 @@ rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_c
       out->svd.v_rows = a->cols;
       out->svd.v_cols = fr.r;
       out->svd.v = host_copy(fr.v.get(), a->cols * (uint64_t)fr.r, s);
+      prof_mark(s, "out: V D2H issued");
     }
     report_to_host(fr.rep, p, &out->report, s);
+    prof_mark(s, "out: report");
     if (flags & RK_WANT_REPAIRED) csr_to_entries_host(fr.repaired ? fr.repaired->csr : m.csr, out->repaired, s);
+    prof_mark(s, "out: repaired");
     if (flags & RK_WANT_RECORDS) {
       out->records.n_records = p.blocks;
       out->records.rows = M;
@@ -875,6 +880,8 @@ rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_c
       out->records.payload = host_copy(fr.blocks.payload.get(), fr.blocks.payload.n, s);
     }
     sync(s);
+    prof_mark(s, "out: records + sync");
+    prof_flush();
   });
 }
 

@@ -578,12 +578,9 @@ def _report_of(r: _Report) -> RepairReport:
 
 
 def _sparse_of(s: _Sparse) -> SparseMatrix:
+    """The library's entry array as the matrix's storage (no copy)."""
     n = int(s.nnz)
-    if n:
-        buf = (C.c_char * (n * ENTRY_DTYPE.itemsize)).from_address(s.entries)
-        e = np.frombuffer(bytes(buf), dtype=ENTRY_DTYPE).copy()
-    else:
-        e = np.zeros(0, dtype=ENTRY_DTYPE)
+    e = _take_array(s, "entries", n, (n,), ENTRY_DTYPE) if n else np.zeros(0, dtype=ENTRY_DTYPE)
     return SparseMatrix._trusted(s.rows, s.cols, e)
 
 
@@ -797,17 +794,21 @@ class _HostBuffer:
             pass
 
 
-def _take_array(struct, field: str, n: int, shape) -> np.ndarray:
+def _take_array(struct, field: str, n: int, shape, dtype=np.float64) -> np.ndarray:
     """Zero-copy numpy view of a large result buffer; ownership moves to the array
     (the struct field is cleared so the record's free does not release it)."""
     ptr = getattr(struct, field)
-    addr = C.cast(ptr, C.c_void_p).value
+    addr = ptr if (ptr is None or isinstance(ptr, int)) else C.cast(ptr, C.c_void_p).value
+    dtype = np.dtype(dtype)
     if n < (1 << 17) or not addr:
-        return _arr(ptr, n, np.float64).reshape(shape)
-    buf = (C.c_double * n).from_address(addr)
-    arr = np.frombuffer(buf, dtype=np.float64).reshape(shape)
+        if not addr or n == 0:
+            return np.zeros(shape, dtype=dtype)
+        raw = (C.c_char * (n * dtype.itemsize)).from_address(addr)
+        return np.frombuffer(raw, dtype=dtype).copy().reshape(shape)
+    buf = (C.c_char * (n * dtype.itemsize)).from_address(addr)
+    arr = np.frombuffer(buf, dtype=dtype).reshape(shape)
     keeper = _HostBuffer(addr)
-    setattr(struct, field, C.cast(C.c_void_p(0), type(ptr)))
+    setattr(struct, field, None if isinstance(ptr, int) else C.cast(C.c_void_p(0), type(ptr)))
     holder = np.ndarray.__new__(_Owned, arr.shape, dtype=arr.dtype, buffer=buf)
     holder._keeper = keeper
     return holder
@@ -1035,12 +1036,14 @@ def make_block_record(block_index: int, svd: SvdResult) -> BlockResultRecord:
 
 
 def _records_of(r: _Records) -> list[BlockResultRecord]:
+    """The records as views of the library's one payload buffer (no copy; the buffer
+    lives as long as any record does)."""
     n = int(r.n_records)
     kept = _arr(r.kept, n, np.int64)
     offs = _arr(r.offset, n, np.int64)
     total = int(sum(kept)) * int(r.rows)
-    flat = _arr(r.payload, total, np.float64)
-    return [BlockResultRecord(d, int(r.rows), int(kept[d]), flat[offs[d]:offs[d] + int(r.rows) * int(kept[d])].copy())
+    flat = _take_array(r, "payload", total, (total,))
+    return [BlockResultRecord(d, int(r.rows), int(kept[d]), flat[offs[d]:offs[d] + int(r.rows) * int(kept[d])])
             for d in range(n)]
 
 
