@@ -378,6 +378,9 @@ struct FullRun {
   MergeOut merge;
   DBuf<double> v;
   uint32_t r = 0;  // V columns
+  // optional: the records' D2H into this host buffer, issued on c.copy right after
+  // the block stage so it overlaps the merge and V (the caller waits on c.copy_ev[1])
+  double* records_host = nullptr;
 };
 
 // repair -> blocks -> merge -> (V); everything device-resident
@@ -414,6 +417,13 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   if (any_failure(fr.blocks)) throw_block_failure(fr.blocks, 0);
   RK_CUDA_CHECK(cudaEventRecord(ev2, s));
   prof_mark(s, "blocks (end)");
+  if (fr.records_host && fr.blocks.payload.n) {
+    RK_CUDA_CHECK(cudaEventRecord(c.copy_ev[0], s));
+    RK_CUDA_CHECK(cudaStreamWaitEvent(c.copy, c.copy_ev[0], 0));
+    RK_CUDA_CHECK(cudaMemcpyAsync(fr.records_host, fr.blocks.payload.get(), fr.blocks.payload.n * sizeof(double),
+                                  cudaMemcpyDeviceToHost, c.copy));
+    RK_CUDA_CHECK(cudaEventRecord(c.copy_ev[1], c.copy));
+  }
   {
     RK_NVTX("rk.merge");
     merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
@@ -548,6 +558,11 @@ rk_status rk_ctx_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   for (auto& ev : ctx->c.ev) cudaEventDestroy(ev);
+  if (ctx->c.copy) {
+    cudaStreamSynchronize(ctx->c.copy);
+    cudaStreamDestroy(ctx->c.copy);
+    for (auto& ev : ctx->c.copy_ev) cudaEventDestroy(ev);
+  }
   if (ctx->c.arena.base) cudaFreeHost(ctx->c.arena.base);
   cudaStreamDestroy(ctx->c.own);
   delete ctx;
@@ -846,6 +861,29 @@ rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_c
     DevMatrix m;
     upload_entries(*a, m, c.stream);
     FullRun fr;
+    double* rec_host = nullptr;
+    if (flags & RK_WANT_RECORDS) {
+      if (!c.copy) {
+        RK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+        for (auto& ev : c.copy_ev) RK_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      }
+      // the records' size is known before the block stage: D blocks of M x k
+      uint64_t tot = 0;
+      for (uint64_t d = 0; d < p.blocks; ++d) {
+        const uint64_t w = p.end(d) - p.begin(d), kf = std::min<uint64_t>(a->rows, w);
+        tot += a->rows * (keep == 0 ? kf : std::min(keep, kf));
+      }
+      rec_host = host_alloc<double>(tot ? tot : 1);
+      fr.records_host = rec_host;
+    }
+    struct RecGuard {  // the copy stream must be done before the payload is freed or on error
+      Ctx& c;
+      double*& p;
+      ~RecGuard() {
+        if (c.copy) cudaStreamSynchronize(c.copy);
+        if (p) host_free(p);
+      }
+    } rec_guard{c, rec_host};
     full_run(c, m, p, method, keep, seed, flags, top_k, fr, &out->timing);
     cudaStream_t s = c.stream;
     const uint64_t M = a->rows;
@@ -877,7 +915,13 @@ rk_status rk_run_pipeline(rk_ctx* ctx, const rk_sparse_view* a, uint64_t block_c
         out->records.kept[d] = fr.blocks.kept[d];
         out->records.offset[d] = fr.blocks.offset[d];
       }
-      out->records.payload = host_copy(fr.blocks.payload.get(), fr.blocks.payload.n, s);
+      if (fr.blocks.payload.n && fr.records_host) {
+        RK_CUDA_CHECK(cudaStreamWaitEvent(s, c.copy_ev[1], 0));  // issued after the block stage
+        out->records.payload = rec_host;
+        rec_host = nullptr;  // owned by the result now
+      } else {
+        out->records.payload = host_copy(fr.blocks.payload.get(), fr.blocks.payload.n, s);
+      }
     }
     sync(s);
     prof_mark(s, "out: records + sync");

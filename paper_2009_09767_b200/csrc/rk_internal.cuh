@@ -304,6 +304,9 @@ struct Ctx {
   bool free_known = false;
   size_t free0 = 0;
   uint64_t reserved0 = 0;
+  // a second stream for result copies that overlap later stages (created on first use)
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copy_ev[2] = {};
 };
 
 // free device memory for planning. Exact (cudaMemGetInfo, slow) at the first call
