@@ -793,12 +793,15 @@ void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, 
   }
   std::vector<SyrkChunk> ch;
   std::vector<uint32_t> c0(L), c1(L);
+  // each record's leading nonzero columns only (record_eff_cols), as records_gram
+  const std::vector<uint32_t> eff =
+      record_eff_cols(payload, offset, kept, M, leaves.front().first, leaves.back().second, s);
   for (uint64_t l = 0; l < L; ++l) {
     c0[l] = (uint32_t)ch.size();
     for (uint32_t d = leaves[l].first; d < leaves[l].second; ++d) {
-      if (!kept[d]) continue;
-      for (uint32_t j0 = 0; j0 < kept[d]; j0 += 256)
-        ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(kept[d], j0 + 256)});
+      if (!eff[d]) continue;
+      for (uint32_t j0 = 0; j0 < eff[d]; j0 += 256)
+        ch.push_back({payload + offset[d], kept[d], j0, std::min<uint32_t>(eff[d], j0 + 256)});
     }
     c1[l] = (uint32_t)ch.size();
   }
