@@ -247,14 +247,22 @@ class Oracle:
         return self._take(fn(str(path).encode())).matrix
 
     def save_matrix_market(self, a, path):
+        """The reference's writer in its own process (oracle/_ref/ref_mm_save): inside a
+        Python process that has loaded numpy's bundled libraries its std::to_chars(double)
+        path crashes under ctypes."""
+        import subprocess
+        import tempfile
         rows, cols, r, c, v = self._coo(a)
-        fn = self.lib.ref_save_matrix_market
-        fn.restype = C.c_int
-        fn.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
-                       C.POINTER(C.c_double), C.c_char_p]
-        if fn(rows, cols, len(r), self._p(r, C.c_uint64), self._p(c, C.c_uint64), self._p(v, C.c_double),
-              str(path).encode()):
-            raise OracleError(4, "save_matrix_market failed")
+        exe = os.path.join(os.path.dirname(REF_SO), "ref_mm_save")
+        with tempfile.NamedTemporaryFile(suffix=".coo", delete=False) as f:
+            f.write(np.array([rows, cols, len(r)], dtype=np.uint64).tobytes())
+            f.write(r.tobytes()); f.write(c.tobytes()); f.write(v.tobytes())
+            tmp = f.name
+        try:
+            if subprocess.run([exe, tmp, str(path)]).returncode:
+                raise OracleError(4, "save_matrix_market failed")
+        finally:
+            os.unlink(tmp)
 
     # ---- evaluation metrics (reference only): proj/src/metrics.cpp:32-114 ----
     def sigma_error(self, a, b) -> float:

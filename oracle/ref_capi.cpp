@@ -325,8 +325,8 @@ int ref_read_block_record(const char* path, uint32_t* index, uint32_t* rows, uin
 }
 
 // ---- Matrix Market -- proj/src/matrix_market.cpp:38-132 ----
-// load: res->matrix on success; status OR_RUNTIME + message "... (line L)" and
-// residual = L on a ParseError (status 6 marks a ParseError)
+// load: res->matrix on success; status 6 (a ParseError) + message "... (line L)" and
+// residual = L. (save: oracle/ref_mm_save.cpp, a separate process.)
 or_result* ref_load_matrix_market(const char* path) {
   or_result* res = fresh();
   try {
@@ -339,16 +339,6 @@ or_result* ref_load_matrix_market(const char* path) {
   }
   return res;
 }
-int ref_save_matrix_market(uint64_t rows, uint64_t cols, uint64_t nnz, const uint64_t* r, const uint64_t* c,
-                           const double* v, const char* path) {
-  try {
-    save_matrix_market(make_sparse(rows, cols, nnz, r, c, v), path);
-    return 0;
-  } catch (const std::exception&) {
-    return 1;
-  }
-}
-
 // ---- evaluation metrics -- proj/src/metrics.cpp:32-114 ----
 double ref_sigma_error(const double* a, uint64_t na, const double* b, uint64_t nb) {
   return sigma_error(std::span<const double>(a, na), std::span<const double>(b, nb));
