@@ -1330,6 +1330,60 @@ __global__ void apply_q_batched_kernel(const ApplyQJob* jobs) {
   apply_q_body(j.qr, j.x, j.x_rows, j.ncols, j.out);
 }
 
+// The same product with the columns in registers: a warp owns CW columns of one job
+// (element i of a column in lane i % 32, slot i / 32), so each reflector is read once
+// per CW columns and the CW dot products reduce side by side. For m <= 32 E.
+template <int CW, int E>
+__global__ void __launch_bounds__(256) apply_q_regs_kernel(const ApplyQJob* jobs) {
+  const ApplyQJob j = jobs[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = j.qr.m, K = j.qr.m < j.qr.n ? j.qr.m : j.qr.n;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t c0 = w0 * CW; c0 < j.ncols; c0 += nw * CW) {
+    double o[CW][E];
+#pragma unroll
+    for (int cw = 0; cw < CW; ++cw)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t i = lane + 32 * e, c = c0 + cw;
+        o[cw][e] = (c < j.ncols && i < j.x_rows) ? j.x[(uint64_t)c * j.x_rows + i] : 0.0;
+      }
+    for (int kk = (int)K - 1; kk >= 0; --kk) {
+      const double beta = j.qr.beta[kk];
+      if (beta == 0.0) continue;
+      const double* __restrict__ v = j.qr.a + (uint64_t)kk * j.qr.lda;  // v0 on the diagonal, then below
+      double vv[E];
+      double d[CW];
+#pragma unroll
+      for (int cw = 0; cw < CW; ++cw) d[cw] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t i = lane + 32 * e;
+        vv[e] = (i >= (uint32_t)kk && i < m) ? __ldg(v + i) : 0.0;
+#pragma unroll
+        for (int cw = 0; cw < CW; ++cw) d[cw] = fma(vv[e], o[cw][e], d[cw]);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1)
+#pragma unroll
+        for (int cw = 0; cw < CW; ++cw) d[cw] += __shfl_xor_sync(0xffffffffu, d[cw], off);
+#pragma unroll
+      for (int cw = 0; cw < CW; ++cw) {
+        const double bw = beta * d[cw];
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[cw][e] = fma(-bw, vv[e], o[cw][e]);
+      }
+    }
+#pragma unroll
+    for (int cw = 0; cw < CW; ++cw)
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t i = lane + 32 * e, c = c0 + cw;
+        if (c < j.ncols && i < m) j.out[(uint64_t)c * m + i] = o[cw][e];
+      }
+  }
+}
+
 // a warp per output column: the reflectors applied last to first (svd.cpp:111-132)
 __device__ void apply_q_body(const QrJob& qr, const double* x, uint32_t x_rows, uint32_t ncols, double* out) {
   const int lane = threadIdx.x & 31;
@@ -1553,10 +1607,21 @@ void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
   uint32_t cmax = 0;
   for (const ApplyQJob& j : jobs) cmax = std::max(cmax, j.ncols);
   if (!cmax) return;
+  uint32_t mmax = 0;
+  for (const ApplyQJob& j : jobs) mmax = std::max(mmax, j.qr.m);
   DBuf<ApplyQJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
-  const unsigned gx = (unsigned)std::min<uint64_t>(ceil_div((uint64_t)cmax * 32, 256), 64);
-  apply_q_batched_kernel<<<dim3(gx, (unsigned)jobs.size()), 256, 0, s>>>(dj.get());
+  constexpr int kCW = 4;
+  const unsigned gr = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div((uint64_t)cmax, 8 * kCW), 64));
+  const dim3 grid(gr, (unsigned)jobs.size());
+  if (mmax <= 128) apply_q_regs_kernel<kCW, 4><<<grid, 256, 0, s>>>(dj.get());
+  else if (mmax <= 256) apply_q_regs_kernel<kCW, 8><<<grid, 256, 0, s>>>(dj.get());
+  else if (mmax <= 512) apply_q_regs_kernel<kCW, 16><<<grid, 256, 0, s>>>(dj.get());
+  else if (mmax <= 1024) apply_q_regs_kernel<2, 32><<<grid, 256, 0, s>>>(dj.get());
+  else {
+    const unsigned gx = (unsigned)std::min<uint64_t>(ceil_div((uint64_t)cmax * 32, 256), 64);
+    apply_q_batched_kernel<<<dim3(gx, (unsigned)jobs.size()), 256, 0, s>>>(dj.get());
+  }
   RK_LAUNCH_CHECK();
 }
 
