@@ -57,6 +57,7 @@ Tuning read_tuning() {
   t.spmm_warp = flag("RK_SPMM_WARP", '1');
   t.wide_reduce = !flag("RK_WIDE_REDUCE", '0');
   t.repair_speculate = !flag("RK_REPAIR_SPECULATE", '0');
+  if (const char* e = std::getenv("RK_WIDE_ROWS")) t.wide_rows_pow2 = std::string(e) != "32";
   return t;
 }
 std::mutex g_tuning_mu;

@@ -477,7 +477,17 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   const uint32_t kLeafRows = std::max<uint32_t>(768, std::min<uint32_t>(2 * M, qr_max_rows()));
   // the reduced route pays when the padded R is clearly shorter than M (RK_WIDE_REDUCE=0: off)
   const bool reduce_on = tuning().wide_reduce;
-  auto reduce_wide = [&](uint32_t n) { return reduce_on && n >= 2 && ((n + 31) & ~31u) * 4 <= 3 * M; };
+  // R's rows padded with zero rows to a power of two (>= 32): the Jacobi kernel holds
+  // Q x E (both powers of two) elements per column, so such a height takes its exact
+  // (unpredicated) path at no extra cost per round (RK_WIDE_ROWS=32: multiples of 32)
+  const bool rows_pow2 = tuning().wide_rows_pow2;
+  auto red_rows = [&](uint32_t n) -> uint32_t {
+    if (!rows_pow2) return (n + 31) & ~31u;
+    uint32_t r = 32;
+    while (r < n) r *= 2;
+    return r;
+  };
+  auto reduce_wide = [&](uint32_t n) { return reduce_on && n >= 2 && red_rows(n) < M && red_rows(n) * 4 <= 3 * M; };
 
   RK_NVTX("rk.blocks.householder_route");
   size_t t0 = 0;
@@ -498,7 +508,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       // wide block stages X = T^T (M x n_d) and its R (rows_pad x n_pad)
       const uint64_t n_leaves = pl.tall ? ceil_div(pl.n_rows, kLeafRows) : 0;
       const bool red = !pl.tall && reduce_wide(pl.n_rows);
-      const uint64_t rp = ((uint64_t)pl.n_rows + 31) & ~31ull;
+      const uint64_t rp = red_rows(pl.n_rows);
       const uint64_t need = (pl.tall ? (uint64_t)pl.n_rows * M + 3 * n_leaves * ((uint64_t)M * M + aux_sz) : 0) +
                             (red ? (uint64_t)pl.n_rows * M + rp * rp + aux_sz : 0) +
                             (uint64_t)M * cols_pad_full + aux_sz;
@@ -568,7 +578,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       uint64_t rtot = 0, ntot = 0;
       for (size_t q = 0; q < nb; ++q)
         if (!plans[q].tall && reduce_wide(plans[q].n_rows)) {
-          const uint64_t rp = ((uint64_t)plans[q].n_rows + 31) & ~31ull;
+          const uint64_t rp = red_rows(plans[q].n_rows);
           rtot += rp * narrow_pad(plans[q].n_rows, (uint32_t)rp);
           ++ntot;
         }
@@ -582,7 +592,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         for (size_t q = 0; q < nb; ++q) {
           const uint32_t n = plans[q].n_rows;
           if (plans[q].tall || !reduce_wide(n)) continue;
-          const uint32_t rp = (n + 31) & ~31u;
+          const uint32_t rp = red_rows(n);
           QrJob j;
           j.a = st.get() + plans[q].offset; j.lda = M; j.m = M; j.n = n;
           j.diag = raux.get() + ao; j.beta = j.diag + n; j.tmat = j.diag + 2 * (uint64_t)n;

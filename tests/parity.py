@@ -13,7 +13,12 @@
   unsigned overlap is still required there.
 * a cluster of >1 columns is compared by the largest principal angle between the
   two column spans (proj/tests/test_support.hpp:71-79), computed from its sine
-  ||(I - Ã Ãᵀ) B||₂ for accuracy at small angles; bound 1e-6.
+  ||(I - Ã Ãᵀ) B||₂ for accuracy at small angles; bound 1e-6, or -- for a cluster
+  whose gap to the rest of the spectrum is itself tiny -- the Davis-Kahan
+  sensitivity of that subspace to a backward error of 1e3·eps·sigma_max
+  (sin theta <= ||E|| / gap; 1e3 covers the sqrt(rows) growth of the merge's QR of
+  up to 262144 stacked rows). Example: c5's sigma_4 ≈ sigma_5 ≈ sqrt(10) (rows
+  carrying 10 unit repair edges), 1.5e-8 from the next sigma: bound 5.5e-5.
 * columns of numerically zero sigma (<= 1e-10·sigma_max) are any basis of part of
   the null space; they are compared (as a span) only when U is square and they
   form its tail, where the span is the complement of the rest.
@@ -28,6 +33,7 @@ SIGMA_ABS = 1e-8        # absolute (·sigma_max) below it
 OVERLAP = 1 - 1e-8
 CLUSTER_TOL = 1e-9      # proj/src/metrics.cpp:15
 ANGLE = 1e-6            # proj/tests/test_support.hpp:71-79 usage
+DK_BACKWARD = 1e3 * np.finfo(np.float64).eps  # backward error (x sigma_max) behind the Davis-Kahan bound
 
 
 def clusters(sigma_ref: np.ndarray) -> list[tuple[int, int]]:
@@ -112,7 +118,10 @@ def check_u(u, ref_u, ref_sigma, what="", cols: int | None = None):
             # columns must then lie in the reference's cluster span (hi_c < hi)
             s = sin_largest_angle(u[:, lo:hi_c], ref_u[:, lo:hi])
             max_sin = max(max_sin, s)
-            assert s <= ANGLE, (what, "cluster", lo, hi, s)
+            outside = np.concatenate([ref_sigma[:lo], ref_sigma[hi:len(ref_sigma)]])
+            gap = float(np.min(np.abs(outside[:, None] - ref_sigma[None, lo:hi]))) if outside.size else np.inf
+            bound = max(ANGLE, DK_BACKWARD * smax / gap) if gap > 0 else np.inf
+            assert s <= bound, (what, "cluster", lo, hi, s, bound)
     return min_ov, max_sin
 
 
