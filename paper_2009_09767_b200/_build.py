@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libranky_b200.so")
-SOURCES = ["rk_scan.cu", "rk_ingest.cu", "rk_repair.cu", "rk_compact.cu", "rk_dense.cu", "rk_metrics.cu", "rk_eval.cu", "rk_workspace.cu", "rk_mm.cu", "rk_records.cu", "rk_qr.cu", "rk_gram.cu", "rk_precond.cu", "rk_spmm.cu",
+SOURCES = ["rk_scan.cu", "rk_ingest.cu", "rk_repair.cu", "rk_compact.cu", "rk_dense.cu", "rk_metrics.cu", "rk_eval.cu", "rk_workspace.cu", "rk_mm.cu", "rk_eig.cu", "rk_records.cu", "rk_qr.cu", "rk_gram.cu", "rk_precond.cu", "rk_spmm.cu",
            "rk_pipeline.cu", "rk_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

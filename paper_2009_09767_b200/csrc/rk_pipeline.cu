@@ -867,6 +867,9 @@ bool gram_merge_eligible(uint32_t M) { return gram_route_enabled() && M <= chole
 // the computed sigma). Returns false -- out untouched -- when rejected.
 bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out) {
   cudaStream_t s = c.stream;
+  // the eigensolver route first (G itself, no Cholesky); it declines for clustered
+  // spectra, M above its cluster-resident size, or kappa above the guard
+  if (gram_merge_eig(c, W.get(), M, out)) return true;
   const uint32_t cp = jacobi_cols_pad(M, M, false, c.smem_optin);
   // rows by descending diagonal, as the blocks' Grams (fewer sweeps)
   DBuf<uint32_t> perm;

@@ -68,6 +68,10 @@ bool gram_merge_eligible(uint32_t M);
 // the reference-algorithm flop count of a Jacobi run (rk_timing::jacobi_flops)
 double jacobi_flops_of(uint64_t sweeps, uint64_t rotations, uint32_t rows, uint32_t cols);
 bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out);
+// rk_eig.cu: the Gram route by a symmetric eigensolver (tridiagonalisation in one
+// cluster, bisection, inverse iteration); false (out untouched) when it declines
+bool eig_merge_eligible(uint32_t M);
+bool gram_merge_eig(Ctx& c, const double* G, uint32_t M, MergeOut& out);
 
 // dense_svd on the device: a is rows x cols row-major (device). Outputs row-major.
 struct DenseSvdOut {

@@ -215,3 +215,25 @@ def test_gram_kernels_bitwise(tuning_env):
         R.dev_outputs_free(out)
     for x, y in zip(outs[0], outs[1]):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("eig", ["1", "0"])
+def test_merge_gram_routes_agree(eig, tuning_env, ref):
+    """The merge's Gram route by the symmetric eigensolver (tridiagonalisation in one
+    cluster, bisection, inverse iteration; rk_eig.cu) and by Cholesky + one-sided
+    Jacobi (RK_EIG_MERGE=0) both reproduce the reference's run_pipeline on c2 slices
+    (well-conditioned merges: the Gram route is taken) and on c1 (rejected: TSQR)."""
+    tuning_env("RK_EIG_MERGE", eig)
+    cfg = configs.CONFIGS["c2"]
+    for scale, blocks in ((262144 // 8, 8), (262144 // 4, 16), (262144 // 16, 4)):
+        a = cfg.generate(scale)
+        r, c, v = a.coo()
+        res = rk.run_pipeline(a, blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True)
+        o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), blocks, cfg.method, cfg.keep, cfg.seed)
+        compare(res.svd, o.sigma, o.u, f"c2 slice {scale} eig {eig}")
+    c1 = configs.CONFIGS["c1"]
+    a = c1.generate()
+    r, c, v = a.coo()
+    res = rk.run_pipeline(a, c1.blocks, c1.method, c1.keep, c1.seed, 1)
+    o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), c1.blocks, c1.method, c1.keep, c1.seed)
+    compare(res.svd, o.sigma, o.u, f"c1 eig {eig}")
