@@ -381,6 +381,9 @@ def cpu_baseline(cfg, a):
 
 def main():
     args = parse()
+    if os.environ.get("RK_BENCH_WATCHDOG"):  # debugging aid: every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["RK_BENCH_WATCHDOG"]), exit=True)
     from paper_2009_09767_b200 import configs
     cfg = configs.CONFIGS[args.config]
     if args.impl == "reference":

@@ -319,7 +319,10 @@ __global__ void eig_finalize(const double* __restrict__ U_asc, const double* __r
 
 }  // namespace
 
-bool eig_merge_eligible(uint32_t M) { return tuning().eig_merge && M >= 8 && M <= kEigMaxM; }
+// measured: at M = 512 (c3) 7.0 ms against the Jacobi's 13 ms; at M = 256 (c2) the
+// Jacobi's 1.7 ms wins (255 tridiagonalisation steps of ~6 us each)
+constexpr uint32_t kEigMinM = 384;
+bool eig_merge_eligible(uint32_t M) { return tuning().eig_merge && M >= kEigMinM && M <= kEigMaxM; }
 
 bool gram_merge_eig(Ctx& c, const double* G, uint32_t M, MergeOut& out) {
   if (!eig_merge_eligible(M)) return false;
