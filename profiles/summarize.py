@@ -69,9 +69,13 @@ def launches(tag, src):
 
 
 def full(tag, src):
-    rep = os.path.join(src, f"{tag}_full.ncu-rep")
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    raw = os.path.join(src, f"{tag}_full_raw.csv")  # capture.sh exports it on the box (the .ncu-rep stays there)
+    if os.path.exists(raw):
+        out = open(raw).read()
+    else:
+        rep = os.path.join(src, f"{tag}_full.ncu-rep")
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
     res = OrderedDict()
@@ -104,7 +108,8 @@ def main():
     mine = {k: v for k, v in agg.items() if k.startswith("<unnamed>::") or k.startswith("rk::")}
     steps = 5  # capture.sh: --steps 2 --warmup 3, every step launches the same kernels
     total = sum(v[1] for v in mine.values()) / steps
-    md = [f"# {tag}: ncu launch list of `bench.py --steps 2 --warmup 3` (c2), per step",
+    cfg = os.environ.get("RK_CAPTURE_CONFIG", "c3")
+    md = [f"# {tag}: ncu launch list of `bench.py --config {cfg} --steps 2 --warmup 3`, per step",
           "", "Cold-cache, serialised per-launch times (`--clock-control none`); library kernels only.", "",
           "| kernel | launches/step | µs/step | share |", "|---|---:|---:|---:|"]
     for k, (n, ns) in sorted(mine.items(), key=lambda kv: -kv[1][1]):
