@@ -59,6 +59,7 @@ Tuning read_tuning() {
   t.repair_speculate = !flag("RK_REPAIR_SPECULATE", '0');
   if (const char* e = std::getenv("RK_WIDE_ROWS")) t.wide_rows_pow2 = std::string(e) != "32";
   t.eig_merge = !flag("RK_EIG_MERGE", '0');
+  t.spmm_tma = !flag("RK_SPMM_TMA", '0');
   return t;
 }
 std::mutex g_tuning_mu;

@@ -145,6 +145,78 @@ __global__ void __launch_bounds__(256) spmm_half_kernel(const uint64_t* __restri
   }
 }
 
+// The warp-per-column kernel with V's rows leaving through the TMA engine: a warp
+// accumulates its column's V row (r doubles, r even, r * 8 <= kTmaRowBytes) in
+// registers, writes it to a per-warp staging row in shared memory, and one lane
+// issues a bulk copy shared -> global (cp.async.bulk, the Blackwell TMA's 1-D mode):
+// whole 16-byte-aligned rows go out as bulk transactions instead of 32 x 16 B store
+// instructions per 512 B, and the warp moves on while the copy drains. Same
+// arithmetic and entry order as spmm_kernel: V is the same bits.
+constexpr int kTmaRowBytes = 4096;
+
+// every writing thread fences its generic-proxy smem writes for the async proxy
+// (fence_for_bulk), the warp synchronises, then one lane issues the copy
+__device__ __forceinline__ void fence_for_bulk() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_store_row(double* g, const double* s, uint32_t bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(256) spmm_tma_kernel(const uint64_t* __restrict__ col_ptr,
+                                                       const uint32_t* __restrict__ row_idx,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ u_ret,
+                                                       const double* __restrict__ inv, uint32_t r, uint64_t col_lo,
+                                                       uint64_t col_hi, double* __restrict__ v) {
+  constexpr int kMaxPairs = kTmaRowBytes / 16 / 32;  // double2 accumulators per lane (8 at 4 KB rows)
+  __shared__ __align__(128) double stage[8][kTmaRowBytes / 8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* srow = stage[wid];
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = col_lo + warp0; c < col_hi; c += nwarps) {
+    const uint64_t e0 = col_ptr[c], e1 = col_ptr[c + 1];
+    double2 acc[kMaxPairs];
+#pragma unroll
+    for (int k = 0; k < kMaxPairs; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (uint64_t e = e0; e < e1; ++e) {
+      const double x = val[e];
+      const double2* ur = reinterpret_cast<const double2*>(u_ret + (uint64_t)row_idx[e] * r);
+#pragma unroll
+      for (int k = 0; k < kMaxPairs; ++k) {
+        const uint32_t j = 64 * k + 2 * lane;
+        if (j < r) {
+          const double2 uu = ur[j / 2];
+          acc[k].x = __dadd_rn(acc[k].x, __dmul_rn(x, uu.x));
+          acc[k].y = __dadd_rn(acc[k].y, __dmul_rn(x, uu.y));
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_read();  // the previous row's copy has read the staging row
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kMaxPairs; ++k) {
+      const uint32_t j = 64 * k + 2 * lane;
+      if (j < r) {
+        double2 o;
+        o.x = __dmul_rn(acc[k].x, inv[j]);
+        o.y = __dmul_rn(acc[k].y, inv[j + 1]);
+        *reinterpret_cast<double2*>(srow + j) = o;
+      }
+    }
+    fence_for_bulk();
+    __syncwarp();
+    if (lane == 0) bulk_store_row(v + (c - col_lo) * r, srow, r * 8u);
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
 }  // namespace
 
 void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const uint32_t* retained,
@@ -168,6 +240,10 @@ void recover_v_device(const DevCsc& a, const double* u, uint32_t u_cols, const u
   if (!tuning().spmm_warp && r % 32 == 0 && r <= 256 && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
     spmm_half_kernel<8><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
                                              col_hi, v);
+  } else if (tuning().spmm_tma && (r & 1) == 0 && r * 8 <= (uint32_t)kTmaRowBytes &&
+             (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+    spmm_tma_kernel<<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
+                                         col_hi, v);
   } else if ((r & 1) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0)
     spmm_kernel<true><<<grid, 256, 0, s>>>(a.ptr.get(), a.idx.get(), a.val.get(), u_ret.get(), inv.get(), r, col_lo,
                                            col_hi, v);
