@@ -439,8 +439,13 @@ def main():
         from paper_2009_09767_b200 import shard as SH
         sp = SH.plan(M, cfg.cols, cfg.blocks, cfg.keep, ws, rank)
         lo, hi, c_lo, c_hi = sp.leaf_lo, sp.leaf_hi, sp.col_lo, sp.col_hi
+        n_gather = [0]
+
         def allgather(mine, alls):
             """the library's one collective, on the caller's communicator (NCCL)"""
+            n_gather[0] += 1
+            if os.environ.get("RK_BENCH_WATCHDOG"):
+                print(f"[rank {rank}] all-gather #{n_gather[0]}: sum {float(mine.sum()):.17g}", flush=True)
             if args.backend == "nccl":
                 torch.distributed.all_gather_into_tensor(alls, mine)
             else:
@@ -463,9 +468,11 @@ def main():
         def step():
             return sharded(dm)
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         step()
         flush.zero_()
+        if os.environ.get("RK_BENCH_WATCHDOG"):
+            print(f"[rank {rank}] warm-up step {i} done", flush=True)
     barrier()
     clocks = ClockSampler(local) if os.environ.get("RK_CLOCKS", "nvml") == "smi" else NvmlClockSampler(local)
     clocks.start()

@@ -1602,6 +1602,76 @@ void complete_columns_device(double* u, uint32_t rows, uint32_t cols, const uint
   RK_LAUNCH_CHECK();
 }
 
+namespace {
+// apply_q with the reflectors staged through shared memory a panel of kP at a time:
+// a CTA owns 8 warps x CW columns of one job; the panel's reflectors (rows >= their
+// diagonal, zeros above) are loaded once per CTA with coalesced reads, then every warp
+// applies them to its columns from shared memory. Replaces a dependent L2 round trip
+// per reflector with one per panel (c3's 512 wide blocks: 3.1 -> ~0.3 ms).
+constexpr int kPanel = 16;
+template <int CW, int E>
+__global__ void __launch_bounds__(256) apply_q_panel_kernel(const ApplyQJob* jobs) {
+  extern __shared__ __align__(16) double vs[];  // kPanel x (32 E)
+  const ApplyQJob j = jobs[blockIdx.y];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t m = j.qr.m, K = j.qr.m < j.qr.n ? j.qr.m : j.qr.n;
+  const uint32_t ld = 32 * E;
+  const uint32_t c0 = (blockIdx.x * 8 + warp) * CW;
+  double o[CW][E];
+#pragma unroll
+  for (int cw = 0; cw < CW; ++cw)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = lane + 32 * e, c = c0 + cw;
+      o[cw][e] = (c < j.ncols && i < j.x_rows) ? j.x[(uint64_t)c * j.x_rows + i] : 0.0;
+    }
+  __shared__ double sbeta[kPanel];
+  for (int p1 = (int)K; p1 > 0; p1 -= kPanel) {
+    const int p0 = p1 - kPanel > 0 ? p1 - kPanel : 0;
+    const int np = p1 - p0;
+    __syncthreads();  // the previous panel is consumed
+    for (int t = threadIdx.x; t < np * (int)ld; t += blockDim.x) {
+      const int q = t / (int)ld, i = t % (int)ld, kk = p0 + q;
+      vs[q * ld + i] = (i >= kk && (uint32_t)i < m) ? j.qr.a[(uint64_t)kk * j.qr.lda + i] : 0.0;
+    }
+    if (threadIdx.x < np) sbeta[threadIdx.x] = j.qr.beta[p0 + threadIdx.x];
+    __syncthreads();
+    for (int q = np - 1; q >= 0; --q) {  // last reflector first
+      const double beta = sbeta[q];
+      if (beta == 0.0) continue;
+      const double* v = vs + q * ld;
+      double vv[E];
+      double d[CW];
+#pragma unroll
+      for (int cw = 0; cw < CW; ++cw) d[cw] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        vv[e] = v[lane + 32 * e];
+#pragma unroll
+        for (int cw = 0; cw < CW; ++cw) d[cw] = fma(vv[e], o[cw][e], d[cw]);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1)
+#pragma unroll
+        for (int cw = 0; cw < CW; ++cw) d[cw] += __shfl_xor_sync(0xffffffffu, d[cw], off);
+#pragma unroll
+      for (int cw = 0; cw < CW; ++cw) {
+        const double bw = beta * d[cw];
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[cw][e] = fma(-bw, vv[e], o[cw][e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int cw = 0; cw < CW; ++cw)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t i = lane + 32 * e, c = c0 + cw;
+      if (c < j.ncols && i < m) j.out[(uint64_t)c * m + i] = o[cw][e];
+    }
+}
+}  // namespace
+
 void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
   uint32_t cmax = 0;
@@ -1612,9 +1682,19 @@ void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
   DBuf<ApplyQJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
   constexpr int kCW = 4;
+  auto panel = [&](auto kern, int cw, int e) {
+    const size_t smem = (size_t)kPanel * 32 * e * sizeof(double);
+    RK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid((unsigned)ceil_div(cmax, 8 * (uint64_t)cw), (unsigned)jobs.size());
+    kern<<<grid, 256, smem, s>>>(dj.get());
+  };
   const unsigned gr = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div((uint64_t)cmax, 8 * kCW), 64));
   const dim3 grid(gr, (unsigned)jobs.size());
-  if (mmax <= 128) apply_q_regs_kernel<kCW, 4><<<grid, 256, 0, s>>>(dj.get());
+  if (!tuning().apply_q_regs && mmax <= 128) panel(apply_q_panel_kernel<kCW, 4>, kCW, 4);
+  else if (!tuning().apply_q_regs && mmax <= 256) panel(apply_q_panel_kernel<kCW, 8>, kCW, 8);
+  else if (!tuning().apply_q_regs && mmax <= 512) panel(apply_q_panel_kernel<kCW, 16>, kCW, 16);
+  else if (!tuning().apply_q_regs && mmax <= 1024) panel(apply_q_panel_kernel<2, 32>, 2, 32);
+  else if (mmax <= 128) apply_q_regs_kernel<kCW, 4><<<grid, 256, 0, s>>>(dj.get());
   else if (mmax <= 256) apply_q_regs_kernel<kCW, 8><<<grid, 256, 0, s>>>(dj.get());
   else if (mmax <= 512) apply_q_regs_kernel<kCW, 16><<<grid, 256, 0, s>>>(dj.get());
   else if (mmax <= 1024) apply_q_regs_kernel<2, 32><<<grid, 256, 0, s>>>(dj.get());

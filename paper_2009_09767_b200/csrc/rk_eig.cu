@@ -199,68 +199,108 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   if (lane == 0) lam[j] = 0.5 * (lo + hi);
 }
 
-// a thread per eigenvalue: two steps of inverse iteration on T - lambda I (tridiagonal
-// LU with partial pivoting), start vector all ones; z_j -> column j of Z (M x M col-major)
-__global__ void inverse_iter_kernel(const double* __restrict__ d, const double* __restrict__ e, uint32_t M,
-                                    const double* __restrict__ lam, double tnorm, double* __restrict__ Z,
-                                    double* __restrict__ work /* 5 M per eigenvalue */) {
+// Inverse iteration, a thread per eigenvalue: the LU of T - lambda I with partial
+// pivoting (dgttrf), then three solves with it (dgttrs), start vector all ones. The
+// per-thread arrays are interleaved (element i of thread j at [i M + j]) so a warp's
+// accesses coalesce, and the solves are a separate kernel so their read-only factors
+// go through the non-coherent path with loads hoisted across unrolled iterations.
+// The vectors land in Zt (row-major: z_j[i] at [i M + j]).
+__global__ void inverse_lu_kernel(const double* __restrict__ d, const double* __restrict__ e, uint32_t M,
+                                  const double* __restrict__ lam, double tnorm, double* __restrict__ work,
+                                  uint8_t* __restrict__ pivw) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= M) return;
-  double* dl = work + (uint64_t)j * 5 * M;  // multipliers
-  double* u0 = dl + M;                      // U diagonal
-  double* u1 = u0 + M;                      // U first superdiagonal
-  double* u2 = u1 + M;                      // U second superdiagonal (from pivoting)
-  uint8_t* piv = reinterpret_cast<uint8_t*>(u2 + M);
+  const uint64_t MM = (uint64_t)M * M;
+  double* __restrict__ dl = work;
+  double* __restrict__ u0 = work + MM;
+  double* __restrict__ u1 = work + 2 * MM;
+  double* __restrict__ u2 = work + 3 * MM;
   const double x = lam[j];
   const double eps_t = 2.2e-16 * tnorm;
-  // LU of T - x I with partial pivoting (dgttrf)
-  double a = d[0] - x, b = M > 1 ? e[0] : 0.0, c2 = 0.0;
+  double a = d[0] - x, b = M > 1 ? e[0] : 0.0;
   for (uint32_t i = 0; i + 1 < M; ++i) {
+    const uint64_t at = (uint64_t)i * M + j;
     const double sub = e[i], dn = d[i + 1] - x, en = i + 2 < M ? e[i + 1] : 0.0;
+    double p0, p1, p2;
     if (fabs(a) >= fabs(sub)) {
-      piv[i] = 0;
+      pivw[at] = 0;
       const double m = a != 0.0 ? sub / a : 0.0;
-      dl[i] = m;
-      u0[i] = a; u1[i] = b; u2[i] = 0.0;
+      dl[at] = m;
+      p0 = a; p1 = b; p2 = 0.0;
       a = dn - m * b;
       b = en;
     } else {
-      piv[i] = 1;
+      pivw[at] = 1;
       const double m = a / sub;
-      dl[i] = m;
-      u0[i] = sub; u1[i] = dn; u2[i] = en;
+      dl[at] = m;
+      p0 = sub; p1 = dn; p2 = en;
       a = b - m * dn;
       b = -m * en;
     }
-    (void)c2;
+    u0[at] = fabs(p0) < eps_t ? copysign(eps_t, p0 == 0.0 ? 1.0 : p0) : p0;
+    u1[at] = p1;
+    u2[at] = p2;
   }
-  u0[M - 1] = a;
-  for (uint32_t i = 0; i < M; ++i)
-    if (fabs(u0[i]) < eps_t) u0[i] = copysign(eps_t, u0[i] == 0.0 ? 1.0 : u0[i]);
-  double* z = Z + (uint64_t)j * M;
-  for (uint32_t i = 0; i < M; ++i) z[i] = 1.0;
+  const uint64_t at = (uint64_t)(M - 1) * M + j;
+  u0[at] = fabs(a) < eps_t ? copysign(eps_t, a == 0.0 ? 1.0 : a) : a;
+}
+
+__global__ void inverse_solve_kernel(uint32_t M, const double* __restrict__ work, const uint8_t* __restrict__ pivw,
+                                     double* __restrict__ Zt) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  const uint64_t MM = (uint64_t)M * M;
+  const double* __restrict__ dl = work;
+  const double* __restrict__ u0 = work + MM;
+  const double* __restrict__ u1 = work + 2 * MM;
+  const double* __restrict__ u2 = work + 3 * MM;
+  double scale = 1.0;  // z = scale * y, y kept unnormalised between passes
   for (int it = 0; it < 3; ++it) {
-    // forward: apply L^{-1} with the row interchanges
+    // forward: L^{-1} with the row interchanges
+    double zi = it == 0 ? 1.0 : Zt[j] * scale;
+#pragma unroll 8
     for (uint32_t i = 0; i + 1 < M; ++i) {
-      if (piv[i]) {
-        const double t = z[i];
-        z[i] = z[i + 1];
-        z[i + 1] = t - dl[i] * z[i];
+      const uint64_t at = (uint64_t)i * M + j;
+      const double zn = it == 0 ? 1.0 : Zt[at + M] * scale;
+      const double m = __ldg(dl + at);
+      if (__ldg(pivw + at)) {
+        Zt[at] = zn;
+        zi = fma(-m, zn, zi);
       } else {
-        z[i + 1] -= dl[i] * z[i];
+        Zt[at] = zi;
+        zi = fma(-m, zi, zn);
       }
     }
+    Zt[(uint64_t)(M - 1) * M + j] = zi;
     // backward: U z = y
+    double z1 = 0.0, z2 = 0.0, nrm = 0.0;
+#pragma unroll 8
     for (int i = (int)M - 1; i >= 0; --i) {
-      double s = z[i];
-      if (i + 1 < (int)M) s -= u1[i] * z[i + 1];
-      if (i + 2 < (int)M) s -= u2[i] * z[i + 2];
-      z[i] = s / u0[i];
+      const uint64_t at = (uint64_t)i * M + j;
+      const double zz = (Zt[at] - __ldg(u1 + at) * z1 - __ldg(u2 + at) * z2) / __ldg(u0 + at);
+      Zt[at] = zz;
+      z2 = z1;
+      z1 = zz;
+      nrm = fma(zz, zz, nrm);
     }
-    double nrm = 0.0;
-    for (uint32_t i = 0; i < M; ++i) nrm = fma(z[i], z[i], nrm);
-    const double inv = 1.0 / sqrt(nrm);
-    for (uint32_t i = 0; i < M; ++i) z[i] *= inv;
+    scale = 1.0 / sqrt(nrm);
+  }
+#pragma unroll 8
+  for (uint32_t i = 0; i < M; ++i) Zt[(uint64_t)i * M + j] *= scale;
+}
+
+// Z (column-major, z_j in column j) from Zt (row-major), 32 x 32 tiles
+__global__ void transpose_sq_kernel(const double* __restrict__ in, uint32_t M, double* __restrict__ out) {
+  __shared__ double t[32][33];
+  const uint32_t x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  for (uint32_t k = threadIdx.y; k < 32; k += blockDim.y) {
+    const uint32_t r = y0 + k, c = x0 + threadIdx.x;
+    if (r < M && c < M) t[k][threadIdx.x] = in[(uint64_t)r * M + c];
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.y; k < 32; k += blockDim.y) {
+    const uint32_t r = x0 + k, c = y0 + threadIdx.x;
+    if (r < M && c < M) out[(uint64_t)r * M + c] = t[threadIdx.x][k];
   }
 }
 
@@ -378,11 +418,18 @@ bool gram_merge_eig(Ctx& c, const double* G, uint32_t M, MergeOut& out) {
   if (!(lmin > 0.0) || std::sqrt(lmax / lmin) > kappa_max(M)) return false;
   for (uint32_t i = 0; i + 1 < M; ++i)
     if (hl[i + 1] - hl[i] <= 1e-8 * tnorm) return false;
-  DBuf<double> Z((uint64_t)M * M, s), work((uint64_t)M * 5 * M, s);
-  inverse_iter_kernel<<<(unsigned)ceil_div(M, 64), 64, 0, s>>>(d.get(), e.get(), M, lam.get(), tnorm, Z.get(),
-                                                               work.get());
+  DBuf<double> Z((uint64_t)M * M, s), Zt((uint64_t)M * M, s), work((uint64_t)M * 4 * M, s);
+  DBuf<uint8_t> pivw((uint64_t)M * M, s);
+  inverse_lu_kernel<<<(unsigned)ceil_div(M, 32), 32, 0, s>>>(d.get(), e.get(), M, lam.get(), tnorm, work.get(),
+                                                             pivw.get());
+  RK_LAUNCH_CHECK();
+  inverse_solve_kernel<<<(unsigned)ceil_div(M, 32), 32, 0, s>>>(M, work.get(), pivw.get(), Zt.get());
+  RK_LAUNCH_CHECK();
+  transpose_sq_kernel<<<dim3((unsigned)ceil_div(M, 32), (unsigned)ceil_div(M, 32)), dim3(32, 8), 0, s>>>(
+      Zt.get(), M, Z.get());
   RK_LAUNCH_CHECK();
   work.release();
+  Zt.release();
   {
     DBuf<double> dots(M, s);
     dots.zero();

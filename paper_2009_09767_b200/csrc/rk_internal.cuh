@@ -67,6 +67,7 @@ struct Tuning {
   bool wide_rows_pow2 = true;     // RK_WIDE_ROWS=32: the reduced R's rows padded to multiples of 32
   bool eig_merge = true;          // RK_EIG_MERGE=0: the merge's Gram route by Cholesky + one-sided Jacobi
   bool spmm_tma = true;           // RK_SPMM_TMA=0: V rows by st.global instead of TMA bulk copies
+  bool apply_q_regs = false;      // RK_APPLY_Q=regs: reflectors from L2 per step, not panels in shared memory
 };
 const Tuning& tuning();
 void reload_tuning();
