@@ -190,18 +190,25 @@ def fp64_peak_tflops(torch):
 def profiled_traffic(dominant):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the newest
     committed `ncu --set full` summary (profiles/*_kernels.json, written by
-    profiles/summarize.py); None when there is none."""
+    profiles/summarize.py): the longest captured launch whose name matches the stage;
+    None when there is none."""
     import glob
-    names = {"block_jacobi": "jacobi_", "block_qr": "qr_kernel", "merge": "jacobi_cluster_kernel<32, 8"}
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))
+    names = {"block_jacobi": ("jacobi_cluster_kernel", "jacobi_warp_kernel"), "block_qr": ("qr_kernel",),
+             "merge": ("tridiag_cluster_kernel", "jacobi_cluster_kernel<32")}
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json")))  # tags sort by round
     for f in reversed(files):
         try:
             kern = json.load(open(f))
         except Exception:
             continue
+        best = None
         for k, launches in kern.items():
-            if names.get(dominant, "?") in k and launches and "traffic_bytes" in launches[0]:
-                return launches[0]["traffic_bytes"], os.path.relpath(f, ROOT) + " :: " + k
+            if any(n in k for n in names.get(dominant, ())) and launches and "traffic_bytes" in launches[0]:
+                d = max(launches, key=lambda x: x.get("duration_ms", 0.0))
+                if best is None or d.get("duration_ms", 0.0) > best[0].get("duration_ms", 0.0):
+                    best = (d, k)
+        if best:
+            return best[0]["traffic_bytes"], os.path.relpath(f, ROOT) + " :: " + best[1]
     return None, None
 
 
