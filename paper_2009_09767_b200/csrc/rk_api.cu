@@ -61,6 +61,7 @@ Tuning read_tuning() {
   t.eig_merge = !flag("RK_EIG_MERGE", '0');
   t.spmm_tma = !flag("RK_SPMM_TMA", '0');
   if (const char* e = std::getenv("RK_APPLY_Q")) t.apply_q_regs = std::string(e) == "regs";
+  t.jacobi_chunk_mb = (uint64_t)num("RK_JACOBI_CHUNK_MB", 0);
   return t;
 }
 std::mutex g_tuning_mu;

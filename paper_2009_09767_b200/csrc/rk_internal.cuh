@@ -68,6 +68,7 @@ struct Tuning {
   bool eig_merge = true;          // RK_EIG_MERGE=0: the merge's Gram route by Cholesky + one-sided Jacobi
   bool spmm_tma = true;           // RK_SPMM_TMA=0: V rows by st.global instead of TMA bulk copies
   bool apply_q_regs = false;      // RK_APPLY_Q=regs: reflectors from L2 per step, not panels in shared memory
+  uint64_t jacobi_chunk_mb = 0;   // RK_JACOBI_CHUNK_MB: cap a batched Jacobi launch's matrices (0: one launch)
 };
 const Tuning& tuning();
 void reload_tuning();

@@ -330,7 +330,18 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
     {
       RK_NVTX("rk.blocks.jacobi");
-      for (auto& kv : by_pad) jacobi_batched(kv.second, s, c.num_sms, c.smem_optin);
+      // launches sized so their matrices stay L2-resident (the kernel re-stages its
+      // column groups every tournament step): c3's 512 reduced matrices are 168 MB
+      const uint64_t cap = tuning().jacobi_chunk_mb << 20;
+      for (auto& kv : by_pad) {
+        std::vector<JacobiJob>& all = kv.second;
+        const uint64_t per = (uint64_t)kv.first.first * kv.first.second * sizeof(double);
+        const size_t n_chunk = cap ? std::max<size_t>(c.num_sms, cap / std::max<uint64_t>(per, 1)) : all.size();
+        for (size_t i0 = 0; i0 < all.size(); i0 += n_chunk) {
+          std::vector<JacobiJob> part(all.begin() + i0, all.begin() + std::min(all.size(), i0 + n_chunk));
+          jacobi_batched(part, s, c.num_sms, c.smem_optin);
+        }
+      }
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[10], s));
     apply_q_batched(aq, s);  // reduced slots: U Sigma = Q [R V; 0]
