@@ -43,6 +43,8 @@ Tuning read_tuning() {
   t.jacobi_gmax = (int)std::max(2.0, std::min(32.0, num("RK_JACOBI_GMAX", 16))) & ~1;
   t.jacobi_single_g = (int)num("RK_JACOBI_SINGLE_G", 8);
   if (const char* e = std::getenv("RK_JACOBI_WARP")) t.jacobi_warp = e[0] == '1' ? 1 : 0;
+  if (const char* e = std::getenv("RK_JACOBI_SMEM")) t.jacobi_smem = e[0] == '1' ? 1 : 0;
+  t.jacobi_smem_cl = (int)num("RK_JACOBI_SMEM_CL", 2);
   t.jacobi_check = num("RK_JACOBI_CHECK", -1.0);
   t.jacobi_cluster = (int)num("RK_JACOBI_CLUSTER", 0);
   t.jacobi_debug = std::getenv("RK_JACOBI_DEBUG") != nullptr;
@@ -563,6 +565,11 @@ rk_status rk_ctx_destroy(rk_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   for (auto& ev : ctx->c.ev) cudaEventDestroy(ev);
+  if (ctx->c.side) {
+    cudaStreamSynchronize(ctx->c.side);
+    cudaStreamDestroy(ctx->c.side);
+    for (auto& ev : ctx->c.side_ev) cudaEventDestroy(ev);
+  }
   if (ctx->c.copy) {
     cudaStreamSynchronize(ctx->c.copy);
     cudaStreamDestroy(ctx->c.copy);

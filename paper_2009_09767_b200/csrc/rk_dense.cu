@@ -1070,6 +1070,407 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
 }
 
 // ===========================================================================
+// Shared-memory-resident Gram-assisted Jacobi (matrices that fit a cluster's
+// shared memory: c3's reduced R factors, c2's 256 x 256 Cholesky factors)
+// ===========================================================================
+// The tournament and the step of jacobi_warp_kernel (H = X^T X by DMMA, the
+// step's rounds on H in the warp's shared memory, X <- X Z by DMMA), but the
+// matrix stays in shared memory for the whole run: a cluster of C CTAs holds it
+// (CTA r owns the column groups [r Gc, (r+1) Gc)), a warp reaches both groups of
+// its pair through (distributed) shared memory, and global memory is touched
+// twice: the load and the write-back. Only the first rows_nz rows are staged
+// (a reduced R is n_d x n_d in a taller zero-padded slot; zero rows stay zero).
+// Convergence is measured on the FRESH H of every step (all 120 pairs of the 16
+// columns, before any rotation touches H), so the within-step rounding of H on
+// graded columns cannot stall or fake it. A group pair whose fresh H has no
+// pair over the rotation threshold skips its rounds and its X Z. Hands over to
+// jacobi_cluster_kernel (check_first) once a sweep's largest fresh ratio is in
+// the quadratic regime; that kernel certifies on W with the reference's rule.
+struct SmemParams {
+  const JacobiJob* jobs;
+  uint32_t ld;        // shared-memory column stride (doubles), = 4 mod 8
+  uint32_t cap_cols;  // columns the layout holds per CTA (multiple of 8)
+  uint32_t nw;        // warps per CTA
+  double stop_ratio;
+};
+constexpr int kSH = kWN * kWS;  // doubles per warp: H (16 x 17); its pad column holds the round's 8 (c, s)
+constexpr int kSmemMaxWarps = 12;
+constexpr int kSmemMisc = 32 + 4;    // s_red, s_pub
+
+
+// One round of the step on H (16 x 17 in the warp's shared memory), all 32 lanes
+// on one instruction stream (no divergent halves):
+//   1. lanes 0..7 take the angles of the round's 8 disjoint pairs (every lane runs
+//      the arithmetic, selects instead of branches) -- and, in the same basic
+//      block, every lane applies the PREVIOUS round's rotations to its row of Z in
+//      registers, which hides under the angle's latency;
+//   2. H <- J^T H J in one pass: the 64 2 x 2 blocks (row pair i, column pair j)
+//      are independent (B' = J_i^T B J_j); a lane owns two of them.
+template <int KIND, int R>
+__device__ __forceinline__ void z_apply(double (&z)[kWN], const double (&cs)[16]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int p, q;
+    round_pair<KIND, R>(i, p, q);
+    const double x = z[p], y = z[q];
+    z[p] = cs[2 * i] * x - cs[2 * i + 1] * y;
+    z[q] = cs[2 * i + 1] * x + cs[2 * i] * y;
+  }
+}
+
+// PK/PR: the previous round (its rotations are in cs and still have to reach Z); PK < 0: none
+template <int KIND, int R, int PK, int PR>
+__device__ __forceinline__ void smem_round2(double* sH, double (&z)[kWN], double (&cs)[16],
+                                            double freeze, uint32_t& nrot) {
+  const int lane = threadIdx.x & 31;
+  {
+    int p, q;
+    round_pair<KIND, R>(lane & 7, p, q);
+    const double ap = sH[p * kWS + p], aq = sH[q * kWS + q], gm = sH[p * kWS + q];
+    if constexpr (PK >= 0) z_apply<PK, PR>(z, cs);  // independent of the angle: overlaps its latency
+    const double prod = ap * aq, g2 = gm * gm;
+    const bool rot = ap > freeze && aq > freeze && g2 > kJacobiTol * kJacobiTol * prod;
+    double c, sn;
+    rotation_cs(ap, aq, rot ? gm : 1.0, c, sn);
+    if (lane < 8) {
+      sH[(2 * lane) * kWS + kWN] = rot ? c : 1.0;
+      sH[(2 * lane + 1) * kWS + kWN] = rot ? sn : 0.0;
+      nrot += rot ? 1u : 0u;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cs[i] = sH[i * kWS + kWN];
+  {
+    const int i = lane >> 2, j0 = 2 * (lane & 3);
+    int pi, qi;
+    round_pair<KIND, R>(i, pi, qi);
+    const double ci = sH[(2 * i) * kWS + kWN], si = sH[(2 * i + 1) * kWS + kWN];
+    double* rp = sH + pi * kWS;
+    double* rq = sH + qi * kWS;
+    double b[2][4];
+    int pj[2], qj[2];
+    double cj[2], sj[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      round_pair<KIND, R>(j0 + u, pj[u], qj[u]);
+      cj[u] = sH[(2 * (j0 + u)) * kWS + kWN];
+      sj[u] = sH[(2 * (j0 + u) + 1) * kWS + kWN];
+      b[u][0] = rp[pj[u]];
+      b[u][1] = rp[qj[u]];
+      b[u][2] = rq[pj[u]];
+      b[u][3] = rq[qj[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double t00 = cj[u] * b[u][0] - sj[u] * b[u][1], t01 = sj[u] * b[u][0] + cj[u] * b[u][1];
+      const double t10 = cj[u] * b[u][2] - sj[u] * b[u][3], t11 = sj[u] * b[u][2] + cj[u] * b[u][3];
+      rp[pj[u]] = ci * t00 - si * t10;
+      rp[qj[u]] = ci * t01 - si * t11;
+      rq[pj[u]] = si * t00 + ci * t10;
+      rq[qj[u]] = si * t01 + ci * t11;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void smem_gram(const double* pA, const double* pB, uint32_t ld, uint32_t rows,
+                                          double* sH) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  const double* pa = pA + (uint32_t)lr * ld + lc;
+  const double* pb = pB + (uint32_t)lr * ld + lc;
+  double h[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) h[i] = 0.0;
+  uint32_t k0 = 0;
+  for (; k0 + 16 <= rows; k0 += 16) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = pa[k0 + 4 * u];
+      b[u] = pb[k0 + 4 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = (u & 1) * 6;
+      dmma884(h[o], h[o + 1], a[u], a[u]);
+      dmma884(h[o + 2], h[o + 3], b[u], a[u]);
+      dmma884(h[o + 4], h[o + 5], b[u], b[u]);
+    }
+  }
+  for (; k0 < rows; k0 += 8) {  // rows is a multiple of 8
+    const double a0 = pa[k0], b0 = pb[k0], a1 = pa[k0 + 4], b1 = pb[k0 + 4];
+    dmma884(h[0], h[1], a0, a0);
+    dmma884(h[2], h[3], b0, a0);
+    dmma884(h[4], h[5], b0, b0);
+    dmma884(h[6], h[7], a1, a1);
+    dmma884(h[8], h[9], b1, a1);
+    dmma884(h[10], h[11], b1, b1);
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int j = 2 * lc + e;
+    const double t00 = h[e] + h[6 + e], t10 = h[2 + e] + h[8 + e], t11 = h[4 + e] + h[10 + e];
+    sH[lr * kWS + j] = t00;
+    sH[(8 + lr) * kWS + j] = t10;
+    sH[j * kWS + 8 + lr] = t10;
+    sH[(8 + lr) * kWS + 8 + j] = t11;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void smem_xz(double* pA, double* pB, uint32_t ld, uint32_t rows, const double* sZ) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double bf[4][2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[kc][nt] = sZ[(4 * kc + lc) * kWN + 8 * nt + lr];
+  const double* src[4];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) {
+    const int t = 4 * kc + lc;
+    src[kc] = (t < kWG ? pA + (uint32_t)t * ld : pB + (uint32_t)(t - kWG) * ld) + lr;
+  }
+  double* dst[2][2];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int t = 8 * nt + 2 * lc + e;
+      dst[nt][e] = (t < kWG ? pA + (uint32_t)t * ld : pB + (uint32_t)(t - kWG) * ld) + lr;
+    }
+  constexpr int kRB = 4;  // 16 loads in flight; every lane's loads precede the first DMMA of the batch
+  for (uint32_t r0 = 0; r0 < rows; r0 += 8 * kRB) {
+    double af[kRB][4];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      const uint32_t r = r0 + 8 * u;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) af[u][kc] = r < rows ? src[kc][r] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      const uint32_t r = r0 + 8 * u;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) dmma884(d0, d1, af[u][kc], bf[kc][nt]);
+        if (r < rows) {
+          dst[nt][0][r] = d0;
+          dst[nt][1][r] = d1;
+        }
+      }
+    }
+  }
+}
+
+template <bool MULTI>
+__global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(SmemParams P) {
+  extern __shared__ __align__(16) double smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned rank = MULTI ? cluster.block_rank() : 0u, csize = MULTI ? cluster.num_blocks() : 1u;
+  const JacobiJob job = P.jobs[blockIdx.x / csize];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t ld = P.ld;
+  const uint32_t colsU = (job.cols + 15u) & ~15u;               // columns in the tournament
+  const uint32_t G = colsU / kWG, npairs = G / 2;
+  const uint32_t Gc = (G + csize - 1) / csize;                  // groups per CTA
+  const uint32_t rows = (min(job.rows, job.rows_nz ? job.rows_nz : job.rows) + 7u) & ~7u;  // staged rows
+  double* mat = smem;                                           // [cap_cols][ld]
+  double* sHall = mat + (uint64_t)P.cap_cols * ld;              // [nw][kSH]
+  double* s_red = sHall + (uint64_t)P.nw * kSH;                 // [32]
+  double* s_pub = s_red + 32;                                   // [4]: amax, ratio^2, rotations (bits), spare
+  double* sH = sHall + (uint64_t)warp * kSH;
+  double* W = job.w;
+  auto sync_all = [&]() {
+    if (MULTI) cluster.sync();
+    else __syncthreads();
+  };
+  auto group_ptr = [&](uint32_t grp) -> double* {  // first column of a group, wherever it lives
+    const uint32_t owner = grp / Gc, loc = grp - owner * Gc;
+    double* base = MULTI ? cluster.map_shared_rank(mat, owner) : mat;
+    return base + (uint64_t)loc * kWG * ld;
+  };
+  // ---- stage this CTA's columns (zero beyond the job's extents) ----
+  const uint32_t my_cols = min(Gc, G > rank * Gc ? G - rank * Gc : 0u) * kWG;
+  for (uint32_t c = warp; c < my_cols; c += P.nw) {
+    const uint32_t j = rank * Gc * kWG + c;
+    const double* wj = W + (uint64_t)j * job.rows;
+    for (uint32_t i = lane; i < rows; i += 32)
+      mat[(uint64_t)c * ld + i] = (j < job.cols_pad && i < job.rows) ? __ldcg(wj + i) : 0.0;
+  }
+  sync_all();
+  const uint32_t pw = rank * P.nw + warp;  // this warp's pair slot
+  unsigned long long total_rot = 0;
+  double last_ratio = 0.0, prev_ratio = INFINITY;
+#ifdef RK_SMEM_PROBE
+  long long pt[6] = {0, 0, 0, 0, 0, 0}, pt0 = 0;  // gram, ratio, rounds, xz, step barrier, sweep head/tail
+  long long skipped = 0, worked = 0;
+#define PROBE_T0() pt0 = clock64()
+#define PROBE_ADD(i) do { const long long now_ = clock64(); pt[i] += now_ - pt0; pt0 = now_; } while (0)
+#else
+#define PROBE_T0()
+#define PROBE_ADD(i)
+#endif
+  int sweep = 0;
+  constexpr int kSmemMaxSweeps = 40;
+  bool go = job.cols >= 2;
+  while (go) {
+    // ---- alpha_max of the sweep (freeze threshold, svd.cpp:222-231) ----
+    double amax = 0.0;
+    for (uint32_t c = warp; c < my_cols; c += P.nw) {
+      const double* x = mat + (uint64_t)c * ld;
+      double a = 0.0;
+      for (uint32_t i = lane; i < rows; i += 32) a += x[i] * x[i];
+      amax = fmax(amax, warp_sum(a));
+    }
+    if (lane == 0) s_red[warp] = amax;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (uint32_t i = 0; i < P.nw; ++i) t = fmax(t, s_red[i]);
+      s_pub[0] = t;
+    }
+    sync_all();
+    amax = 0.0;
+    for (unsigned r = 0; r < csize; ++r) amax = fmax(amax, (MULTI ? cluster.map_shared_rank(s_pub, r) : s_pub)[0]);
+    const double freeze = kJacobiTol * kJacobiTol * amax;
+    uint32_t nrot = 0;
+    double best_g2 = 0.0, best_prod = 1.0;  // the largest gamma^2 / (alpha_p alpha_q) as a fraction
+    for (uint32_t step = 0; step + 1 < G; ++step) {
+      if (pw < npairs) {
+        double* pA = group_ptr(rr_slot(pw, step, G));
+        double* pB = group_ptr(rr_slot(G - 1 - pw, step, G));
+        PROBE_T0();
+        smem_gram(pA, pB, ld, rows, sH);
+        PROBE_ADD(0);
+        // fresh ratios of the 16 columns' pairs; does any pair this step rotates exceed the threshold?
+        bool need = false;
+        {
+          // the 120 pairs folded into 8 rows of 15 (row fr, then row 15 - fr), 4 lanes a row
+          const int fr = lane >> 2, sub = lane & 3;
+#pragma unroll
+          for (int e0 = 0; e0 < 16; e0 += 4) {
+            const int e = e0 + sub;
+            if (e < 15) {
+              const bool first = e < 15 - fr;
+              const int i = first ? fr : 15 - fr, j = first ? fr + 1 + e : 1 + e;
+              const double aii = sH[i * kWS + i], ajj = sH[j * kWS + j], gij = sH[i * kWS + j];
+              const double prod = aii * ajj, g2 = gij * gij;
+              const bool live = aii > freeze && ajj > freeze;
+              if (live && g2 * best_prod > best_g2 * prod) {
+                best_g2 = g2;
+                best_prod = prod;
+              }
+              need = need || (live && g2 > kJacobiTol * kJacobiTol * prod && (step == 0 || (i < kWG && j >= kWG)));
+            }
+          }
+        }
+        const bool any_need = __any_sync(0xffffffffu, need);
+        PROBE_ADD(1);
+#ifdef RK_SMEM_PROBE
+        if (any_need) ++worked; else ++skipped;
+#endif
+        if (any_need) {
+          double z[kWN], cs[16];
+#pragma unroll
+          for (int k = 0; k < kWN; ++k) z[k] = (k == (lane & 15)) ? 1.0 : 0.0;  // lanes 16..31 mirror 0..15
+          if (step == 0) {
+            smem_round2<1, 0, -1, 0>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 1, 1, 0>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 2, 1, 1>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 3, 1, 2>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 4, 1, 3>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 5, 1, 4>(sH, z, cs, freeze, nrot);
+            smem_round2<1, 6, 1, 5>(sH, z, cs, freeze, nrot);
+            smem_round2<0, 0, 1, 6>(sH, z, cs, freeze, nrot);
+          } else {
+            smem_round2<0, 0, -1, 0>(sH, z, cs, freeze, nrot);
+          }
+          smem_round2<0, 1, 0, 0>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 2, 0, 1>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 3, 0, 2>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 4, 0, 3>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 5, 0, 4>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 6, 0, 5>(sH, z, cs, freeze, nrot);
+          smem_round2<0, 7, 0, 6>(sH, z, cs, freeze, nrot);
+          z_apply<0, 7>(z, cs);
+          if (lane < kWN) {  // H is dead: Z (16 x 16 row-major) takes its place
+#pragma unroll
+            for (int k = 0; k < kWN; ++k) sH[lane * kWN + k] = z[k];
+          }
+          __syncwarp();
+          PROBE_ADD(2);
+          smem_xz(pA, pB, ld, rows, sH);
+          PROBE_ADD(3);
+        }
+      }
+      PROBE_T0();
+      sync_all();
+      PROBE_ADD(4);
+    }
+    // ---- the sweep's rotations and largest fresh ratio, over the cluster ----
+    unsigned long long r64 = nrot;
+    double max_r2 = best_g2 / best_prod;
+    for (int o = 16; o; o >>= 1) {
+      r64 += __shfl_xor_sync(0xffffffffu, r64, o);
+      max_r2 = fmax(max_r2, __shfl_xor_sync(0xffffffffu, max_r2, o));
+    }
+    if (lane == 0) {
+      s_red[warp] = max_r2;
+      s_red[16 + warp] = __longlong_as_double((long long)r64);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      unsigned long long rr = 0;
+      for (uint32_t i = 0; i < P.nw; ++i) {
+        t = fmax(t, s_red[i]);
+        rr += (unsigned long long)__double_as_longlong(s_red[16 + i]);
+      }
+      s_pub[1] = t;
+      s_pub[2] = __longlong_as_double((long long)rr);
+    }
+    sync_all();
+    double t = 0.0;
+    unsigned long long rot = 0;
+    for (unsigned r = 0; r < csize; ++r) {
+      const double* pub = MULTI ? cluster.map_shared_rank(s_pub, r) : s_pub;
+      t = fmax(t, pub[1]);
+      rot += (unsigned long long)__double_as_longlong(pub[2]);
+    }
+    total_rot += rot;
+    last_ratio = sqrt(t);
+    ++sweep;
+    const bool stagnant = sweep >= 4 && last_ratio < 1e-4 && last_ratio > 0.25 * prev_ratio;
+    if (rot == 0 || last_ratio < P.stop_ratio || stagnant || sweep >= kSmemMaxSweeps) go = false;
+#ifdef RK_SMEM_PROBE
+    if (blockIdx.x == 0 && tid == 0)
+      printf("[smem] sweep %d rot %llu ratio %.2e | G %u rows %u cl %u | cyc gram %lld ratio %lld rounds %lld xz %lld bar %lld | worked %lld skipped %lld\n",
+             sweep, rot, last_ratio, G, rows, csize, pt[0], pt[1], pt[2], pt[3], pt[4], worked, skipped);
+#endif
+    prev_ratio = last_ratio;
+    sync_all();  // everyone has read the published values before the next sweep overwrites them
+  }
+  // ---- write back (only the staged rows: the rest of the slot was and stays zero) ----
+  for (uint32_t c = warp; c < my_cols; c += P.nw) {
+    const uint32_t j = rank * Gc * kWG + c;
+    if (j >= job.cols_pad) continue;
+    double* wj = W + (uint64_t)j * job.rows;
+    for (uint32_t i = lane; i < rows && i < job.rows; i += 32) wj[i] = mat[(uint64_t)c * ld + i];
+  }
+  if (rank == 0 && tid == 0) {
+    job.stats[0] = (uint64_t)sweep;
+    job.stats[1] = total_rot;
+    job.stats[2] = 0ull;
+    job.stats[3] = (uint64_t)__double_as_longlong(last_ratio);
+    job.stats[4] = job.stats[5] = job.stats[6] = 0ull;
+  }
+}
+
+// ===========================================================================
 // finalize
 // ===========================================================================
 
@@ -1450,6 +1851,100 @@ void jacobi_plan(uint32_t rows, uint32_t cols, bool with_v, size_t smem_budget, 
 size_t jacobi_smem(uint32_t rows, uint32_t g, uint32_t cols_pad, bool with_v) {
   return (size_t)2 * g * (rows + 8) * 8 + (with_v ? (size_t)2 * g * (cols_pad + 8) * 8 : 0) + (size_t)2 * g * 8;
 }
+// The shared-memory Jacobi over a batch: every job gets the smallest cluster whose
+// shared memory holds its staged matrix (a function of the job's own shape), jobs
+// of one cluster size share a launch. false (nothing launched): a job does not fit.
+static bool jacobi_smem_batched(const std::vector<JacobiJob>& jobs, const JacobiJob* d_jobs, cudaStream_t s,
+                                size_t smem_optin, double stop_ratio, const SideStream* side) {
+  struct Shape { uint32_t cl, cap_cols, nw, rows; };
+  auto shape_of = [&](const JacobiJob& j, Shape& sh) {
+    const uint32_t colsU = (j.cols + 15u) & ~15u, G = colsU / kWG, npairs = G / 2;
+    const uint32_t rows = (std::min(j.rows, j.rows_nz ? j.rows_nz : j.rows) + 7u) & ~7u;
+    // clusters of more than two CTAs lose to the direct kernel (measured on c2's 256 x 256: 11.5 vs 6.1 ms)
+    const uint32_t cl_max = (uint32_t)std::max(1, std::min(8, tuning().jacobi_smem_cl));
+    for (uint32_t cl = 1; cl <= cl_max; cl *= 2) {
+      const uint32_t Gc = (uint32_t)ceil_div(G, cl), nw = (uint32_t)ceil_div(npairs, cl);
+      const size_t bytes = ((size_t)Gc * kWG * (rows + 4) + (size_t)nw * kSH + kSmemMisc) * sizeof(double);
+      if (nw <= (uint32_t)kSmemMaxWarps && bytes <= smem_optin) {
+        sh = {cl, Gc * kWG, std::max(nw, 1u), rows};
+        return true;
+      }
+    }
+    return false;
+  };
+  // contiguous runs of one cluster size (a launch addresses jobs by blockIdx)
+  std::vector<Shape> shapes(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i)
+    if (!shape_of(jobs[i], shapes[i])) return false;
+  bool forked = false;
+  for (size_t i0 = 0; i0 < jobs.size();) {
+    size_t i1 = i0;
+    Shape m = shapes[i0];
+    while (i1 < jobs.size() && shapes[i1].cl == m.cl) {
+      m.cap_cols = std::max(m.cap_cols, shapes[i1].cap_cols);
+      m.nw = std::max(m.nw, shapes[i1].nw);
+      m.rows = std::max(m.rows, shapes[i1].rows);
+      ++i1;
+    }
+    // the widest and the tallest job of a run may differ: the layout must still fit
+    size_t bytes = ((size_t)m.cap_cols * (m.rows + 4) + (size_t)m.nw * kSH + kSmemMisc) * sizeof(double);
+    while (bytes > smem_optin && i1 > i0 + 1) {  // shorten the run until its envelope fits
+      --i1;
+      m = shapes[i0];
+      for (size_t i = i0; i < i1; ++i) {
+        m.cap_cols = std::max(m.cap_cols, shapes[i].cap_cols);
+        m.nw = std::max(m.nw, shapes[i].nw);
+        m.rows = std::max(m.rows, shapes[i].rows);
+      }
+      bytes = ((size_t)m.cap_cols * (m.rows + 4) + (size_t)m.nw * kSH + kSmemMisc) * sizeof(double);
+    }
+    SmemParams P{d_jobs + i0, m.rows + 4, m.cap_cols, m.nw, stop_ratio};
+    const unsigned n = (unsigned)(i1 - i0);
+    // runs are independent (disjoint jobs): every run but the last goes to the side
+    // stream, so a short run of clustered jobs shares the device with the main run
+    const bool aside = side && side->stream && i1 < jobs.size();
+    cudaStream_t ls = aside ? side->stream : s;
+    if (aside && !forked) {
+      RK_CUDA_CHECK(cudaEventRecord(side->fork, s));
+      RK_CUDA_CHECK(cudaStreamWaitEvent(side->stream, side->fork, 0));
+      forked = true;
+    }
+    if (m.cl == 1) {
+      RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      jacobi_smem_kernel<false><<<n, m.nw * 32, bytes, ls>>>(P);
+      RK_LAUNCH_CHECK();
+    } else {
+      void* args[] = {&P};
+      RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      launch_cluster_kernel((const void*)jacobi_smem_kernel<true>, n * m.cl, m.cl, m.nw * 32, bytes, ls, args);
+    }
+    i0 = i1;
+  }
+  if (forked) {
+    RK_CUDA_CHECK(cudaEventRecord(side->join, side->stream));
+    RK_CUDA_CHECK(cudaStreamWaitEvent(s, side->join, 0));
+  }
+  return true;
+}
+
+bool jacobi_smem_try(std::vector<JacobiJob>& jobs, cudaStream_t s, size_t smem_optin, const SideStream* side) {
+  const Tuning& tn = tuning();
+  if (jobs.empty() || tn.jacobi_smem == 0) return false;
+  for (const JacobiJob& j : jobs)
+    if (j.v || j.pre) return false;
+  // largest first: runs of one cluster size are contiguous, and the longest jobs of
+  // a launch start first (the last wave is the short ones)
+  std::stable_sort(jobs.begin(), jobs.end(), [](const JacobiJob& a, const JacobiJob& b) {
+    return std::max(a.cols, 1u) * (uint64_t)(a.rows_nz ? a.rows_nz : a.rows) >
+           std::max(b.cols, 1u) * (uint64_t)(b.rows_nz ? b.rows_nz : b.rows);
+  });
+  DBuf<JacobiJob> dj(jobs.size(), s);
+  to_device(dj.get(), jobs.data(), jobs.size(), s);
+  if (!jacobi_smem_batched(jobs, dj.get(), s, smem_optin, tn.jacobi_check >= 0 ? tn.jacobi_check : 1e-7, side)) return false;
+  for (JacobiJob& j : jobs) j.pre = 1;
+  return true;
+}
+
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency) {
   if (jobs.empty()) return;
   // jobs in one launch share rows / cols_pad / with_v (the caller groups them);
@@ -1486,6 +1981,13 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   const Tuning& tn = tuning();
   const bool warp_default = rows >= 512 && !latency;  // a function of the shape only (see latency)
   bool use_warp = (tn.jacobi_warp >= 0 ? tn.jacobi_warp == 1 : warp_default) && !with_v && cols_pad % 16 == 0;
+  // matrices that fit shared memory: the resident Gram-assisted kernel first (any
+  // conditioning: it measures convergence on fresh Grams and the direct kernel
+  // certifies) -- here, or already run by the caller over a larger batch (pre)
+  bool all_pre = true;
+  for (const JacobiJob& j : jobs) all_pre = all_pre && j.pre;
+  bool use_smem = all_pre || (!latency && jacobi_smem_try(jobs, s, smem_optin, nullptr));
+  if (use_smem) use_warp = false;
   if (use_warp) {
     WarpParams WP{nullptr, cols_pad / kWG, tn.jacobi_check >= 0 ? tn.jacobi_check : 1e-7};
     DBuf<JacobiJob> djw(jobs.size(), s);
@@ -1518,7 +2020,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // reference's rule whatever the threshold.
   const double check_default = latency ? 1e-7 : 1e-5;
   JacobiParams P{dj.get(), g, G, with_v ? 1 : 0, tn.jacobi_check >= 0 ? tn.jacobi_check : check_default,
-                 use_warp ? 1 : 0, tn.jacobi_debug ? 1 : 0};
+                 (use_warp || use_smem) ? 1 : 0, tn.jacobi_debug ? 1 : 0};
   void* kargs[] = {&P};
   // lanes per pair: enough lane groups for the g pairs of a round; E = column
   // elements per lane held in registers by the cross rounds (0: shared-memory path)

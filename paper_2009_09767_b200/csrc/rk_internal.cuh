@@ -50,6 +50,8 @@ struct Tuning {
   int jacobi_gmax = 16;           // RK_JACOBI_GMAX: group-size cap
   int jacobi_single_g = 8;        // RK_JACOBI_SINGLE_G: the merge's group size
   int jacobi_warp = -1;           // RK_JACOBI_WARP=0/1 (-1: by shape)
+  int jacobi_smem = -1;           // RK_JACOBI_SMEM=0/1: the shared-memory-resident Gram-assisted kernel (-1: batched blocks)
+  int jacobi_smem_cl = 2;         // RK_JACOBI_SMEM_CL: its largest cluster (1, 2, 4, 8)
   double jacobi_check = -1.0;     // RK_JACOBI_CHECK: tail-check ratio (<0: by workload; 0 off)
   int jacobi_cluster = 0;         // RK_JACOBI_CLUSTER: cluster size override (0: planned)
   bool jacobi_debug = false;      // RK_JACOBI_DEBUG=1
@@ -312,6 +314,9 @@ struct Ctx {
   // a second stream for result copies that overlap later stages (created on first use)
   cudaStream_t copy = nullptr;
   cudaEvent_t copy_ev[2] = {};
+  // a side stream for independent launches of one stage (created on first use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[2] = {};
 };
 
 // free device memory for planning. Exact (cudaMemGetInfo, slow) at the first call
@@ -410,12 +415,18 @@ struct JacobiJob {    // one-sided Jacobi on the columns of w (rows x cols, col-
   double* alpha;      // cols_pad scratch
   uint64_t* stats;    // [0] sweeps, [1] rotations, [2] status (0 ok, 1 not converged), [3] residual bits, [4..7] scratch
   uint32_t gram_ok = 0;  // well-conditioned (kappa <= kappa_max): the Gram-assisted kernel may run it
+  uint32_t rows_nz = 0;  // > 0: only the first rows_nz rows can be nonzero (a reduced R in a taller slot)
+  uint32_t pre = 0;      // jacobi_smem_try already ran it: jacobi_batched only certifies
 };
 // latency: one latency-critical matrix (the merge) -- smaller groups, larger
 // clusters. Never set for blocks: a block's rotation sequence (and with it its
 // rounding) must not depend on how many blocks share the launch, so that the
 // sharded path is bitwise identical for every rank count.
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency = false);
+// the shared-memory-resident Gram-assisted kernel over a (heterogeneous) batch without V; true: every job ran
+// (pre set) and jacobi_batched only has to certify. false: nothing was launched (a job does not fit, or switched off)
+struct SideStream { cudaStream_t stream; cudaEvent_t fork, join; };  // optional: independent launches overlap the main stream's
+bool jacobi_smem_try(std::vector<JacobiJob>& jobs, cudaStream_t s, size_t smem_optin, const SideStream* side);
 // rk_precond.cu: FP32 Jacobi sweeps, then W <- W V with V the (Newton-Schulz
 // orthogonalized) right singular vectors they give -- for gram_ok square jobs
 bool precondition_eligible(const JacobiJob& j);

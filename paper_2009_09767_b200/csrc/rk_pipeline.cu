@@ -323,6 +323,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       j.alpha = alpha.get() + (uint64_t)q * cols_pad_full;
       j.stats = stats.get() + 8 * q;
       j.gram_ok = gram_ok ? 1u : 0u;
+      j.rows_nz = reduced ? std::max<uint32_t>(cols[q], 1) : 0u;  // R is n_d x n_d
       jrows[q] = j.rows;
       by_pad[{j.rows, j.cols_pad}].push_back(j);
       if (reduced) aq.push_back({red->qr[q], red->mats[q], j.rows, cols[q], slots[q]});
@@ -333,6 +334,20 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       // launches sized so their matrices stay L2-resident (the kernel re-stages its
       // column groups every tournament step): c3's 512 reduced matrices are 168 MB
       const uint64_t cap = tuning().jacobi_chunk_mb << 20;
+      {
+        // one launch of the shared-memory kernel over every width class; the per-width
+        // launches below then only certify
+        std::vector<JacobiJob> every;
+        for (auto& kv : by_pad) every.insert(every.end(), kv.second.begin(), kv.second.end());
+        if (!c.side) {
+          RK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+          for (auto& ev : c.side_ev) RK_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        const SideStream side{c.side, c.side_ev[0], c.side_ev[1]};
+        if (jacobi_smem_try(every, s, c.smem_optin, &side))
+          for (auto& kv : by_pad)
+            for (JacobiJob& j : kv.second) j.pre = 1;
+      }
       for (auto& kv : by_pad) {
         std::vector<JacobiJob>& all = kv.second;
         const uint64_t per = (uint64_t)kv.first.first * kv.first.second * sizeof(double);
