@@ -62,7 +62,10 @@ Tuning read_tuning() {
   if (const char* e = std::getenv("RK_WIDE_ROWS")) t.wide_rows_pow2 = std::string(e) != "32";
   t.eig_merge = !flag("RK_EIG_MERGE", '0');
   t.spmm_tma = !flag("RK_SPMM_TMA", '0');
-  if (const char* e = std::getenv("RK_APPLY_Q")) t.apply_q_regs = std::string(e) == "regs";
+  if (const char* e = std::getenv("RK_APPLY_Q")) {
+    t.apply_q_regs = std::string(e) == "regs";
+    t.apply_q_wy = std::string(e) == "wy";
+  }
   t.jacobi_chunk_mb = (uint64_t)num("RK_JACOBI_CHUNK_MB", 0);
   return t;
 }

@@ -758,7 +758,9 @@ __global__ void __launch_bounds__(kJThreads, (E <= 16 && !(Q == 32 && GT == 8) ?
 // route admits its rounding stays far below the 1e-14 rotation threshold. Once a
 // sweep's largest |gamma| / sqrt(alpha_p alpha_q) is in the quadratic regime the
 // kernel hands over to jacobi_cluster_kernel, which certifies convergence on W
-// itself (tail_check) -- the reference's stopping rule.
+// itself (tail_check) -- the reference's stopping rule. Convergence is measured on
+// the fresh H of every step (fresh_scan), so the within-step rounding of H on graded
+// columns neither stalls nor fakes it: any conditioning may run here.
 constexpr int kWG = 8, kWN = 16, kWS = 17;
 
 struct WarpParams {
@@ -832,6 +834,143 @@ __device__ __forceinline__ void warp_round(double* sH, double* sCS, double (&z)[
       sH[lane * kWS + p] = cs[2 * i] * x - cs[2 * i + 1] * y;
       sH[lane * kWS + q] = cs[2 * i + 1] * x + cs[2 * i] * y;
     }
+  }
+  __syncwarp();
+}
+
+// One round of the step on H (16 x 17 in the warp's shared memory), all 32 lanes
+// on one instruction stream (no divergent halves):
+//   1. lanes 0..7 take the angles of the round's 8 disjoint pairs (every lane runs
+//      the arithmetic, selects instead of branches) -- and, in the same basic
+//      block, every lane applies the PREVIOUS round's rotations to its row of Z in
+//      registers, which hides under the angle's latency;
+//   2. H <- J^T H J in one pass: the 64 2 x 2 blocks (row pair i, column pair j)
+//      are independent (B' = J_i^T B J_j); a lane owns two of them.
+template <int KIND, int R>
+__device__ __forceinline__ void z_apply(double (&z)[kWN], const double (&cs)[16]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int p, q;
+    round_pair<KIND, R>(i, p, q);
+    const double x = z[p], y = z[q];
+    z[p] = cs[2 * i] * x - cs[2 * i + 1] * y;
+    z[q] = cs[2 * i + 1] * x + cs[2 * i] * y;
+  }
+}
+
+// PK/PR: the previous round (its rotations are in cs and still have to reach Z); PK < 0: none
+template <int KIND, int R, int PK, int PR>
+__device__ __forceinline__ void smem_round2(double* sH, double (&z)[kWN], double (&cs)[16],
+                                            double freeze, uint32_t& nrot) {
+  const int lane = threadIdx.x & 31;
+  {
+    int p, q;
+    round_pair<KIND, R>(lane & 7, p, q);
+    const double ap = sH[p * kWS + p], aq = sH[q * kWS + q], gm = sH[p * kWS + q];
+    if constexpr (PK >= 0) z_apply<PK, PR>(z, cs);  // independent of the angle: overlaps its latency
+    const double prod = ap * aq, g2 = gm * gm;
+    const bool rot = ap > freeze && aq > freeze && g2 > kJacobiTol * kJacobiTol * prod;
+    double c, sn;
+    rotation_cs(ap, aq, rot ? gm : 1.0, c, sn);
+    if (lane < 8) {
+      sH[(2 * lane) * kWS + kWN] = rot ? c : 1.0;
+      sH[(2 * lane + 1) * kWS + kWN] = rot ? sn : 0.0;
+      nrot += rot ? 1u : 0u;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cs[i] = sH[i * kWS + kWN];
+  {
+    const int i = lane >> 2, j0 = 2 * (lane & 3);
+    int pi, qi;
+    round_pair<KIND, R>(i, pi, qi);
+    const double ci = sH[(2 * i) * kWS + kWN], si = sH[(2 * i + 1) * kWS + kWN];
+    double* rp = sH + pi * kWS;
+    double* rq = sH + qi * kWS;
+    double b[2][4];
+    int pj[2], qj[2];
+    double cj[2], sj[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      round_pair<KIND, R>(j0 + u, pj[u], qj[u]);
+      cj[u] = sH[(2 * (j0 + u)) * kWS + kWN];
+      sj[u] = sH[(2 * (j0 + u) + 1) * kWS + kWN];
+      b[u][0] = rp[pj[u]];
+      b[u][1] = rp[qj[u]];
+      b[u][2] = rq[pj[u]];
+      b[u][3] = rq[qj[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double t00 = cj[u] * b[u][0] - sj[u] * b[u][1], t01 = sj[u] * b[u][0] + cj[u] * b[u][1];
+      const double t10 = cj[u] * b[u][2] - sj[u] * b[u][3], t11 = sj[u] * b[u][2] + cj[u] * b[u][3];
+      rp[pj[u]] = ci * t00 - si * t10;
+      rp[qj[u]] = ci * t01 - si * t11;
+      rq[pj[u]] = si * t00 + ci * t10;
+      rq[qj[u]] = si * t01 + ci * t11;
+    }
+  }
+  __syncwarp();
+}
+
+// The fresh H of a step (before any rotation touches it): the largest
+// gamma^2 / (alpha_p alpha_q) over the 120 pairs of its 16 columns, kept as a
+// fraction (best_g2 / best_prod), and whether any pair this step rotates (all of
+// them in step 0, the cross pairs later) is over the rotation threshold. The pairs
+// are folded into 8 rows of 15 (row fr, then row 15 - fr), 4 lanes a row.
+__device__ __forceinline__ bool fresh_scan(const double* sH, double freeze, bool intra, double& best_g2,
+                                           double& best_prod) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, sub = lane & 3;
+  bool need = false;
+#pragma unroll
+  for (int e0 = 0; e0 < 16; e0 += 4) {
+    const int e = e0 + sub;
+    if (e < 15) {
+      const bool first = e < 15 - fr;
+      const int i = first ? fr : 15 - fr, j = first ? fr + 1 + e : 1 + e;
+      const double aii = sH[i * kWS + i], ajj = sH[j * kWS + j], gij = sH[i * kWS + j];
+      const double prod = aii * ajj, g2 = gij * gij;
+      const bool live = aii > freeze && ajj > freeze;
+      if (live && g2 * best_prod > best_g2 * prod) {
+        best_g2 = g2;
+        best_prod = prod;
+      }
+      need = need || (live && g2 > kJacobiTol * kJacobiTol * prod && (intra || (i < kWG && j >= kWG)));
+    }
+  }
+  return __any_sync(0xffffffffu, need);
+}
+
+// The rounds of one step on H; leaves Z (16 x 16 row-major, stride kWN) where H was.
+__device__ __forceinline__ void step_rounds(double* sH, bool intra, double freeze, uint32_t& nrot) {
+  const int lane = threadIdx.x & 31;
+  double z[kWN], cs[16];
+#pragma unroll
+  for (int k = 0; k < kWN; ++k) z[k] = (k == (lane & 15)) ? 1.0 : 0.0;  // lanes 16..31 mirror 0..15
+  if (intra) {
+    smem_round2<1, 0, -1, 0>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 1, 1, 0>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 2, 1, 1>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 3, 1, 2>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 4, 1, 3>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 5, 1, 4>(sH, z, cs, freeze, nrot);
+    smem_round2<1, 6, 1, 5>(sH, z, cs, freeze, nrot);
+    smem_round2<0, 0, 1, 6>(sH, z, cs, freeze, nrot);
+  } else {
+    smem_round2<0, 0, -1, 0>(sH, z, cs, freeze, nrot);
+  }
+  smem_round2<0, 1, 0, 0>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 2, 0, 1>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 3, 0, 2>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 4, 0, 3>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 5, 0, 4>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 6, 0, 5>(sH, z, cs, freeze, nrot);
+  smem_round2<0, 7, 0, 6>(sH, z, cs, freeze, nrot);
+  z_apply<0, 7>(z, cs);
+  if (lane < kWN) {  // H is dead: Z takes its place
+#pragma unroll
+    for (int k = 0; k < kWN; ++k) sH[lane * kWN + k] = z[k];
   }
   __syncwarp();
 }
@@ -940,15 +1079,13 @@ __device__ __forceinline__ void warp_xz(double* __restrict__ W, uint32_t rows, u
   }
 }
 
-__global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
+__global__ void __launch_bounds__(kJThreads, 2) jacobi_warp_kernel(WarpParams P) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
   const JacobiJob job = P.jobs[blockIdx.x / csize];
   const uint32_t rows = job.rows, cols_pad = job.cols_pad, G = P.G, npairs = G / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ double sH[kJWarps][kWN * kWS];
-  __shared__ double sZ[kJWarps][kWN * kWN];
-  __shared__ double sCS[kJWarps][16];
+  __shared__ double sH[kJWarps][kWN * kWS];  // H, then Z (step_rounds)
   __shared__ double s_red[kJWarps];
   __shared__ double s_amax;
   __shared__ unsigned long long s_rot;
@@ -990,43 +1127,24 @@ __global__ void __launch_bounds__(kJThreads) jacobi_warp_kernel(WarpParams P) {
     __syncthreads();
     const double freeze = kJacobiTol * kJacobiTol * s_amax;
     uint32_t nrot = 0;
-    double max_r2 = 0.0;
+    double best_g2 = 0.0, best_prod = 1.0;  // the sweep's largest fresh ratio^2, as a fraction
     for (uint32_t step = 0; step + 1 < G; ++step) {
       for (uint32_t pw = w; pw < npairs; pw += csize * kJWarps) {
         const uint32_t cA = rr_slot(pw, step, G) * kWG, cB = rr_slot(G - 1 - pw, step, G) * kWG;
         double* h = sH[warp];
         warp_gram(W, rows, cA, cB, h);
-        double z[kWN];
-#pragma unroll
-        for (int k = 0; k < kWN; ++k) z[k] = (k == lane - 16) ? 1.0 : 0.0;
-        if (step == 0) {
-          warp_round<1, 0>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 1>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 2>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 3>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 4>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 5>(h, sCS[warp], z, freeze, max_r2, nrot);
-          warp_round<1, 6>(h, sCS[warp], z, freeze, max_r2, nrot);
+        // rotate only where the fresh H has a pair over the threshold (late sweeps: few)
+        if (fresh_scan(h, freeze, step == 0, best_g2, best_prod)) {
+          step_rounds(h, step == 0, freeze, nrot);
+          warp_xz(W, rows, cA, cB, h);
         }
-        warp_round<0, 0>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 1>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 2>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 3>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 4>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 5>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 6>(h, sCS[warp], z, freeze, max_r2, nrot);
-        warp_round<0, 7>(h, sCS[warp], z, freeze, max_r2, nrot);
-        if (lane >= kWN) {
-#pragma unroll
-          for (int k = 0; k < kWN; ++k) sZ[warp][(lane - kWN) * kWN + k] = z[k];
-        }
-        __syncwarp();
-        warp_xz(W, rows, cA, cB, sZ[warp]);
+        __syncwarp();  // Z is consumed before the next pair's H lands on it
       }
       cluster.sync();
     }
     // rotations and the largest ratio of the sweep, over the cluster
     unsigned long long r64 = nrot;
+    double max_r2 = best_g2 / best_prod;
     for (int o = 16; o; o >>= 1) {
       r64 += __shfl_xor_sync(0xffffffffu, r64, o);
       max_r2 = fmax(max_r2, __shfl_xor_sync(0xffffffffu, max_r2, o));
@@ -1097,82 +1215,6 @@ constexpr int kSH = kWN * kWS;  // doubles per warp: H (16 x 17); its pad column
 constexpr int kSmemMaxWarps = 12;
 constexpr int kSmemMisc = 32 + 4;    // s_red, s_pub
 
-
-// One round of the step on H (16 x 17 in the warp's shared memory), all 32 lanes
-// on one instruction stream (no divergent halves):
-//   1. lanes 0..7 take the angles of the round's 8 disjoint pairs (every lane runs
-//      the arithmetic, selects instead of branches) -- and, in the same basic
-//      block, every lane applies the PREVIOUS round's rotations to its row of Z in
-//      registers, which hides under the angle's latency;
-//   2. H <- J^T H J in one pass: the 64 2 x 2 blocks (row pair i, column pair j)
-//      are independent (B' = J_i^T B J_j); a lane owns two of them.
-template <int KIND, int R>
-__device__ __forceinline__ void z_apply(double (&z)[kWN], const double (&cs)[16]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int p, q;
-    round_pair<KIND, R>(i, p, q);
-    const double x = z[p], y = z[q];
-    z[p] = cs[2 * i] * x - cs[2 * i + 1] * y;
-    z[q] = cs[2 * i + 1] * x + cs[2 * i] * y;
-  }
-}
-
-// PK/PR: the previous round (its rotations are in cs and still have to reach Z); PK < 0: none
-template <int KIND, int R, int PK, int PR>
-__device__ __forceinline__ void smem_round2(double* sH, double (&z)[kWN], double (&cs)[16],
-                                            double freeze, uint32_t& nrot) {
-  const int lane = threadIdx.x & 31;
-  {
-    int p, q;
-    round_pair<KIND, R>(lane & 7, p, q);
-    const double ap = sH[p * kWS + p], aq = sH[q * kWS + q], gm = sH[p * kWS + q];
-    if constexpr (PK >= 0) z_apply<PK, PR>(z, cs);  // independent of the angle: overlaps its latency
-    const double prod = ap * aq, g2 = gm * gm;
-    const bool rot = ap > freeze && aq > freeze && g2 > kJacobiTol * kJacobiTol * prod;
-    double c, sn;
-    rotation_cs(ap, aq, rot ? gm : 1.0, c, sn);
-    if (lane < 8) {
-      sH[(2 * lane) * kWS + kWN] = rot ? c : 1.0;
-      sH[(2 * lane + 1) * kWS + kWN] = rot ? sn : 0.0;
-      nrot += rot ? 1u : 0u;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) cs[i] = sH[i * kWS + kWN];
-  {
-    const int i = lane >> 2, j0 = 2 * (lane & 3);
-    int pi, qi;
-    round_pair<KIND, R>(i, pi, qi);
-    const double ci = sH[(2 * i) * kWS + kWN], si = sH[(2 * i + 1) * kWS + kWN];
-    double* rp = sH + pi * kWS;
-    double* rq = sH + qi * kWS;
-    double b[2][4];
-    int pj[2], qj[2];
-    double cj[2], sj[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      round_pair<KIND, R>(j0 + u, pj[u], qj[u]);
-      cj[u] = sH[(2 * (j0 + u)) * kWS + kWN];
-      sj[u] = sH[(2 * (j0 + u) + 1) * kWS + kWN];
-      b[u][0] = rp[pj[u]];
-      b[u][1] = rp[qj[u]];
-      b[u][2] = rq[pj[u]];
-      b[u][3] = rq[qj[u]];
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const double t00 = cj[u] * b[u][0] - sj[u] * b[u][1], t01 = sj[u] * b[u][0] + cj[u] * b[u][1];
-      const double t10 = cj[u] * b[u][2] - sj[u] * b[u][3], t11 = sj[u] * b[u][2] + cj[u] * b[u][3];
-      rp[pj[u]] = ci * t00 - si * t10;
-      rp[qj[u]] = ci * t01 - si * t11;
-      rq[pj[u]] = si * t00 + ci * t10;
-      rq[qj[u]] = si * t01 + ci * t11;
-    }
-  }
-  __syncwarp();
-}
 
 __device__ __forceinline__ void smem_gram(const double* pA, const double* pB, uint32_t ld, uint32_t rows,
                                           double* sH) {
@@ -1347,61 +1389,13 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(Smem
         smem_gram(pA, pB, ld, rows, sH);
         PROBE_ADD(0);
         // fresh ratios of the 16 columns' pairs; does any pair this step rotates exceed the threshold?
-        bool need = false;
-        {
-          // the 120 pairs folded into 8 rows of 15 (row fr, then row 15 - fr), 4 lanes a row
-          const int fr = lane >> 2, sub = lane & 3;
-#pragma unroll
-          for (int e0 = 0; e0 < 16; e0 += 4) {
-            const int e = e0 + sub;
-            if (e < 15) {
-              const bool first = e < 15 - fr;
-              const int i = first ? fr : 15 - fr, j = first ? fr + 1 + e : 1 + e;
-              const double aii = sH[i * kWS + i], ajj = sH[j * kWS + j], gij = sH[i * kWS + j];
-              const double prod = aii * ajj, g2 = gij * gij;
-              const bool live = aii > freeze && ajj > freeze;
-              if (live && g2 * best_prod > best_g2 * prod) {
-                best_g2 = g2;
-                best_prod = prod;
-              }
-              need = need || (live && g2 > kJacobiTol * kJacobiTol * prod && (step == 0 || (i < kWG && j >= kWG)));
-            }
-          }
-        }
-        const bool any_need = __any_sync(0xffffffffu, need);
+        const bool any_need = fresh_scan(sH, freeze, step == 0, best_g2, best_prod);
         PROBE_ADD(1);
 #ifdef RK_SMEM_PROBE
         if (any_need) ++worked; else ++skipped;
 #endif
         if (any_need) {
-          double z[kWN], cs[16];
-#pragma unroll
-          for (int k = 0; k < kWN; ++k) z[k] = (k == (lane & 15)) ? 1.0 : 0.0;  // lanes 16..31 mirror 0..15
-          if (step == 0) {
-            smem_round2<1, 0, -1, 0>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 1, 1, 0>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 2, 1, 1>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 3, 1, 2>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 4, 1, 3>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 5, 1, 4>(sH, z, cs, freeze, nrot);
-            smem_round2<1, 6, 1, 5>(sH, z, cs, freeze, nrot);
-            smem_round2<0, 0, 1, 6>(sH, z, cs, freeze, nrot);
-          } else {
-            smem_round2<0, 0, -1, 0>(sH, z, cs, freeze, nrot);
-          }
-          smem_round2<0, 1, 0, 0>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 2, 0, 1>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 3, 0, 2>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 4, 0, 3>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 5, 0, 4>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 6, 0, 5>(sH, z, cs, freeze, nrot);
-          smem_round2<0, 7, 0, 6>(sH, z, cs, freeze, nrot);
-          z_apply<0, 7>(z, cs);
-          if (lane < kWN) {  // H is dead: Z (16 x 16 row-major) takes its place
-#pragma unroll
-            for (int k = 0; k < kWN; ++k) sH[lane * kWN + k] = z[k];
-          }
-          __syncwarp();
+          step_rounds(sH, step == 0, freeze, nrot);
           PROBE_ADD(2);
           smem_xz(pA, pB, ld, rows, sH);
           PROBE_ADD(3);
@@ -2183,6 +2177,12 @@ void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
   for (const ApplyQJob& j : jobs) mmax = std::max(mmax, j.qr.m);
   DBuf<ApplyQJob> dj(jobs.size(), s);
   to_device(dj.get(), jobs.data(), jobs.size(), s);
+  {  // factored with T kept: the compact-WY apply on the tensor cores
+    uint32_t nbw = jobs[0].wy_nb;
+    for (const ApplyQJob& j : jobs)
+      if (j.wy_nb != nbw || j.qr.split || !j.qr.tmat) nbw = 0;
+    if (nbw && tuning().apply_q_wy && apply_q_wy_batched(dj.get(), jobs.size(), mmax, nbw, s)) return;
+  }
   constexpr int kCW = 4;
   auto panel = [&](auto kern, int cw, int e) {
     const size_t smem = (size_t)kPanel * 32 * e * sizeof(double);

@@ -70,6 +70,7 @@ struct Tuning {
   bool eig_merge = true;          // RK_EIG_MERGE=0: the merge's Gram route by Cholesky + one-sided Jacobi
   bool spmm_tma = true;           // RK_SPMM_TMA=0: V rows by st.global instead of TMA bulk copies
   bool apply_q_regs = false;      // RK_APPLY_Q=regs: reflectors from L2 per step, not panels in shared memory
+  bool apply_q_wy = true;         // RK_APPLY_Q=panel|regs: no compact-WY apply for factored jobs that kept T
   uint64_t jacobi_chunk_mb = 0;   // RK_JACOBI_CHUNK_MB: cap a batched Jacobi launch's matrices (0: one launch)
 };
 const Tuning& tuning();
@@ -475,7 +476,11 @@ struct ApplyQJob {    // out (qr.m x ncols col-major, ld qr.m) = Q [x; 0], x x_r
   const double* x;
   uint32_t x_rows, ncols;
   double* out;
+  uint32_t wy_nb = 0;  // > 0: qr.tmat holds the compact-WY T factors of panels this wide (dense job)
 };
+// rk_qr.cu: the panel width qr_batched factors an h_max-row batch with; apply_q through the T factors
+uint32_t qr_panel_nb(uint32_t h_max);
+bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t nb, cudaStream_t s);
 void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s);
 
 // rk_spmm.cu -- V = A^T U Sigma^-1 over the CSC

@@ -326,7 +326,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       j.rows_nz = reduced ? std::max<uint32_t>(cols[q], 1) : 0u;  // R is n_d x n_d
       jrows[q] = j.rows;
       by_pad[{j.rows, j.cols_pad}].push_back(j);
-      if (reduced) aq.push_back({red->qr[q], red->mats[q], j.rows, cols[q], slots[q]});
+      if (reduced) aq.push_back({red->qr[q], red->mats[q], j.rows, cols[q], slots[q], qr_panel_nb(M)});
     }
     RK_CUDA_CHECK(cudaEventRecord(c.ev[9], s));
     {

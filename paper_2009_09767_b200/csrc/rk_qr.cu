@@ -39,6 +39,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileN = 8;  // columns per warp tile (MMA n)
+constexpr int kKB = 8;     // k-steps (4 rows each) whose loads are issued together
+constexpr int kRBq = 4;    // 8-row blocks whose loads are issued together
 
 __device__ __forceinline__ double wsum(double x) {
 #pragma unroll
@@ -187,8 +189,7 @@ __global__ void __launch_bounds__(kThreads, 2) qr_kernel(const QrJob* __restrict
         double* dst = A + (uint64_t)(k0 + q) * lda;
         for (int i = tid; i < h; i += kThreads) dst[R(i)] = P[q * ldp + i];
       }
-      if (csize > 1)
-        for (int t = tid; t < NB * NB; t += kThreads) tglob[t] = sT[t];
+      for (int t = tid; t < NB * NB; t += kThreads) tglob[t] = sT[t];  // kept: apply_q_wy reads it
     }
     csync();
     if (rank != 0) {
@@ -213,14 +214,24 @@ __global__ void __launch_bounds__(kThreads, 2) qr_kernel(const QrJob* __restrict
       double w[(NB + 7) / 8][2];
 #pragma unroll
       for (int hh = 0; hh < (NB + 7) / 8; ++hh) w[hh][0] = w[hh][1] = 0.0;
-      for (int i0 = 0; i0 < h; i0 += 4) {
-        const int i = i0 + lc;
-        const double bv = (jb_ok && i < h) ? __ldcg(cb + R(i)) : 0.0;
+      // 8 k-steps per batch: the batch's loads are in flight together (one L2 round
+      // trip per 32 rows instead of one per 4)
+      for (int i0 = 0; i0 < h; i0 += 4 * kKB) {
+        double bv[kKB];
 #pragma unroll
-        for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
-          const int r = hh * 8 + lr;
-          const double av = (r < nbk && i >= r && i < h) ? P[r * ldp + i] : 0.0;
-          dmma(w[hh][0], w[hh][1], av, bv);
+        for (int u = 0; u < kKB; ++u) {
+          const int i = i0 + 4 * u + lc;
+          bv[u] = (jb_ok && i < h) ? __ldcg(cb + R(i)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kKB; ++u) {
+          const int i = i0 + 4 * u + lc;
+#pragma unroll
+          for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
+            const int r = hh * 8 + lr;
+            const double av = (r < nbk && i >= r && i < h) ? P[r * ldp + i] : 0.0;
+            dmma(w[hh][0], w[hh][1], av, bv[u]);
+          }
         }
       }
       // W -> smem (row r = hh*8 + lr, cols 2lc, 2lc+1), then W' = -(T^T W) in place
@@ -255,27 +266,171 @@ __global__ void __launch_bounds__(kThreads, 2) qr_kernel(const QrJob* __restrict
       const int ja = j0 + 2 * lc;
       double* ca0 = A + (uint64_t)min(ja, n - 1) * lda;
       double* ca1 = A + (uint64_t)min(ja + 1, n - 1) * lda;
-      for (int i0 = 0; i0 < h; i0 += 8) {
-        const int i = i0 + lr;
-        const bool row_ok = i < h;
-        const uint32_t gi = row_ok ? R(i) : 0u;
-        double d0 = (row_ok && ja < n) ? __ldcg(ca0 + gi) : 0.0;
-        double d1 = (row_ok && ja + 1 < n) ? __ldcg(ca1 + gi) : 0.0;
+      double bw[(NB + 3) / 4];
 #pragma unroll
-        for (int kk = 0; kk < NB; kk += 4) {
-          const int r = kk + lc;
-          const double av = (r < nbk && row_ok && i >= r) ? P[r * ldp + i] : 0.0;
-          const double bv = (kk + lc < NB) ? wt[(kk + lc) * 8 + lr] : 0.0;
-          dmma(d0, d1, av, bv);
+      for (int kk = 0; kk < NB; kk += 4) bw[kk / 4] = (kk + lc < NB) ? wt[(kk + lc) * 8 + lr] : 0.0;
+      for (int i0 = 0; i0 < h; i0 += 8 * kRBq) {
+        double d0[kRBq], d1[kRBq];
+        uint32_t gi[kRBq];
+#pragma unroll
+        for (int u = 0; u < kRBq; ++u) {
+          const int i = i0 + 8 * u + lr;
+          const bool row_ok = i < h;
+          gi[u] = row_ok ? R(i) : 0u;
+          d0[u] = (row_ok && ja < n) ? __ldcg(ca0 + gi[u]) : 0.0;
+          d1[u] = (row_ok && ja + 1 < n) ? __ldcg(ca1 + gi[u]) : 0.0;
         }
-        if (row_ok) {
-          if (ja < n) ca0[gi] = d0;
-          if (ja + 1 < n) ca1[gi] = d1;
+#pragma unroll
+        for (int u = 0; u < kRBq; ++u) {
+          const int i = i0 + 8 * u + lr;
+          const bool row_ok = i < h;
+#pragma unroll
+          for (int kk = 0; kk < NB; kk += 4) {
+            const int r = kk + lc;
+            const double av = (r < nbk && row_ok && i >= r) ? P[r * ldp + i] : 0.0;
+            dmma(d0[u], d1[u], av, bw[kk / 4]);
+          }
+          if (row_ok) {
+            if (ja < n) ca0[gi[u]] = d0[u];
+            if (ja + 1 < n) ca1[gi[u]] = d1[u];
+          }
         }
       }
       __syncwarp();
     }
     csync();
+  }
+}
+
+
+// out (m x ncols, ld m) = Q [x; 0] for a job factored by qr_kernel<NB> (dense, not
+// stacked), through the compact-WY panels the factorisation left in tmat:
+// Q = Q_1 Q_2 ... Q_P, Q_p = I - V_p T_p V_p^T, applied last panel first. One CTA per
+// job, one warp per 8-column tile of out (the tile stays with its warp for all
+// panels); per panel W = V^T O and O += V (-(T W)) run on the FP64 tensor cores
+// exactly as the factorisation's trailing update does (svd.cpp:111-132 applies the
+// same reflectors one at a time).
+template <int NB>
+__global__ void __launch_bounds__(kThreads, 2) apply_q_wy_kernel(const ApplyQJob* __restrict__ jobs, uint32_t ldp) {
+  extern __shared__ __align__(16) double sm[];
+  const ApplyQJob aj = jobs[blockIdx.x];
+  const QrJob& job = aj.qr;
+  const int m = (int)job.m, K = (int)(job.m < job.n ? job.m : job.n), ncols = (int)aj.ncols;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  double* P = sm;                     // NB x ldp
+  double* sT = P + (size_t)NB * ldp;  // NB x NB, T(r, c) at r * NB + c
+  double* wt = sT + NB * NB + warp * (NB * 8);
+  double* O = aj.out;
+  const int ntiles = (ncols + kTileN - 1) / kTileN;
+  // O = [x; 0]
+  for (int tile = warp; tile < ntiles; tile += kWarps)
+    for (int cc = 0; cc < kTileN; ++cc) {
+      const int c = tile * kTileN + cc;
+      if (c >= ncols) break;
+      for (int i = lane; i < m; i += 32)
+        O[(uint64_t)c * m + i] = i < (int)aj.x_rows ? __ldcg(aj.x + (uint64_t)c * aj.x_rows + i) : 0.0;
+    }
+  __syncwarp();
+  const int npanels = (K + NB - 1) / NB;
+  for (int pi = npanels - 1; pi >= 0; --pi) {
+    const int k0 = pi * NB, nbk = min(NB, K - k0), h = m - k0;
+    __syncthreads();  // the previous panel is consumed
+    for (int q = 0; q < nbk; ++q) {
+      const double* src = job.a + (uint64_t)(k0 + q) * job.lda + k0;
+      for (int i = tid; i < h; i += kThreads) P[q * ldp + i] = __ldcg(src + i);
+    }
+    const double* tglob = job.tmat + (uint64_t)pi * NB * NB;
+    for (int t = tid; t < NB * NB; t += kThreads) sT[t] = __ldcg(tglob + t);
+    __syncthreads();
+    for (int tile = warp; tile < ntiles; tile += kWarps) {
+      const int j0 = tile * kTileN;
+      // pass 1: W = V^T O (NB x 8), k = rows k0..m-1
+      const int jb = j0 + lr;
+      const bool jb_ok = jb < ncols;
+      const double* cb = O + (uint64_t)(jb_ok ? jb : ncols - 1) * m + k0;
+      double w[(NB + 7) / 8][2];
+#pragma unroll
+      for (int hh = 0; hh < (NB + 7) / 8; ++hh) w[hh][0] = w[hh][1] = 0.0;
+      for (int i0 = 0; i0 < h; i0 += 4 * kKB) {
+        double bv[kKB];
+#pragma unroll
+        for (int u = 0; u < kKB; ++u) {
+          const int i = i0 + 4 * u + lc;
+          bv[u] = (jb_ok && i < h) ? cb[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kKB; ++u) {
+          const int i = i0 + 4 * u + lc;
+#pragma unroll
+          for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
+            const int r = hh * 8 + lr;
+            const double av = (r < nbk && i >= r && i < h) ? P[r * ldp + i] : 0.0;
+            dmma(w[hh][0], w[hh][1], av, bv[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int hh = 0; hh < (NB + 7) / 8; ++hh) {
+        const int r = hh * 8 + lr;
+        if (r < NB) {
+          wt[r * 8 + 2 * lc] = w[hh][0];
+          wt[r * 8 + 2 * lc + 1] = w[hh][1];
+        }
+      }
+      __syncwarp();
+      // W' = -(T W): T upper triangular
+      double wn[(NB * 8 + 31) / 32];
+#pragma unroll
+      for (int e = 0; e < (NB * 8 + 31) / 32; ++e) {
+        const int idx = e * 32 + lane;
+        double t = 0.0;
+        if (idx < NB * 8) {
+          const int r = idx >> 3, q = idx & 7;
+          for (int s2 = r; s2 < NB; ++s2) t += sT[r * NB + s2] * wt[s2 * 8 + q];
+        }
+        wn[e] = -t;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < (NB * 8 + 31) / 32; ++e) {
+        const int idx = e * 32 + lane;
+        if (idx < NB * 8) wt[idx] = wn[e];
+      }
+      __syncwarp();
+      // pass 2: O(8 rows x 8 cols) += V(8 x NB) W'
+      const int ja = j0 + 2 * lc;
+      double* ca0 = O + (uint64_t)min(ja, ncols - 1) * m + k0;
+      double* ca1 = O + (uint64_t)min(ja + 1, ncols - 1) * m + k0;
+      double bw[NB / 4];
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) bw[kk / 4] = wt[(kk + lc) * 8 + lr];
+      for (int i0 = 0; i0 < h; i0 += 8 * kRBq) {
+        double d0[kRBq], d1[kRBq];
+#pragma unroll
+        for (int u = 0; u < kRBq; ++u) {
+          const int i = i0 + 8 * u + lr;
+          d0[u] = (i < h && ja < ncols) ? ca0[i] : 0.0;
+          d1[u] = (i < h && ja + 1 < ncols) ? ca1[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRBq; ++u) {
+          const int i = i0 + 8 * u + lr;
+          const bool row_ok = i < h;
+#pragma unroll
+          for (int kk = 0; kk < NB; kk += 4) {
+            const int r = kk + lc;
+            const double av = (r < nbk && row_ok && i >= r) ? P[r * ldp + i] : 0.0;
+            dmma(d0[u], d1[u], av, bw[kk / 4]);
+          }
+          if (row_ok) {
+            if (ja < ncols) ca0[i] = d0[u];
+            if (ja + 1 < ncols) ca1[i] = d1[u];
+          }
+        }
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -304,6 +459,28 @@ void launch_qr(const std::vector<QrJob>& jobs, const QrJob* d_jobs, unsigned cl,
 }  // namespace
 
 uint32_t qr_max_rows() { return 24000; }
+
+static int qr_nb_for(uint32_t h_max) {
+  const size_t budget = 224 * 1024;
+  int nb = 16;
+  while (nb > 1 && (nb == 16 ? qr_smem<16>(h_max) : nb == 8 ? qr_smem<8>(h_max) : nb == 4 ? qr_smem<4>(h_max)
+                                                                                          : qr_smem<2>(h_max)) > budget)
+    nb /= 2;
+  return nb;
+}
+
+uint32_t qr_panel_nb(uint32_t h_max) { return (uint32_t)qr_nb_for(h_max); }
+
+bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t nb, cudaStream_t s) {
+  if (nb != 16 || !n_jobs) return false;  // the panel width every m <= ~1700 factors with
+  const uint32_t ldp = panel_ld(m_max);
+  const size_t smem = ((size_t)16 * ldp + 16 * 16 + kWarps * 16 * 8) * sizeof(double);
+  if (smem > 224 * 1024) return false;
+  RK_CUDA_CHECK(cudaFuncSetAttribute(apply_q_wy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  apply_q_wy_kernel<16><<<(unsigned)n_jobs, kThreads, smem, s>>>(d_jobs, ldp);
+  RK_LAUNCH_CHECK();
+  return true;
+}
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s, int sms) {
   if (jobs.empty()) return;
