@@ -2181,7 +2181,7 @@ void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s) {
     uint32_t nbw = jobs[0].wy_nb;
     for (const ApplyQJob& j : jobs)
       if (j.wy_nb != nbw || j.qr.split || !j.qr.tmat) nbw = 0;
-    if (nbw && tuning().apply_q_wy && apply_q_wy_batched(dj.get(), jobs.size(), mmax, nbw, s)) return;
+    if (nbw && tuning().apply_q_wy && apply_q_wy_batched(dj.get(), jobs.size(), mmax, cmax, nbw, s)) return;
   }
   constexpr int kCW = 4;
   auto panel = [&](auto kern, int cw, int e) {

@@ -480,7 +480,8 @@ struct ApplyQJob {    // out (qr.m x ncols col-major, ld qr.m) = Q [x; 0], x x_r
 };
 // rk_qr.cu: the panel width qr_batched factors an h_max-row batch with; apply_q through the T factors
 uint32_t qr_panel_nb(uint32_t h_max);
-bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t nb, cudaStream_t s);
+bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t c_max, uint32_t nb,
+                        cudaStream_t s);
 void apply_q_batched(const std::vector<ApplyQJob>& jobs, cudaStream_t s);
 
 // rk_spmm.cu -- V = A^T U Sigma^-1 over the CSC

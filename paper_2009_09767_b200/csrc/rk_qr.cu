@@ -314,6 +314,7 @@ template <int NB>
 __global__ void __launch_bounds__(kThreads, 2) apply_q_wy_kernel(const ApplyQJob* __restrict__ jobs, uint32_t ldp) {
   extern __shared__ __align__(16) double sm[];
   const ApplyQJob aj = jobs[blockIdx.x];
+  const int wslot = blockIdx.y * kWarps + (threadIdx.x >> 5), wstride = gridDim.y * kWarps;  // tiles over the job's CTAs
   const QrJob& job = aj.qr;
   const int m = (int)job.m, K = (int)(job.m < job.n ? job.m : job.n), ncols = (int)aj.ncols;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 2) apply_q_wy_kernel(const ApplyQJob
   double* O = aj.out;
   const int ntiles = (ncols + kTileN - 1) / kTileN;
   // O = [x; 0]
-  for (int tile = warp; tile < ntiles; tile += kWarps)
+  for (int tile = wslot; tile < ntiles; tile += wstride)
     for (int cc = 0; cc < kTileN; ++cc) {
       const int c = tile * kTileN + cc;
       if (c >= ncols) break;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2) apply_q_wy_kernel(const ApplyQJob
     const double* tglob = job.tmat + (uint64_t)pi * NB * NB;
     for (int t = tid; t < NB * NB; t += kThreads) sT[t] = __ldcg(tglob + t);
     __syncthreads();
-    for (int tile = warp; tile < ntiles; tile += kWarps) {
+    for (int tile = wslot; tile < ntiles; tile += wstride) {
       const int j0 = tile * kTileN;
       // pass 1: W = V^T O (NB x 8), k = rows k0..m-1
       const int jb = j0 + lr;
@@ -471,13 +472,16 @@ static int qr_nb_for(uint32_t h_max) {
 
 uint32_t qr_panel_nb(uint32_t h_max) { return (uint32_t)qr_nb_for(h_max); }
 
-bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t nb, cudaStream_t s) {
+bool apply_q_wy_batched(const ApplyQJob* d_jobs, size_t n_jobs, uint32_t m_max, uint32_t c_max, uint32_t nb,
+                        cudaStream_t s) {
   if (nb != 16 || !n_jobs) return false;  // the panel width every m <= ~1700 factors with
   const uint32_t ldp = panel_ld(m_max);
   const size_t smem = ((size_t)16 * ldp + 16 * 16 + kWarps * 16 * 8) * sizeof(double);
   if (smem > 224 * 1024) return false;
   RK_CUDA_CHECK(cudaFuncSetAttribute(apply_q_wy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  apply_q_wy_kernel<16><<<(unsigned)n_jobs, kThreads, smem, s>>>(d_jobs, ldp);
+  // a warp per 8-column tile: enough CTAs per job that no warp takes a second tile
+  const unsigned gy = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(8, ceil_div(ceil_div(c_max, kTileN), kWarps)));
+  apply_q_wy_kernel<16><<<dim3((unsigned)n_jobs, gy), kThreads, smem, s>>>(d_jobs, ldp);
   RK_LAUNCH_CHECK();
   return true;
 }
