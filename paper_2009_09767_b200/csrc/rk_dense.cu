@@ -1465,6 +1465,323 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(Smem
 }
 
 // ===========================================================================
+// Wide pair blocks (matrices too large for shared memory: c4's 1024^2, c5's 2048^2)
+// ===========================================================================
+// The 16-column warp steps above move 3 x 16 columns through L2/HBM for every
+// 0.9 flop per byte: at 1024+ rows the batch streams from HBM and the kernel is
+// bandwidth-bound. Here a CTA owns a pair of 32-column groups for one tournament
+// step (one launch per step; the kernel boundary is the step's barrier):
+//   1. H = X^T X (64 x 64, X = the pair's 64 columns) on the FP64 tensor cores: every
+//      warp takes a slab of rows and the 36 upper 8 x 8 tiles (8 loads feed 36 DMMAs
+//      per 4 rows), the slabs are added in warp order in shared memory;
+//   2. the inner solve on H in shared memory: the 64 columns are 8 sub-groups of 8;
+//      four warps run the sub-group pairs of an inner step (cross pairs A x B only,
+//      all pairs in tournament step 0) with the 16-column rounds (step_rounds), then
+//      H <- Z~^T H Z~ and Z <- Z Z~ by DMMA (columns, barrier, rows);
+//   3. X <- X Z (Z 64 x 64) by DMMA, 128 DMMAs per 16 loads.
+// 11 flop per byte of L2/HBM traffic instead of 0.9. Every cross pair of columns is
+// rotated once per sweep, as in the narrower kernels; convergence is measured on the
+// sub-blocks as they enter their rounds, and jacobi_cluster_kernel certifies on W.
+constexpr int kWide = 64, kWideS = 65, kWideG = 32;  // pair-block columns, smem stride, columns per group
+
+struct WideParams {
+  const JacobiJob* jobs;
+  uint32_t G;     // groups of kWideG columns (even)
+  uint32_t step;  // tournament step
+};
+
+// per-job scratch in stats: [4] rotations of the sweep, [5] max ratio^2 bits, [6] alpha_max bits, [7] done
+__global__ void __launch_bounds__(256) wide_sweep_begin(const JacobiJob* jobs) {
+  const JacobiJob job = jobs[blockIdx.x];
+  if (job.stats[7]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double red[8];
+  double amax = 0.0;
+  for (uint32_t j = warp; j < job.cols_pad; j += 8) {
+    const double* wj = job.w + (uint64_t)j * job.rows;
+    double a = 0.0;
+    for (uint32_t i = lane; i < job.rows; i += 32) {
+      const double x = __ldcg(wj + i);
+      a += x * x;
+    }
+    amax = fmax(amax, warp_sum(a));
+  }
+  if (lane == 0) red[warp] = amax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < 8; ++i) amax = fmax(amax, red[i]);
+    job.stats[4] = 0ull;
+    job.stats[5] = 0ull;
+    job.stats[6] = (uint64_t)__double_as_longlong(amax);
+  }
+}
+
+__global__ void wide_sweep_end(const JacobiJob* jobs, uint32_t njobs, double stop_ratio, int max_sweeps,
+                               uint32_t* active) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= njobs) return;
+  const JacobiJob job = jobs[q];
+  if (job.stats[7]) return;
+  const unsigned long long rot = job.stats[4];
+  const double ratio = sqrt(__longlong_as_double((long long)job.stats[5]));
+  job.stats[0] += 1ull;
+  job.stats[1] += rot;
+  job.stats[3] = (uint64_t)__double_as_longlong(ratio);
+  if (rot == 0 || ratio < stop_ratio || (int)job.stats[0] >= max_sweeps) job.stats[7] = 1ull;
+  else atomicAdd(active, 1u);
+}
+
+__global__ void wide_finish(const JacobiJob* jobs, uint32_t njobs) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= njobs) return;
+  const JacobiJob job = jobs[q];
+  job.stats[2] = 0ull;
+  job.stats[4] = job.stats[5] = job.stats[6] = job.stats[7] = 0ull;
+}
+
+// C (64 x 16 columns col_of(0..15) of S, stride kWideS) <- C Z16 (Z16 16 x 16 row-major, stride kWN)
+template <typename F>
+__device__ __forceinline__ void wide_cols_update(double* S, F col_of, const double* sZ) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double bf[4][2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) bf[kc][nt] = sZ[(4 * kc + lc) * kWN + 8 * nt + lr];
+  int cin[4], cout[2][2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) cin[kc] = col_of(4 * kc + lc);
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) cout[nt][e] = col_of(8 * nt + 2 * lc + e);
+#pragma unroll
+  for (int rt = 0; rt < kWide / 8; ++rt) {
+    const int r = 8 * rt + lr;
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = S[r * kWideS + cin[kc]];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) dmma884(d0, d1, a[kc], bf[kc][nt]);
+      S[r * kWideS + cout[nt][0]] = d0;
+      S[r * kWideS + cout[nt][1]] = d1;
+    }
+    __syncwarp();  // the tile's reads precede its writes for every lane (a fragment spans the 16 columns)
+  }
+}
+
+// R (16 rows row_of(0..15) x 64 of S) <- Z16^T R
+template <typename F>
+__device__ __forceinline__ void wide_rows_update(double* S, F row_of, const double* sZ) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double af[2][4];  // A = Z16^T: A[8 mt + lr][4 kc + lc] = Z16[4 kc + lc][8 mt + lr]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) af[mt][kc] = sZ[(4 * kc + lc) * kWN + 8 * mt + lr];
+  int rin[4], rout[2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc) rin[kc] = row_of(4 * kc + lc);
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) rout[mt] = row_of(8 * mt + lr);
+#pragma unroll
+  for (int nt = 0; nt < kWide / 8; ++nt) {
+    double b[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) b[kc] = S[rin[kc] * kWideS + 8 * nt + lr];
+    double d[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      d[mt][0] = d[mt][1] = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) dmma884(d[mt][0], d[mt][1], af[mt][kc], b[kc]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      S[rout[mt] * kWideS + 8 * nt + 2 * lc] = d[mt][0];
+      S[rout[mt] * kWideS + 8 * nt + 2 * lc + 1] = d[mt][1];
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) {
+  extern __shared__ __align__(16) double wsm[];
+  const JacobiJob job = P.jobs[blockIdx.y];
+  if (job.stats[7]) return;  // converged in an earlier sweep
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lc = lane & 3;
+  const uint32_t rows = job.rows, G = P.G, step = P.step, pw = blockIdx.x;
+  double* H = wsm;                       // 64 x 65
+  double* Z = H + kWide * kWideS;        // 64 x 65
+  double* sHall = Z + kWide * kWideS;    // 4 x kSH (the inner solve's warps)
+  __shared__ int s_any;
+  __shared__ double s_red[8];
+  __shared__ unsigned s_rot;
+  const uint32_t gA = rr_slot(pw, step, G), gB = rr_slot(G - 1 - pw, step, G);
+  double* XA = job.w + (uint64_t)gA * kWideG * rows;
+  double* XB = job.w + (uint64_t)gB * kWideG * rows;
+  auto col_ptr = [&](int t) -> double* { return (t < kWideG ? XA + (uint64_t)t * rows : XB + (uint64_t)(t - kWideG) * rows); };
+  const double freeze = kJacobiTol * kJacobiTol * __longlong_as_double((long long)job.stats[6]);
+  if (tid == 0) {
+    s_any = 0;
+    s_rot = 0u;
+  }
+  for (int t = tid; t < kWide * kWideS; t += 256) Z[t] = ((t / kWideS) == (t % kWideS)) ? 1.0 : 0.0;
+
+  // ---- 1. H = X^T X: this warp's slab of rows, the 36 upper tiles ----
+  {
+    double acc[36][2];
+#pragma unroll
+    for (int i = 0; i < 36; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const uint32_t slab = rows / 8, r_lo = warp * slab;
+    const double* src[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) src[t] = col_ptr(8 * t + lr) + r_lo + lc;
+    for (uint32_t k0 = 0; k0 < slab; k0 += 8) {
+      double a[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[u][t] = __ldcg(src[t] + k0 + 4 * u);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        int idx = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = i; j < 8; ++j) {
+            dmma884(acc[idx][0], acc[idx][1], a[u][i], a[u][j]);
+            ++idx;
+          }
+      }
+    }
+    // the slabs summed in warp order (deterministic), mirrored below the diagonal
+    for (int w = 0; w < 8; ++w) {
+      if (warp == w) {
+        int idx = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = i; j < 8; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = 8 * i + lr, c = 8 * j + 2 * lc + e;
+              const double v = (w == 0 ? 0.0 : H[r * kWideS + c]) + acc[idx][e];
+              H[r * kWideS + c] = v;
+            }
+            ++idx;
+          }
+      }
+      __syncthreads();
+    }
+    // mirror: (c, r) = (r, c) for tiles above the diagonal
+    for (int t = tid; t < kWide * kWide; t += 256) {
+      const int r = t / kWide, c = t % kWide;
+      if ((r >> 3) > (c >> 3)) H[r * kWideS + c] = H[c * kWideS + r];
+    }
+    __syncthreads();
+  }
+
+  // ---- 2. the inner solve: sub-groups 0..3 = group A, 4..7 = group B ----
+  uint32_t nrot = 0;
+  double best_g2 = 0.0, best_prod = 1.0;
+  const int n_inner = step == 0 ? 7 : 4;
+  for (int it = 0; it < n_inner; ++it) {
+    bool need = false;
+    int sa = 0, sb = 0;
+    double* sH = sHall + (warp & 3) * kSH;
+    if (warp < 4) {
+      if (step == 0) {
+        sa = (int)rr_slot((uint32_t)warp, (uint32_t)it, 8u);
+        sb = (int)rr_slot((uint32_t)(7 - warp), (uint32_t)it, 8u);
+      } else {
+        sa = warp;
+        sb = 4 + ((warp + it) & 3);
+      }
+      // the pair's 16 x 16 block of H
+      for (int t = lane; t < kWN * kWN; t += 32) {
+        const int r = t >> 4, c = t & 15;
+        const int mr = r < 8 ? 8 * sa + r : 8 * sb + r - 8, mc = c < 8 ? 8 * sa + c : 8 * sb + c - 8;
+        sH[r * kWS + c] = H[mr * kWideS + mc];
+      }
+      __syncwarp();
+      const bool intra = step == 0 && it == 0;
+      need = fresh_scan(sH, freeze, intra, best_g2, best_prod);
+      if (need) {
+        step_rounds(sH, intra, freeze, nrot);
+        auto idx_of = [&](int t) { return t < 8 ? 8 * sa + t : 8 * sb + t - 8; };
+        wide_cols_update(H, idx_of, sH);
+        wide_cols_update(Z, idx_of, sH);
+        if (lane == 0) s_any = 1;
+      }
+    }
+    __syncthreads();
+    if (warp < 4 && need) {
+      auto idx_of = [&](int t) { return t < 8 ? 8 * sa + t : 8 * sb + t - 8; };
+      wide_rows_update(H, idx_of, sH);
+    }
+    __syncthreads();
+  }
+  // the step's statistics
+  {
+    unsigned r32 = nrot;
+    double r2 = best_g2 / best_prod;
+    for (int o = 16; o; o >>= 1) {
+      r32 += __shfl_xor_sync(0xffffffffu, r32, o);
+      r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+    }
+    if (lane == 0) {
+      s_red[warp] = r2;
+      if (r32) atomicAdd(&s_rot, r32);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < 4; ++i) t = fmax(t, s_red[i]);
+      if (s_rot) atomicAdd(reinterpret_cast<unsigned long long*>(job.stats + 4), (unsigned long long)s_rot);
+      atomicMax(reinterpret_cast<unsigned long long*>(job.stats + 5), (unsigned long long)__double_as_longlong(t));
+    }
+  }
+  if (!s_any) return;  // nothing rotated: Z = I
+
+  // ---- 3. X <- X Z: this warp's slab, 16 rows at a time ----
+  {
+    const uint32_t slab = rows / 8, r_lo = warp * slab;
+    const double* src[16];
+#pragma unroll
+    for (int kc = 0; kc < 16; ++kc) src[kc] = col_ptr(4 * kc + lc) + r_lo + lr;
+    for (uint32_t r0 = 0; r0 < slab; r0 += 16) {
+      double a[2][16];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int kc = 0; kc < 16; ++kc) a[u][kc] = __ldcg(src[kc] + r0 + 8 * u);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int kc = 0; kc < 16; ++kc) {
+          const double b = Z[(4 * kc + lc) * kWideS + 8 * nt + lr];
+          dmma884(d[0][0], d[0][1], a[0][kc], b);
+          dmma884(d[1][0], d[1][1], a[1][kc], b);
+        }
+        double* o0 = col_ptr(8 * nt + 2 * lc) + r_lo + r0 + lr;
+        double* o1 = col_ptr(8 * nt + 2 * lc + 1) + r_lo + r0 + lr;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          o0[8 * u] = d[u][0];
+          o1[8 * u] = d[u][1];
+        }
+      }
+    }
+  }
+}
+
+// ===========================================================================
 // finalize
 // ===========================================================================
 
@@ -1921,6 +2238,38 @@ static bool jacobi_smem_batched(const std::vector<JacobiJob>& jobs, const Jacobi
   return true;
 }
 
+// The wide pair-block kernel over a homogeneous batch (one launch per tournament
+// step; the host reads the number of unconverged jobs once per sweep).
+static bool jacobi_wide_batched(const std::vector<JacobiJob>& jobs, const JacobiJob* d_jobs, cudaStream_t s,
+                                double stop_ratio) {
+  const uint32_t rows = jobs[0].rows, cols_pad = jobs[0].cols_pad;
+  if (rows % 128 != 0 || cols_pad % (2 * kWideG) != 0 || cols_pad < 4 * kWideG) return false;
+  const uint32_t G = cols_pad / kWideG, njobs = (uint32_t)jobs.size();
+  const size_t smem = ((size_t)2 * kWide * kWideS + 4 * kSH) * sizeof(double);
+  RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_wide_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DBuf<uint32_t> active(1, s);
+  constexpr int kWideMaxSweeps = 30;
+  for (int sweep = 0; sweep < kWideMaxSweeps; ++sweep) {
+    wide_sweep_begin<<<njobs, 256, 0, s>>>(d_jobs);
+    RK_LAUNCH_CHECK();
+    for (uint32_t step = 0; step + 1 < G; ++step) {
+      WideParams P{d_jobs, G, step};
+      jacobi_wide_step_kernel<<<dim3(G / 2, njobs), 256, smem, s>>>(P);
+      RK_LAUNCH_CHECK();
+    }
+    active.zero();
+    wide_sweep_end<<<(unsigned)ceil_div(njobs, 256), 256, 0, s>>>(d_jobs, njobs, stop_ratio, kWideMaxSweeps, active.get());
+    RK_LAUNCH_CHECK();
+    std::vector<uint32_t> h;
+    to_host(h, active.get(), 1, s);
+    sync(s);
+    if (h[0] == 0) break;
+  }
+  wide_finish<<<(unsigned)ceil_div(njobs, 256), 256, 0, s>>>(d_jobs, njobs);
+  RK_LAUNCH_CHECK();
+  return true;
+}
+
 bool jacobi_smem_try(std::vector<JacobiJob>& jobs, cudaStream_t s, size_t smem_optin, const SideStream* side) {
   const Tuning& tn = tuning();
   if (jobs.empty() || tn.jacobi_smem == 0) return false;
@@ -1982,7 +2331,15 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   for (const JacobiJob& j : jobs) all_pre = all_pre && j.pre;
   bool use_smem = all_pre || (!latency && jacobi_smem_try(jobs, s, smem_optin, nullptr));
   if (use_smem) use_warp = false;
-  if (use_warp) {
+  // large matrices: the wide pair-block kernel (RK_JACOBI_WIDE=0: the 16-column warp kernel)
+  bool use_wide = false;
+  if ((use_warp || (latency && tn.jacobi_warp != 0)) && !use_smem && !with_v && tn.jacobi_wide && rows >= 1024) {
+    DBuf<JacobiJob> djw(jobs.size(), s);
+    to_device(djw.get(), jobs.data(), jobs.size(), s);
+    use_wide = jacobi_wide_batched(jobs, djw.get(), s, tn.jacobi_check >= 0 ? tn.jacobi_check : 1e-7);
+  }
+  if (use_wide) use_warp = true;  // the direct kernel starts with the certifying check
+  else if (use_warp) {
     WarpParams WP{nullptr, cols_pad / kWG, tn.jacobi_check >= 0 ? tn.jacobi_check : 1e-7};
     DBuf<JacobiJob> djw(jobs.size(), s);
     to_device(djw.get(), jobs.data(), jobs.size(), s);

@@ -52,6 +52,7 @@ struct Tuning {
   int jacobi_warp = -1;           // RK_JACOBI_WARP=0/1 (-1: by shape)
   int jacobi_smem = -1;           // RK_JACOBI_SMEM=0/1: the shared-memory-resident Gram-assisted kernel (-1: batched blocks)
   int jacobi_smem_cl = 2;         // RK_JACOBI_SMEM_CL: its largest cluster (1, 2, 4, 8)
+  bool jacobi_wide = true;        // RK_JACOBI_WIDE=0: no wide pair-block kernel for >= 1024-row matrices
   double jacobi_check = -1.0;     // RK_JACOBI_CHECK: tail-check ratio (<0: by workload; 0 off)
   int jacobi_cluster = 0;         // RK_JACOBI_CLUSTER: cluster size override (0: planned)
   bool jacobi_debug = false;      // RK_JACOBI_DEBUG=1
@@ -65,6 +66,7 @@ struct Tuning {
   float precond_stop = 1e-5f;     // RK_PRECOND_STOP
   bool spmm_warp = false;         // RK_SPMM_WARP=1: warp-per-column V SpMM
   bool wide_reduce = true;        // RK_WIDE_REDUCE=0: wide blocks' Jacobi on X = T^T, not on its R
+  bool presence_csr = false;      // RK_PRESENCE=csr: the rank check's flags by a thread per CSR entry (row search)
   bool repair_speculate = true;   // RK_REPAIR_SPECULATE=0: the neighbor replay without speculated sets
   bool wide_rows_pow2 = true;     // RK_WIDE_ROWS=32: the reduced R's rows padded to multiples of 32
   bool eig_merge = true;          // RK_EIG_MERGE=0: the merge's Gram route by Cholesky + one-sided Jacobi

@@ -47,6 +47,32 @@ __global__ void presence_flat_kernel(const uint64_t* __restrict__ row_ptr, const
   }
 }
 
+// The same flags from the CSC: block d's entries are one contiguous slice of the
+// column-ordered entries, so a CTA streams the slice's row indices (4 bytes per
+// entry, coalesced, the only HBM traffic) and sets presence[d * rows + row] -- no
+// search, same-value races only. grid = (slices of a block, blocks).
+__global__ void __launch_bounds__(256) presence_csc_kernel(const uint64_t* __restrict__ col_ptr,
+                                                           const uint32_t* __restrict__ row_idx, uint64_t rows,
+                                                           Partition p, uint32_t* __restrict__ presence) {
+  for (uint64_t d = blockIdx.y; d < p.blocks; d += gridDim.y) {
+    const uint64_t e0 = col_ptr[p.begin(d)], e1 = col_ptr[p.end(d)];
+    uint32_t* f = presence + d * rows;
+    // 4 entries per thread and step (one 16-byte load where aligned)
+    for (uint64_t e = e0 + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < e1;
+         e += (uint64_t)gridDim.x * blockDim.x * 4) {
+      if (e + 4 <= e1 && (e & 3) == 0) {
+        const uint4 r = __ldcs(reinterpret_cast<const uint4*>(row_idx + e));
+        f[r.x] = 1u;
+        f[r.y] = 1u;
+        f[r.z] = 1u;
+        f[r.w] = 1u;
+      } else {
+        for (uint64_t k = e; k < e + 4 && k < e1; ++k) f[__ldcs(row_idx + k)] = 1u;
+      }
+    }
+  }
+}
+
 __global__ void invert_flags(uint32_t* f, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -429,6 +455,22 @@ __global__ void rng_eval(uint64_t n, uint64_t seed, const uint64_t* block, const
 
 }  // namespace
 
+
+// the rank check's presence flags (repair.cpp:42-50): from the CSC slices
+// (RK_PRESENCE=csr: one thread per CSR entry with a row search)
+static void presence_launch(const DevMatrix& a, const Partition& p, uint32_t* flag, cudaStream_t s) {
+  if (tuning().presence_csr) {
+    presence_flat_kernel<<<grid_for(a.csr.nnz), kT, 0, s>>>(a.csr.ptr.get(), a.csr.idx.get(), a.csr.rows, a.csr.nnz, p,
+                                                             flag);
+  } else {
+    const uint64_t per_block = ceil_div(a.csc.nnz, p.blocks);
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(64, ceil_div(per_block, 256 * 4 * 4)));
+    const unsigned gy = (unsigned)std::min<uint64_t>(p.blocks, 65535);
+    presence_csc_kernel<<<dim3(gx, gy), 256, 0, s>>>(a.csc.ptr.get(), a.csc.idx.get(), a.csr.rows, p, flag);
+  }
+  RK_LAUNCH_CHECK();
+}
+
 void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uint64_t seed, RepairOut& out,
                    cudaStream_t s) {
   const uint64_t rows = a.csr.rows, D = p.blocks;
@@ -443,9 +485,7 @@ void repair_device(const DevMatrix& a, const Partition& p, rk_method method, uin
   DBuf<uint32_t> flag(n_flags ? n_flags : 1, s);
   flag.zero();
   if (a.csr.nnz) {
-    presence_flat_kernel<<<grid_for(a.csr.nnz), kT, 0, s>>>(a.csr.ptr.get(), a.csr.idx.get(), rows, a.csr.nnz, p,
-                                                             flag.get());
-    RK_LAUNCH_CHECK();
+    presence_launch(a, p, flag.get(), s);
   }
   invert_flags<<<grid_for(n_flags), kT, 0, s>>>(flag.get(), n_flags);
   RK_LAUNCH_CHECK();
