@@ -432,8 +432,14 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   if (fr.records_host && fr.blocks.payload.n) {
     RK_CUDA_CHECK(cudaEventRecord(c.copy_ev[0], s));
     RK_CUDA_CHECK(cudaStreamWaitEvent(c.copy, c.copy_ev[0], 0));
-    RK_CUDA_CHECK(cudaMemcpyAsync(fr.records_host, fr.blocks.payload.get(), fr.blocks.payload.n * sizeof(double),
-                                  cudaMemcpyDeviceToHost, c.copy));
+    // in 32 MiB pieces: the merge's small result reads (effective columns, the kappa
+    // guard, the bisection bounds) share the D2H engine and would otherwise queue
+    // behind the whole 1 GiB transfer (c3: the SYRK segment waited 32 ms)
+    const uint64_t total = fr.blocks.payload.n * sizeof(double), piece = 32ull << 20;
+    for (uint64_t off = 0; off < total; off += piece)
+      RK_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(fr.records_host) + off,
+                                    reinterpret_cast<const char*>(fr.blocks.payload.get()) + off,
+                                    std::min(piece, total - off), cudaMemcpyDeviceToHost, c.copy));
     RK_CUDA_CHECK(cudaEventRecord(c.copy_ev[1], c.copy));
   }
   {

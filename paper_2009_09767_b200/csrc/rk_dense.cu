@@ -1609,7 +1609,7 @@ __device__ __forceinline__ void wide_rows_update(double* S, F row_of, const doub
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) {
+__global__ void __launch_bounds__(256, 2) jacobi_wide_step_kernel(WideParams P) {
   extern __shared__ __align__(16) double wsm[];
   const JacobiJob job = P.jobs[blockIdx.y];
   if (job.stats[7]) return;  // converged in an earlier sweep
@@ -1624,7 +1624,6 @@ __global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) 
   const uint32_t gA = rr_slot(pw, step, G), gB = rr_slot(G - 1 - pw, step, G);
   double* XA = job.w + (uint64_t)gA * kWideG * rows;
   double* XB = job.w + (uint64_t)gB * kWideG * rows;
-  auto col_ptr = [&](int t) -> double* { return (t < kWideG ? XA + (uint64_t)t * rows : XB + (uint64_t)(t - kWideG) * rows); };
   const double freeze = kJacobiTol * kJacobiTol * __longlong_as_double((long long)job.stats[6]);
   if (tid == 0) {
     s_any = 0;
@@ -1632,58 +1631,102 @@ __global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) 
   }
   for (int t = tid; t < kWide * kWideS; t += 256) Z[t] = ((t / kWideS) == (t % kWideS)) ? 1.0 : 0.0;
 
-  // ---- 1. H = X^T X: this warp's slab of rows, the 36 upper tiles ----
+  // ---- 1. H = X^T X. The 36 upper 8 x 8 tiles in four sets -- the two diagonal 4 x 4
+  // super-blocks (10 tiles each, 4 column tiles to load) and the two halves of the
+  // off-diagonal one (8 tiles, 6 column tiles) -- times two halves of the rows: a
+  // warp holds 10 accumulator tiles (not 36), so two CTAs share an SM ----
   {
-    double acc[36][2];
+    const int ts = warp & 3, rh = warp >> 2;
+    const uint32_t slab = rows / 2, r_lo = rh * slab;
+    auto tile_ptr = [&](int t) -> const double* {  // column 8 t + lr of the pair block
+      return (t < 4 ? XA : XB) + (uint64_t)(8 * (t & 3) + lr) * rows + r_lo + lc;
+    };
+    auto put = [&](int i, int j, const double (&acc)[2]) {  // tile (i, j) and its mirror
 #pragma unroll
-    for (int i = 0; i < 36; ++i) acc[i][0] = acc[i][1] = 0.0;
-    const uint32_t slab = rows / 8, r_lo = warp * slab;
-    const double* src[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) src[t] = col_ptr(8 * t + lr) + r_lo + lc;
-    for (uint32_t k0 = 0; k0 < slab; k0 += 8) {
-      double a[2][8];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) a[u][t] = __ldcg(src[t] + k0 + 4 * u);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        int idx = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = i; j < 8; ++j) {
-            dmma884(acc[idx][0], acc[idx][1], a[u][i], a[u][j]);
-            ++idx;
-          }
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * i + lr, c = 8 * j + 2 * lc + e;
+        const double v = (rh == 0 ? 0.0 : H[r * kWideS + c]) + acc[e];
+        H[r * kWideS + c] = v;
+        if (i != j) H[c * kWideS + r] = v;
       }
-    }
-    // the slabs summed in warp order (deterministic), mirrored below the diagonal
-    for (int w = 0; w < 8; ++w) {
-      if (warp == w) {
-        int idx = 0;
+    };
+    constexpr int kKBw = 4;  // k-steps whose loads are in flight together
+    if (ts == 0 || ts == 3) {
+      const int base = ts == 0 ? 0 : 4;
+      const double* src[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+      for (int t = 0; t < 4; ++t) src[t] = tile_ptr(base + t);
+      double acc[10][2];
 #pragma unroll
-          for (int j = i; j < 8; ++j) {
+      for (int i = 0; i < 10; ++i) acc[i][0] = acc[i][1] = 0.0;
+      for (uint32_t k0 = 0; k0 < slab; k0 += 4 * kKBw) {
+        double a[kKBw][4];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = 8 * i + lr, c = 8 * j + 2 * lc + e;
-              const double v = (w == 0 ? 0.0 : H[r * kWideS + c]) + acc[idx][e];
-              H[r * kWideS + c] = v;
+        for (int u = 0; u < kKBw; ++u)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) a[u][t] = __ldcg(src[t] + k0 + 4 * u);
+#pragma unroll
+        for (int u = 0; u < kKBw; ++u) {
+          int idx = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i; j < 4; ++j) {
+              dmma884(acc[idx][0], acc[idx][1], a[u][i], a[u][j]);
+              ++idx;
             }
-            ++idx;
-          }
+        }
       }
-      __syncthreads();
+      for (int turn = 0; turn < 2; ++turn) {  // the row halves summed in order
+        if (rh == turn) {
+          int idx = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = i; j < 4; ++j) {
+              put(base + i, base + j, acc[idx]);
+              ++idx;
+            }
+        }
+        __syncthreads();
+      }
+    } else {
+      const int r0 = ts == 1 ? 0 : 2;
+      const double* srcR[2];
+      const double* srcC[4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) srcR[t] = tile_ptr(r0 + t);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) srcC[t] = tile_ptr(4 + t);
+      double acc[8][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+      for (uint32_t k0 = 0; k0 < slab; k0 += 4 * kKBw) {
+        double ar[kKBw][2], ac[kKBw][4];
+#pragma unroll
+        for (int u = 0; u < kKBw; ++u) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) ar[u][t] = __ldcg(srcR[t] + k0 + 4 * u);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) ac[u][t] = __ldcg(srcC[t] + k0 + 4 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kKBw; ++u)
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[4 * i + j][0], acc[4 * i + j][1], ar[u][i], ac[u][j]);
+      }
+      for (int turn = 0; turn < 2; ++turn) {
+        if (rh == turn) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) put(r0 + i, 4 + j, acc[4 * i + j]);
+        }
+        __syncthreads();
+      }
     }
-    // mirror: (c, r) = (r, c) for tiles above the diagonal
-    for (int t = tid; t < kWide * kWide; t += 256) {
-      const int r = t / kWide, c = t % kWide;
-      if ((r >> 3) > (c >> 3)) H[r * kWideS + c] = H[c * kWideS + r];
-    }
-    __syncthreads();
   }
 
   // ---- 2. the inner solve: sub-groups 0..3 = group A, 4..7 = group B ----
@@ -1751,15 +1794,15 @@ __global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) 
   // ---- 3. X <- X Z: this warp's slab, 16 rows at a time ----
   {
     const uint32_t slab = rows / 8, r_lo = warp * slab;
-    const double* src[16];
-#pragma unroll
-    for (int kc = 0; kc < 16; ++kc) src[kc] = col_ptr(4 * kc + lc) + r_lo + lr;
+    const uint64_t cs4 = (uint64_t)4 * rows;  // four columns on
+    const double* inA = XA + (uint64_t)lc * rows + r_lo + lr;  // column 4 kc + lc, kc < 8: group A
+    const double* inB = XB + (uint64_t)lc * rows + r_lo + lr;
     for (uint32_t r0 = 0; r0 < slab; r0 += 16) {
       double a[2][16];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int kc = 0; kc < 16; ++kc) a[u][kc] = __ldcg(src[kc] + r0 + 8 * u);
+        for (int kc = 0; kc < 16; ++kc) a[u][kc] = __ldcg((kc < 8 ? inA : inB) + (uint64_t)(kc & 7) * cs4 + r0 + 8 * u);
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -1769,8 +1812,8 @@ __global__ void __launch_bounds__(256, 1) jacobi_wide_step_kernel(WideParams P) 
           dmma884(d[0][0], d[0][1], a[0][kc], b);
           dmma884(d[1][0], d[1][1], a[1][kc], b);
         }
-        double* o0 = col_ptr(8 * nt + 2 * lc) + r_lo + r0 + lr;
-        double* o1 = col_ptr(8 * nt + 2 * lc + 1) + r_lo + r0 + lr;
+        double* o0 = (nt < 4 ? XA : XB) + (uint64_t)(8 * (nt & 3) + 2 * lc) * rows + r_lo + r0 + lr;
+        double* o1 = o0 + rows;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           o0[8 * u] = d[u][0];
@@ -2243,7 +2286,7 @@ static bool jacobi_smem_batched(const std::vector<JacobiJob>& jobs, const Jacobi
 static bool jacobi_wide_batched(const std::vector<JacobiJob>& jobs, const JacobiJob* d_jobs, cudaStream_t s,
                                 double stop_ratio) {
   const uint32_t rows = jobs[0].rows, cols_pad = jobs[0].cols_pad;
-  if (rows % 128 != 0 || cols_pad % (2 * kWideG) != 0 || cols_pad < 4 * kWideG) return false;
+  if (rows % 128 != 0 || cols_pad % (2 * kWideG) != 0 || cols_pad < 4 * kWideG) return false;  // slabs of 16-row batches
   const uint32_t G = cols_pad / kWideG, njobs = (uint32_t)jobs.size();
   const size_t smem = ((size_t)2 * kWide * kWideS + 4 * kSH) * sizeof(double);
   RK_CUDA_CHECK(cudaFuncSetAttribute(jacobi_wide_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
