@@ -2331,6 +2331,19 @@ bool jacobi_smem_try(std::vector<JacobiJob>& jobs, cudaStream_t s, size_t smem_o
   return true;
 }
 
+bool jacobi_smem_fits(const JacobiJob& j, size_t smem_optin) {
+  if (j.v || tuning().jacobi_smem == 0) return false;
+  const uint32_t colsU = (j.cols + 15u) & ~15u, G = colsU / kWG, npairs = G / 2;
+  const uint32_t rows = (std::min(j.rows, j.rows_nz ? j.rows_nz : j.rows) + 7u) & ~7u;
+  const uint32_t cl_max = (uint32_t)std::max(1, std::min(8, tuning().jacobi_smem_cl));
+  for (uint32_t cl = 1; cl <= cl_max; cl *= 2) {
+    const uint32_t Gc = (uint32_t)ceil_div(G, cl), nw = (uint32_t)ceil_div(npairs, cl);
+    const size_t bytes = ((size_t)Gc * kWG * (rows + 4) + (size_t)nw * kSH + kSmemMisc) * sizeof(double);
+    if (nw <= (uint32_t)kSmemMaxWarps && bytes <= smem_optin) return true;
+  }
+  return false;
+}
+
 void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_t smem_optin, bool latency) {
   if (jobs.empty()) return;
   // jobs in one launch share rows / cols_pad / with_v (the caller groups them);
@@ -2370,8 +2383,18 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
   // matrices that fit shared memory: the resident Gram-assisted kernel first (any
   // conditioning: it measures convergence on fresh Grams and the direct kernel
   // certifies) -- here, or already run by the caller over a larger batch (pre)
-  bool all_pre = true;
-  for (const JacobiJob& j : jobs) all_pre = all_pre && j.pre;
+  bool all_pre = true, any_pre = false;
+  for (const JacobiJob& j : jobs) {
+    all_pre = all_pre && j.pre;
+    any_pre = any_pre || j.pre;
+  }
+  if (any_pre && !all_pre) {  // the caller's shared-memory pass took only the jobs that fit: finish the two sets apart
+    std::vector<JacobiJob> done, rest;
+    for (const JacobiJob& j : jobs) (j.pre ? done : rest).push_back(j);
+    jacobi_batched(done, s, sms, smem_optin, latency);
+    jacobi_batched(rest, s, sms, smem_optin, latency);
+    return;
+  }
   bool use_smem = all_pre || (!latency && jacobi_smem_try(jobs, s, smem_optin, nullptr));
   if (use_smem) use_warp = false;
   // large matrices: the wide pair-block kernel (RK_JACOBI_WIDE=0: the 16-column warp kernel)

@@ -180,6 +180,70 @@ __global__ void syrk_records_kernel(const SyrkChunk* __restrict__ chunks, uint32
   }
 }
 
+// The same partials with a 32 x 32 block (4 x 4 tiles) per warp: 8 loaded fragments
+// feed up to 16 DMMAs per k-step instead of 2 feeding 1, a quarter of the L2 traffic
+// (c3: 19.8 GB per merge with a tile per warp -- the kernel ran at the L2's rate,
+// not the tensor cores'). Every tile accumulates its k-steps in the same order with
+// the same zero padding, so the partials are bit-identical to syrk_records_kernel's.
+// M % 32 == 0.
+__global__ void __launch_bounds__(256) syrk_records_kernel4(const SyrkChunk* __restrict__ chunks, uint32_t n_chunks,
+                                                             uint32_t M, double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  const uint32_t nb = M / 32;
+  const uint64_t n_pairs = (uint64_t)nb * (nb + 1) / 2;
+  const uint64_t total = n_pairs * n_chunks;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < total;
+       w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t kc = (uint32_t)(w / n_pairs);
+    const uint64_t bp = w % n_pairs;
+    uint32_t bi = (uint32_t)((sqrt(8.0 * (double)bp + 1.0) - 1.0) * 0.5);
+    while ((uint64_t)bi * (bi + 1) / 2 > bp) --bi;
+    while ((uint64_t)(bi + 1) * (bi + 2) / 2 <= bp) ++bi;
+    const uint32_t bj = (uint32_t)(bp - (uint64_t)bi * (bi + 1) / 2);  // bi >= bj
+    const bool diag = bi == bj;
+    const SyrkChunk c = chunks[kc];
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const double* pa[4];
+    const double* pb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      pa[i] = c.base + (uint64_t)(bi * 32 + i * 8 + lr) * c.k;
+      pb[i] = c.base + (uint64_t)(bj * 32 + i * 8 + lr) * c.k;
+    }
+#pragma unroll 2
+    for (uint32_t j = c.j0; j < c.j1; j += 4) {
+      const uint32_t jj = j + lc;
+      const bool ok = jj < c.j1;
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = ok ? pa[i][jj] : 0.0;
+        b[i] = ok ? pb[i][jj] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jx = 0; jx < 4; ++jx)
+          if (!diag || i >= jx) dmma(acc[i][jx][0], acc[i][jx][1], a[i], b[jx]);
+    }
+    double* out = partial + (uint64_t)kc * M * M;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jx = 0; jx < 4; ++jx)
+        if (!diag || i >= jx) {
+          const uint32_t r = bi * 32 + i * 8 + lr, s0 = bj * 32 + jx * 8 + 2 * lc;
+          out[r + (uint64_t)s0 * M] = acc[i][jx][0];
+          out[r + (uint64_t)(s0 + 1) * M] = acc[i][jx][1];
+        }
+  }
+}
+
 // G = sum of the partials in chunk order, mirrored to the upper triangle
 __global__ void reduce_partials(const double* __restrict__ partial, uint32_t n_chunks, uint32_t M,
                                 double* __restrict__ G) {
@@ -655,6 +719,19 @@ unsigned grid_for(uint64_t n, unsigned cap = 1u << 20) {
   return (unsigned)g;
 }
 
+// split-K SYRK launch: a 32 x 32 block per warp where M allows
+static void launch_syrk(const SyrkChunk* d_chunks, uint32_t n_chunks, uint32_t M, double* partial, cudaStream_t s) {
+  if (M % 32 == 0 && tuning().syrk_block4) {
+    const uint64_t nb = M / 32, warps = nb * (nb + 1) / 2 * n_chunks;
+    syrk_records_kernel4<<<grid_for(warps * 32), 256, 0, s>>>(d_chunks, n_chunks, M, partial);
+  } else {
+    const uint64_t tiles = M / 8, warps = tiles * (tiles + 1) / 2 * n_chunks;
+    syrk_records_kernel<<<grid_for(warps * 32), 256, 0, s>>>(d_chunks, n_chunks, M, partial);
+  }
+  RK_LAUNCH_CHECK();
+}
+
+
 }  // namespace
 
 void sparse_gram(const DevMatrix& m, const Partition& p, uint64_t d_lo, uint64_t nblk, double* G, uint64_t stride,
@@ -742,10 +819,7 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
   DBuf<SyrkChunk> dch(ch.size(), s);
   to_device(dch.get(), ch.data(), ch.size(), s);
   DBuf<double> partial(ch.size() * (uint64_t)M * M, s);
-  const uint64_t tiles = M / 8;
-  const uint64_t warps = tiles * (tiles + 1) / 2 * ch.size();
-  syrk_records_kernel<<<grid_for(warps * 32), 256, 0, s>>>(dch.get(), (uint32_t)ch.size(), M, partial.get());
-  RK_LAUNCH_CHECK();
+  launch_syrk(dch.get(), (uint32_t)ch.size(), M, partial.get(), s);
   RK_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(double) * M * M, s));
   reduce_partials<<<grid_for((uint64_t)M * M), 256, 0, s>>>(partial.get(), (uint32_t)ch.size(), M, G);
   RK_LAUNCH_CHECK();
@@ -810,10 +884,7 @@ void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, 
     DBuf<SyrkChunk> dch(ch.size(), s);
     to_device(dch.get(), ch.data(), ch.size(), s);
     DBuf<double> partial(ch.size() * mm, s);
-    const uint64_t tiles = M / 8;
-    const uint64_t warps = tiles * (tiles + 1) / 2 * ch.size();
-    syrk_records_kernel<<<grid_for(warps * 32), 256, 0, s>>>(dch.get(), (uint32_t)ch.size(), M, partial.get());
-    RK_LAUNCH_CHECK();
+    launch_syrk(dch.get(), (uint32_t)ch.size(), M, partial.get(), s);
     DBuf<uint32_t> d0(L, s), d1(L, s);
     to_device(d0.get(), c0.data(), L, s);
     to_device(d1.get(), c1.data(), L, s);

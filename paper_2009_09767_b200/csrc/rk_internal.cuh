@@ -67,6 +67,7 @@ struct Tuning {
   bool spmm_warp = false;         // RK_SPMM_WARP=1: warp-per-column V SpMM
   bool wide_reduce = true;        // RK_WIDE_REDUCE=0: wide blocks' Jacobi on X = T^T, not on its R
   bool presence_csr = false;      // RK_PRESENCE=csr: the rank check's flags by a thread per CSR entry (row search)
+  bool syrk_block4 = true;        // RK_SYRK=tile: the merge's SYRK with one 8 x 8 tile per warp
   bool repair_speculate = true;   // RK_REPAIR_SPECULATE=0: the neighbor replay without speculated sets
   bool wide_rows_pow2 = true;     // RK_WIDE_ROWS=32: the reduced R's rows padded to multiples of 32
   bool eig_merge = true;          // RK_EIG_MERGE=0: the merge's Gram route by Cholesky + one-sided Jacobi
@@ -430,6 +431,7 @@ void jacobi_batched(std::vector<JacobiJob>& jobs, cudaStream_t s, int sms, size_
 // (pre set) and jacobi_batched only has to certify. false: nothing was launched (a job does not fit, or switched off)
 struct SideStream { cudaStream_t stream; cudaEvent_t fork, join; };  // optional: independent launches overlap the main stream's
 bool jacobi_smem_try(std::vector<JacobiJob>& jobs, cudaStream_t s, size_t smem_optin, const SideStream* side);
+bool jacobi_smem_fits(const JacobiJob& j, size_t smem_optin);  // a cluster's shared memory holds its staged matrix
 // rk_precond.cu: FP32 Jacobi sweeps, then W <- W V with V the (Newton-Schulz
 // orthogonalized) right singular vectors they give -- for gram_ok square jobs
 bool precondition_eligible(const JacobiJob& j);

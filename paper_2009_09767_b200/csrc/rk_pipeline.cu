@@ -338,15 +338,18 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
         // one launch of the shared-memory kernel over every width class; the per-width
         // launches below then only certify
         std::vector<JacobiJob> every;
-        for (auto& kv : by_pad) every.insert(every.end(), kv.second.begin(), kv.second.end());
+        for (auto& kv : by_pad)
+          for (const JacobiJob& j : kv.second)
+            if (jacobi_smem_fits(j, c.smem_optin)) every.push_back(j);
         if (!c.side) {
           RK_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
           for (auto& ev : c.side_ev) RK_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         }
         const SideStream side{c.side, c.side_ev[0], c.side_ev[1]};
-        if (jacobi_smem_try(every, s, c.smem_optin, &side))
+        if (!every.empty() && jacobi_smem_try(every, s, c.smem_optin, &side))
           for (auto& kv : by_pad)
-            for (JacobiJob& j : kv.second) j.pre = 1;
+            for (JacobiJob& j : kv.second)
+              if (jacobi_smem_fits(j, c.smem_optin)) j.pre = 1;
       }
       for (auto& kv : by_pad) {
         std::vector<JacobiJob>& all = kv.second;

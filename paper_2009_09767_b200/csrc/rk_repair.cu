@@ -53,21 +53,38 @@ __global__ void presence_flat_kernel(const uint64_t* __restrict__ row_ptr, const
 // search, same-value races only. grid = (slices of a block, blocks).
 __global__ void __launch_bounds__(256) presence_csc_kernel(const uint64_t* __restrict__ col_ptr,
                                                            const uint32_t* __restrict__ row_idx, uint64_t rows,
-                                                           Partition p, uint32_t* __restrict__ presence) {
+                                                           uint64_t nnz, Partition p, uint32_t* __restrict__ presence) {
   for (uint64_t d = blockIdx.y; d < p.blocks; d += gridDim.y) {
     const uint64_t e0 = col_ptr[p.begin(d)], e1 = col_ptr[p.end(d)];
     uint32_t* f = presence + d * rows;
-    // 4 entries per thread and step (one 16-byte load where aligned)
-    for (uint64_t e = e0 + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < e1;
-         e += (uint64_t)gridDim.x * blockDim.x * 4) {
-      if (e + 4 <= e1 && (e & 3) == 0) {
-        const uint4 r = __ldcs(reinterpret_cast<const uint4*>(row_idx + e));
-        f[r.x] = 1u;
-        f[r.y] = 1u;
-        f[r.z] = 1u;
-        f[r.w] = 1u;
-      } else {
-        for (uint64_t k = e; k < e + 4 && k < e1; ++k) f[__ldcs(row_idx + k)] = 1u;
+    // 16-byte loads from the slice's aligned start (entries outside [e0, e1) masked),
+    // two per thread and step, both issued before the first flag store
+    const uint64_t eb = e0 & ~(uint64_t)3;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t e = eb + ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; e < e1; e += 2 * stride) {
+      uint4 r[2];
+      bool ok[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t eu = e + u * stride;
+        ok[u] = eu < e1;
+        r[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (ok[u] && eu + 4 <= nnz) {
+          r[u] = __ldcs(reinterpret_cast<const uint4*>(row_idx + eu));
+        } else if (ok[u]) {
+          r[u].x = eu < nnz ? row_idx[eu] : 0u;
+          r[u].y = eu + 1 < nnz ? row_idx[eu + 1] : 0u;
+          r[u].z = eu + 2 < nnz ? row_idx[eu + 2] : 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        const uint64_t eu = e + u * stride;
+        if (eu >= e0 && eu < e1) f[r[u].x] = 1u;
+        if (eu + 1 >= e0 && eu + 1 < e1) f[r[u].y] = 1u;
+        if (eu + 2 >= e0 && eu + 2 < e1) f[r[u].z] = 1u;
+        if (eu + 3 >= e0 && eu + 3 < e1) f[r[u].w] = 1u;
       }
     }
   }
@@ -464,9 +481,9 @@ static void presence_launch(const DevMatrix& a, const Partition& p, uint32_t* fl
                                                              flag);
   } else {
     const uint64_t per_block = ceil_div(a.csc.nnz, p.blocks);
-    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(64, ceil_div(per_block, 256 * 4 * 4)));
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(64, ceil_div(per_block, 256 * 4 * 2)));
     const unsigned gy = (unsigned)std::min<uint64_t>(p.blocks, 65535);
-    presence_csc_kernel<<<dim3(gx, gy), 256, 0, s>>>(a.csc.ptr.get(), a.csc.idx.get(), a.csr.rows, p, flag);
+    presence_csc_kernel<<<dim3(gx, gy), 256, 0, s>>>(a.csc.ptr.get(), a.csc.idx.get(), a.csr.rows, a.csc.nnz, p, flag);
   }
   RK_LAUNCH_CHECK();
 }

@@ -1297,6 +1297,10 @@ def dev_sharded_full_svd(m: DeviceMatrix, block_count: int, method, keep: int, s
         mine = torch.as_tensor(_CudaArray(d_mine, (count,)), device="cuda")
         alls = torch.as_tensor(_CudaArray(d_all, (count * world,)), device="cuda")
         allgather(mine, alls)
+        # the C ABI's contract: `all` is filled when the callback returns. torch's collectives and
+        # copies are asynchronous on torch's current stream, which is not the library's (a context
+        # on torch's default stream runs on its own non-blocking stream), so wait for them here
+        torch.cuda.current_stream().synchronize()
 
     fn = ALLGATHER_FN(cb)
     out = C.POINTER(DevOutputs)()

@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_launches.log 2>&1 || exit 2
 ncu --set full --clock-control none --import-source on \
     -k regex:'jacobi|qr_kernel|spmm|sparse_gram|cholesky|syrk_records|neighbor|speculate|presence|random_fill|apply_q|tridiag|bisect|inverse_iter' \
-    --launch-count 12 -f -o /tmp/${tag}_full \
+    --launch-count 24 -f -o /tmp/${tag}_full \
     python bench.py --config $cfg --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_full.log 2>&1 || exit 3
 # the report itself stays on the box (gpurun_out is capped at 64 MiB): its raw page as CSV
 ncu -i /tmp/${tag}_full.ncu-rep --page raw --csv > gpurun_out/${tag}_full_raw.csv || exit 4

@@ -196,6 +196,42 @@ def test_variant_switches_agree(env, tuning_env, ref):
     assert np.array_equal(res.svd.v, vr)
 
 
+@pytest.mark.parametrize("env", [("RK_JACOBI_SMEM", "0"), ("RK_JACOBI_SMEM_CL", "1"), ("RK_APPLY_Q", "panel"),
+                                 ("RK_PRESENCE", "csr")])
+def test_wide_block_variants_agree(env, tuning_env, ref):
+    """c3's route (wide blocks: QR of X = T^T, Jacobi on R, apply_q; NeighborChecker) against the
+    reference's run_pipeline on a 16-block slice, with the round-2 kernels switched off one at a
+    time: the direct Jacobi instead of the shared-memory Gram-assisted one, one-CTA jobs only (the
+    larger R factors then take the direct kernel), apply_q reflector by reflector instead of
+    compact-WY, the rank check from the CSR instead of the CSC slices."""
+    tuning_env(*env)
+    cfg = configs.CONFIGS["c3"]
+    blocks = 16
+    a = cfg.generate(8192 * blocks)
+    r, c, v = a.coo()
+    res = rk.run_pipeline(a, blocks, cfg.method, cfg.keep, cfg.seed, 1, want_v=True)
+    o = ref.run_pipeline((a.rows(), a.cols(), r, c, v), blocks, cfg.method, cfg.keep, cfg.seed)
+    assert np.array_equal(res.report.edges_array(), o.edges)
+    compare(res.svd, o.sigma, o.u, f"c3 slice {env}")
+    vr = ref.recover_right_vectors((a.rows(), a.cols(), *res.repaired.coo()), res.svd.u, res.svd.sigma, 1e-10)
+    assert np.array_equal(res.svd.v, vr)
+
+
+def test_syrk_block_kernel_bitwise(tuning_env):
+    """The merge's SYRK with a 32 x 32 block per warp (default) and with one 8 x 8 tile per warp
+    (RK_SYRK=tile) accumulate every tile's k-steps in the same order: the pipeline's outputs are
+    bitwise the same."""
+    cfg = configs.CONFIGS["c2"]
+    a = cfg.generate(262144 // 4)
+    outs = []
+    for mode in ("block", "tile"):
+        tuning_env("RK_SYRK", mode)
+        res = rk.run_pipeline(a, cfg.blocks // 4, cfg.method, cfg.keep, cfg.seed, 1)
+        outs.append((res.svd.sigma.copy(), res.svd.u.copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
 def test_gram_kernels_bitwise(tuning_env):
     """The block Gram from rows x columns (default) and from row pairs (the
     merge-join kernel, RK_GRAM_PAIRS=1) add every G(r, s) in ascending column

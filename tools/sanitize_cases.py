@@ -46,3 +46,14 @@ if which in ("all", "dense"):
     low = rng.standard_normal((40, 5)) @ rng.standard_normal((5, 30))
     rk.dense_svd(low)
     print("dense", s.sigma[:2], rk.numerical_rank(low, 1e-10), rk.left_vector_error(s.u, s.u, s.sigma), flush=True)
+if which in ("all", "c3s"):
+    # a c3 slice: wide blocks on the reduced route (QR with T kept, the shared-memory Gram-assisted Jacobi at
+    # cluster sizes 1 and 2, the compact-WY apply_q), NeighborChecker, eigensolver merge
+    cfg = configs.CONFIGS["c3"]
+    res = rk.run_pipeline(cfg.generate(8192 * 16), 16, cfg.method, cfg.keep, cfg.seed, 1, want_v=True)
+    print("c3 slice", res.svd.sigma[:3], flush=True)
+if which in ("all", "wide"):
+    # a c4 slice: 1024-row Gram-route blocks through the wide pair-block Jacobi (one launch per step)
+    cfg = configs.CONFIGS["c4"]
+    res = rk.run_pipeline(cfg.generate(16384 * 2), 2, cfg.method, cfg.keep, cfg.seed, 1, want_v=False)
+    print("c4 slice", res.svd.sigma[:3], flush=True)
