@@ -1517,13 +1517,14 @@ __global__ void __launch_bounds__(256) wide_sweep_begin(const JacobiJob* jobs) {
 }
 
 __global__ void wide_sweep_end(const JacobiJob* jobs, uint32_t njobs, double stop_ratio, int max_sweeps,
-                               uint32_t* active) {
+                               uint32_t* active, int debug) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= njobs) return;
   const JacobiJob job = jobs[q];
   if (job.stats[7]) return;
   const unsigned long long rot = job.stats[4];
   const double ratio = sqrt(__longlong_as_double((long long)job.stats[5]));
+  if (debug && q == 0) printf("[wide] job 0 sweep %d: rot %llu ratio %.3e\n", (int)job.stats[0] + 1, rot, ratio);
   job.stats[0] += 1ull;
   job.stats[1] += rot;
   job.stats[3] = (uint64_t)__double_as_longlong(ratio);
@@ -2301,7 +2302,8 @@ static bool jacobi_wide_batched(const std::vector<JacobiJob>& jobs, const Jacobi
       RK_LAUNCH_CHECK();
     }
     active.zero();
-    wide_sweep_end<<<(unsigned)ceil_div(njobs, 256), 256, 0, s>>>(d_jobs, njobs, stop_ratio, kWideMaxSweeps, active.get());
+    wide_sweep_end<<<(unsigned)ceil_div(njobs, 256), 256, 0, s>>>(d_jobs, njobs, stop_ratio, kWideMaxSweeps, active.get(),
+                                                                      tuning().jacobi_debug ? 1 : 0);
     RK_LAUNCH_CHECK();
     std::vector<uint32_t> h;
     to_host(h, active.get(), 1, s);
