@@ -46,6 +46,7 @@ Tuning read_tuning() {
   if (const char* e = std::getenv("RK_JACOBI_SMEM")) t.jacobi_smem = e[0] == '1' ? 1 : 0;
   t.jacobi_smem_cl = (int)num("RK_JACOBI_SMEM_CL", 2);
   if (const char* e = std::getenv("RK_JACOBI_WIDE")) t.jacobi_wide = e[0] != '0';
+  if (const char* e = std::getenv("RK_JACOBI_CARRY")) t.jacobi_carry = e[0] != '0';
   if (const char* e = std::getenv("RK_PRESENCE")) t.presence_csr = std::string(e) == "csr";
   if (const char* e = std::getenv("RK_SYRK")) t.syrk_block4 = std::string(e) != "tile";
   t.jacobi_check = num("RK_JACOBI_CHECK", -1.0);

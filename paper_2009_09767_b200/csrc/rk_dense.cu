@@ -943,7 +943,8 @@ __device__ __forceinline__ bool fresh_scan(const double* sH, double freeze, bool
 }
 
 // The rounds of one step on H; leaves Z (16 x 16 row-major, stride kWN) where H was.
-__device__ __forceinline__ void step_rounds(double* sH, bool intra, double freeze, uint32_t& nrot) {
+__device__ __forceinline__ void step_rounds(double* sH, bool intra, double freeze, uint32_t& nrot,
+                                            double* keepA = nullptr, double* keepB = nullptr) {
   const int lane = threadIdx.x & 31;
   double z[kWN], cs[16];
 #pragma unroll
@@ -968,6 +969,15 @@ __device__ __forceinline__ void step_rounds(double* sH, bool intra, double freez
   smem_round2<0, 6, 0, 5>(sH, z, cs, freeze, nrot);
   smem_round2<0, 7, 0, 6>(sH, z, cs, freeze, nrot);
   z_apply<0, 7>(z, cs);
+  if (keepA) {  // the rotated diagonal blocks (8 x 8 each) outlive the step: the groups carry them
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = lane + 32 * u, i = t >> 3, j = t & 7;
+      __stcg(keepA + t, sH[i * kWS + j]);
+      __stcg(keepB + t, sH[(kWG + i) * kWS + kWG + j]);
+    }
+    __syncwarp();
+  }
   if (lane < kWN) {  // H is dead: Z takes its place
 #pragma unroll
     for (int k = 0; k < kWN; ++k) sH[lane * kWN + k] = z[k];
@@ -1210,6 +1220,8 @@ struct SmemParams {
   uint32_t cap_cols;  // columns the layout holds per CTA (multiple of 8)
   uint32_t nw;        // warps per CTA
   double stop_ratio;
+  double* keep;          // per job of the launch: its groups' carried diagonal blocks (null: full Grams every step)
+  uint64_t keep_stride;  // doubles per job
 };
 constexpr int kSH = kWN * kWS;  // doubles per warp: H (16 x 17); its pad column holds the round's 8 (c, s)
 constexpr int kSmemMaxWarps = 12;
@@ -1257,6 +1269,57 @@ __device__ __forceinline__ void smem_gram(const double* pA, const double* pB, ui
     sH[(8 + lr) * kWS + j] = t10;
     sH[j * kWS + 8 + lr] = t10;
     sH[(8 + lr) * kWS + 8 + j] = t11;
+  }
+  __syncwarp();
+}
+
+// The cross block (B, A) only, by DMMA; the two diagonal blocks come from the
+// groups' carried 8 x 8 blocks (kept by step_rounds after the groups' last step,
+// seeded afresh by the full Gram of every sweep's step 0): a third of the Gram's
+// DMMAs. The carried blocks are H entries that have been through the rotations of
+// the steps since -- the same two-sided updates the rounds of one step apply.
+__device__ __forceinline__ void smem_gram_cross(const double* pA, const double* pB, uint32_t ld, uint32_t rows,
+                                                const double* keepA, const double* keepB, double* sH) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+  double da[2], db[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {  // issued first: in flight during the DMMA loop
+    da[u] = __ldcg(keepA + lane + 32 * u);
+    db[u] = __ldcg(keepB + lane + 32 * u);
+  }
+  const double* pa = pA + (uint32_t)lr * ld + lc;
+  const double* pb = pB + (uint32_t)lr * ld + lc;
+  double h[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i][0] = h[i][1] = 0.0;
+  uint32_t k0 = 0;
+  for (; k0 + 16 <= rows; k0 += 16) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = pa[k0 + 4 * u];
+      b[u] = pb[k0 + 4 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma884(h[u][0], h[u][1], b[u], a[u]);
+  }
+  for (; k0 < rows; k0 += 8) {  // rows is a multiple of 8
+    const double a0 = pa[k0], b0 = pb[k0], a1 = pa[k0 + 4], b1 = pb[k0 + 4];
+    dmma884(h[0][0], h[0][1], b0, a0);
+    dmma884(h[1][0], h[1][1], b1, a1);
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int j = 2 * lc + e;
+    const double t10 = (h[0][e] + h[1][e]) + (h[2][e] + h[3][e]);
+    sH[(8 + lr) * kWS + j] = t10;
+    sH[j * kWS + 8 + lr] = t10;
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = lane + 32 * u, i = t >> 3, j = t & 7;
+    sH[i * kWS + j] = da[u];
+    sH[(kWG + i) * kWS + kWG + j] = db[u];
   }
   __syncwarp();
 }
@@ -1345,6 +1408,7 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(Smem
   }
   sync_all();
   const uint32_t pw = rank * P.nw + warp;  // this warp's pair slot
+  double* keep = P.keep ? P.keep + (uint64_t)(blockIdx.x / csize) * P.keep_stride : nullptr;  // G x 64 carried blocks
   unsigned long long total_rot = 0;
   double last_ratio = 0.0, prev_ratio = INFINITY;
 #ifdef RK_SMEM_PROBE
@@ -1383,10 +1447,17 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(Smem
     double best_g2 = 0.0, best_prod = 1.0;  // the largest gamma^2 / (alpha_p alpha_q) as a fraction
     for (uint32_t step = 0; step + 1 < G; ++step) {
       if (pw < npairs) {
-        double* pA = group_ptr(rr_slot(pw, step, G));
-        double* pB = group_ptr(rr_slot(G - 1 - pw, step, G));
+        const uint32_t gA = rr_slot(pw, step, G), gB = rr_slot(G - 1 - pw, step, G);
+        double* pA = group_ptr(gA);
+        double* pB = group_ptr(gB);
+        double* keepA = keep ? keep + (uint64_t)gA * (kWG * kWG) : nullptr;
+        double* keepB = keep ? keep + (uint64_t)gB * (kWG * kWG) : nullptr;
         PROBE_T0();
-        smem_gram(pA, pB, ld, rows, sH);
+        if (step == 0 || !keep) {
+          smem_gram(pA, pB, ld, rows, sH);
+        } else {
+          smem_gram_cross(pA, pB, ld, rows, keepA, keepB, sH);
+        }
         PROBE_ADD(0);
         // fresh ratios of the 16 columns' pairs; does any pair this step rotates exceed the threshold?
         const bool any_need = fresh_scan(sH, freeze, step == 0, best_g2, best_prod);
@@ -1395,10 +1466,17 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) jacobi_smem_kernel(Smem
         if (any_need) ++worked; else ++skipped;
 #endif
         if (any_need) {
-          step_rounds(sH, step == 0, freeze, nrot);
+          step_rounds(sH, step == 0, freeze, nrot, keepA, keepB);
           PROBE_ADD(2);
           smem_xz(pA, pB, ld, rows, sH);
           PROBE_ADD(3);
+        } else if (keep && step == 0) {  // seed the carried blocks with the fresh ones
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int t = lane + 32 * u, i = t >> 3, j = t & 7;
+            __stcg(keepA + t, sH[i * kWS + j]);
+            __stcg(keepB + t, sH[(kWG + i) * kWS + kWG + j]);
+          }
         }
       }
       PROBE_T0();
@@ -2232,6 +2310,12 @@ static bool jacobi_smem_batched(const std::vector<JacobiJob>& jobs, const Jacobi
   for (size_t i = 0; i < jobs.size(); ++i)
     if (!shape_of(jobs[i], shapes[i])) return false;
   bool forked = false;
+  // the groups' carried diagonal blocks: (columns / 8) x 64 doubles per job, allocated before any
+  // launch is forked to the side stream and freed in stream order after the join
+  uint64_t keep_stride = 0;
+  for (const Shape& sh : shapes) keep_stride = std::max<uint64_t>(keep_stride, (uint64_t)sh.cap_cols * sh.cl * kWG);
+  DBuf<double> keep_all;
+  if (tuning().jacobi_carry) keep_all.alloc(jobs.size() * keep_stride, s);
   for (size_t i0 = 0; i0 < jobs.size();) {
     size_t i1 = i0;
     Shape m = shapes[i0];
@@ -2253,8 +2337,9 @@ static bool jacobi_smem_batched(const std::vector<JacobiJob>& jobs, const Jacobi
       }
       bytes = ((size_t)m.cap_cols * (m.rows + 4) + (size_t)m.nw * kSH + kSmemMisc) * sizeof(double);
     }
-    SmemParams P{d_jobs + i0, m.rows + 4, m.cap_cols, m.nw, stop_ratio};
     const unsigned n = (unsigned)(i1 - i0);
+    double* keep = keep_all.get() ? keep_all.get() + (uint64_t)i0 * keep_stride : nullptr;
+    SmemParams P{d_jobs + i0, m.rows + 4, m.cap_cols, m.nw, stop_ratio, keep, keep_stride};
     // runs are independent (disjoint jobs): every run but the last goes to the side
     // stream, so a short run of clustered jobs shares the device with the main run
     const bool aside = side && side->stream && i1 < jobs.size();

@@ -52,6 +52,7 @@ struct Tuning {
   int jacobi_warp = -1;           // RK_JACOBI_WARP=0/1 (-1: by shape)
   int jacobi_smem = -1;           // RK_JACOBI_SMEM=0/1: the shared-memory-resident Gram-assisted kernel (-1: batched blocks)
   int jacobi_smem_cl = 2;         // RK_JACOBI_SMEM_CL: its largest cluster (1, 2, 4, 8)
+  bool jacobi_carry = true;       // RK_JACOBI_CARRY=0: the shared-memory kernel forms the full 16 x 16 Gram every step
   bool jacobi_wide = true;        // RK_JACOBI_WIDE=0: no wide pair-block kernel for >= 1024-row matrices
   double jacobi_check = -1.0;     // RK_JACOBI_CHECK: tail-check ratio (<0: by workload; 0 off)
   int jacobi_cluster = 0;         // RK_JACOBI_CLUSTER: cluster size override (0: planned)
