@@ -113,12 +113,23 @@ __global__ void fill_kernel(const uint64_t* col_ptr, const uint32_t* row_idx, co
       uint32_t before = carry;
       for (int w = 0; w < warp; ++w) before += warp_tot[w];
       const uint32_t idx = before + inc - f;
-      if (f) {
-        if (phase == 0) {
-          for (uint64_t k = col_ptr[x]; k < col_ptr[x + 1]; ++k) put(idx, row_idx[k], val[k]);
-        } else {
-          put(pl.n_multi + idx, x, sqrt(single[i_blk * rows + x]));
+      if (phase == 0) {
+        // a short column is scattered by its own thread; a long one (Zipf columns have up to M
+        // entries: one thread's dependent loads were the kernel's long pole) by its whole warp
+        const uint64_t k0 = f ? col_ptr[x] : 0, k1 = f ? col_ptr[x + 1] : 0;
+        constexpr uint64_t kLong = 8;
+        if (f && k1 - k0 <= kLong)
+          for (uint64_t k = k0; k < k1; ++k) put(idx, row_idx[k], val[k]);
+        unsigned heavy = __ballot_sync(0xffffffffu, f && k1 - k0 > kLong);
+        while (heavy) {
+          const int src = __ffs(heavy) - 1;
+          heavy &= heavy - 1;
+          const uint64_t b0 = __shfl_sync(0xffffffffu, k0, src), b1 = __shfl_sync(0xffffffffu, k1, src);
+          const uint32_t t = __shfl_sync(0xffffffffu, idx, src);
+          for (uint64_t k = b0 + lane; k < b1; k += 32) put(t, row_idx[k], val[k]);
         }
+      } else if (f) {
+        put(pl.n_multi + idx, x, sqrt(single[i_blk * rows + x]));
       }
       __syncthreads();
       if (threadIdx.x == kT - 1) carry = before + inc;
