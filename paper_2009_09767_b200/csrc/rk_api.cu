@@ -446,7 +446,8 @@ void full_run(Ctx& c, const DevMatrix& a, const Partition& p, rk_method method, 
   }
   {
     RK_NVTX("rk.merge");
-    merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge);
+    merge_records(c, fr.blocks.payload.get(), fr.blocks.offset, fr.blocks.kept, (uint32_t)rep.csr.rows, fr.merge,
+                  &fr.blocks.eff);
   }
   RK_CUDA_CHECK(cudaEventRecord(ev3, s));
   prof_mark(s, "merge (end)");
@@ -1351,11 +1352,11 @@ void shard_factor(rk_ctx* ctx, const rk_dev_matrix* a, uint64_t block_count, rk_
   if (gram) {
     std::vector<std::pair<uint32_t, uint32_t>> lr;
     for (const TreeLeaf& L : sh->local) lr.push_back({L.r0, L.r1});
-    leaf_gram_tree(br.payload.get(), br.offset, br.kept, M, lr, d_out, s);
+    leaf_gram_tree(br.payload.get(), br.offset, br.kept, M, lr, d_out, s, &br.eff);
     sh->has_records = true;
   } else {
     DBuf<double> R;
-    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, sh->local, 0, sh->local.size(), R);
+    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, sh->local, 0, sh->local.size(), R, &br.eff);
     RK_CUDA_CHECK(cudaMemcpyAsync(d_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice, s));
     if (keep_records) sh->has_records = true;
     else br.payload.release();
@@ -1461,7 +1462,7 @@ rk_status rk_dev_shard_tsqr(rk_ctx* ctx, rk_dev_shard* shard, double* d_root_out
     const uint32_t M = (uint32_t)shard->rep()->csr.rows;
     BlockStageResult& br = shard->blocks;
     DBuf<double> R;
-    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, shard->local, 0, shard->local.size(), R);
+    merge_subtree(c, br.payload.get(), br.offset, br.kept, M, shard->local, 0, shard->local.size(), R, &br.eff);
     RK_CUDA_CHECK(cudaMemcpyAsync(d_root_out, R.get(), sizeof(double) * (uint64_t)M * M, cudaMemcpyDeviceToDevice,
                                   c.stream));
     sync(c.stream);

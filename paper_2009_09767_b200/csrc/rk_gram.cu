@@ -781,9 +781,13 @@ __global__ void record_effective_cols(const double* payload, const uint64_t* off
 
 std::vector<uint32_t> record_eff_cols(const double* payload, const std::vector<uint64_t>& offset,
                                       const std::vector<uint32_t>& kept, uint32_t M, uint32_t r_lo, uint32_t r_hi,
-                                      cudaStream_t s) {
+                                      cudaStream_t s, const std::vector<uint32_t>* hint) {
   std::vector<uint32_t> eff(kept.size(), 0);
   if (r_hi <= r_lo || !M) return eff;
+  if (hint && hint->size() == kept.size()) {  // the block stage knows: no scan of the records
+    for (uint32_t d = r_lo; d < r_hi; ++d) eff[d] = std::min((*hint)[d], kept[d]);
+    return eff;
+  }
   DBuf<uint64_t> doff(offset.size(), s);
   DBuf<uint32_t> dkept(kept.size(), s), deff(kept.size(), s);
   to_device(doff.get(), offset.data(), offset.size(), s);
@@ -797,7 +801,7 @@ std::vector<uint32_t> record_eff_cols(const double* payload, const std::vector<u
 }
 
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
-                  uint32_t M, double* G, cudaStream_t s) {
+                  uint32_t M, double* G, cudaStream_t s, const std::vector<uint32_t>* eff_hint) {
   if (M % 8) fail(RK_RUNTIME, "records_gram: M must be a multiple of 8");
   // split-K chunks of at most kChunk columns of one record; each chunk has an
   // M x M partial, so the chunk width grows with M to bound that buffer (c4:
@@ -805,7 +809,7 @@ void records_gram(const double* payload, const std::vector<uint64_t>& offset, co
   const uint32_t kChunk = M <= 256 ? 256u : 1024u;
   // only each record's leading nonzero columns (record_eff_cols): the zero ones add
   // nothing to P P^T (c3: ~385 of 512 per record)
-  const std::vector<uint32_t> eff = record_eff_cols(payload, offset, kept, M, 0, (uint32_t)kept.size(), s);
+  const std::vector<uint32_t> eff = record_eff_cols(payload, offset, kept, M, 0, (uint32_t)kept.size(), s, eff_hint);
   std::vector<SyrkChunk> ch;
   for (size_t d = 0; d < kept.size(); ++d) {
     if (!eff[d]) continue;
@@ -858,7 +862,8 @@ void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s) {
 }
 
 void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
-                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s) {
+                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s,
+                    const std::vector<uint32_t>* eff_hint) {
   if (M % 8) fail(RK_RUNTIME, "leaf_gram_tree: M must be a multiple of 8");
   const uint64_t mm = (uint64_t)M * M, L = leaves.size();
   if (L == 0) {
@@ -869,7 +874,7 @@ void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, 
   std::vector<uint32_t> c0(L), c1(L);
   // each record's leading nonzero columns only (record_eff_cols), as records_gram
   const std::vector<uint32_t> eff =
-      record_eff_cols(payload, offset, kept, M, leaves.front().first, leaves.back().second, s);
+      record_eff_cols(payload, offset, kept, M, leaves.front().first, leaves.back().second, s, eff_hint);
   for (uint64_t l = 0; l < L; ++l) {
     c0[l] = (uint32_t)ch.size();
     for (uint32_t d = leaves[l].first; d < leaves[l].second; ++d) {

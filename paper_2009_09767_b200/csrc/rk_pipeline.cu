@@ -217,6 +217,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
   const uint64_t nblk = d_hi - d_lo;
   out.offset.assign(nblk, 0);
   out.kept.assign(nblk, 0);
+  out.eff.assign(nblk, 0);
   out.failures.assign(nblk, std::string());
   if (nblk == 0) return;
 
@@ -373,6 +374,7 @@ void block_stage(Ctx& c, const DevMatrix& a, const Partition& p, uint64_t d_lo, 
       f.rows = M;
       f.cols = cols_pad_full;
       f.k = out.kept[i];
+      out.eff[i] = std::min<uint32_t>(out.kept[i], std::max<uint32_t>(cols[q], 1));  // columns past cols[q] are zero
       f.payload = out.payload.get() + out.offset[i];
       f.order = order.get() + (uint64_t)q * cols_pad_full;
       f.scratch = fscratch.get() + (uint64_t)q * cols_pad_full;
@@ -773,7 +775,7 @@ void tsqr_forest(Ctx& c, uint32_t n, std::vector<std::vector<LeafRef>>& leaves, 
 
 void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
                    const std::vector<uint32_t>& kept, uint32_t M, const std::vector<TreeLeaf>& leaves,
-                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out) {
+                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out, const std::vector<uint32_t>* eff_hint) {
   cudaStream_t s = c.stream;
   DBuf<uint64_t> doff(offset.size(), s);
   DBuf<uint32_t> dkept(kept.size(), s);
@@ -782,7 +784,7 @@ void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& o
   // the leaves keep the record grouping of `kept` (data-independent, so a shard's
   // subtree is a node of the whole tree), but stack only each record's nonzero columns
   const uint32_t rec_lo = leaves[leaf_lo].r0, rec_hi = leaves[leaf_hi - 1].r1;
-  const std::vector<uint32_t> heff = record_eff_cols(payload, offset, kept, M, rec_lo, rec_hi, s);
+  const std::vector<uint32_t> heff = record_eff_cols(payload, offset, kept, M, rec_lo, rec_hi, s, eff_hint);
   DBuf<uint32_t> deff(kept.size(), s);
   to_device(deff.get(), heff.data(), heff.size(), s);
   std::vector<DBuf<double>> bufs;
@@ -934,7 +936,7 @@ bool gram_merge(Ctx& c, DBuf<double>& W, uint32_t M, MergeOut& out) {
 }
 
 void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
-                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out) {
+                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out, const std::vector<uint32_t>* eff_hint) {
   cudaStream_t s = c.stream;
   uint64_t total = 0;
   for (uint32_t k : kept) total += k;
@@ -951,7 +953,7 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
       DBuf<double> W((uint64_t)M * cp, s);
       W.zero();
       prof_mark(s, "mrg alloc");
-      records_gram(payload, offset, kept, M, W.get(), s);
+      records_gram(payload, offset, kept, M, W.get(), s, eff_hint);
       prof_mark(s, "mrg syrk");
       if (gram_merge(c, W, M, out)) {
         const double Md = M;
@@ -961,7 +963,7 @@ void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& o
     }
     std::vector<TreeLeaf> leaves = merge_leaves(kept, M);
     std::vector<DBuf<double>> roots(1);
-    merge_subtree(c, payload, offset, kept, M, leaves, 0, leaves.size(), roots[0]);
+    merge_subtree(c, payload, offset, kept, M, leaves, 0, leaves.size(), roots[0], eff_hint);
     merge_finish(c, roots, M, out);
     out.flops = 2.0 * (double)total * M * (double)M + jacobi_flops_of(out.sweeps, out.rotations, M, M);
     return;

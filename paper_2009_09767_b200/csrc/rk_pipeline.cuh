@@ -18,6 +18,9 @@ struct BlockStageResult {
   DBuf<double> payload;               // records back to back (M x kept row-major each)
   std::vector<uint64_t> offset;       // doubles into payload, per block
   std::vector<uint32_t> kept;
+  // per block: columns past eff are zero by construction (a block of n_d < kept nonzero columns); the
+  // merge reads only those and need not scan the records for it (record_eff_cols)
+  std::vector<uint32_t> eff;
   std::vector<std::string> failures;  // per block, empty = ok (reference "block task d failed: ...")
   double conv_residual = 0.0;
   uint64_t sweeps_max = 0, rotations = 0, sweeps_sum = 0;
@@ -55,12 +58,13 @@ std::vector<TreeLeaf> merge_leaves(const std::vector<uint32_t>& kept, uint32_t M
 // R factor (M x M column-major, upper) of the stacked leaves [leaf_lo, leaf_hi)
 void merge_subtree(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
                    const std::vector<uint32_t>& kept, uint32_t M, const std::vector<TreeLeaf>& leaves,
-                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out);
+                   size_t leaf_lo, size_t leaf_hi, DBuf<double>& r_out, const std::vector<uint32_t>* eff_hint = nullptr);
 // top of the tree over R factors (each M x M column-major), then Jacobi on R^T
 void merge_finish(Ctx& c, std::vector<DBuf<double>>& roots, uint32_t M, MergeOut& out);
 // the whole proxy SVD of the records (sigma, U of P)
 void merge_records(Ctx& c, const double* payload, const std::vector<uint64_t>& offset,
-                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out);
+                   const std::vector<uint32_t>& kept, uint32_t M, MergeOut& out,
+                   const std::vector<uint32_t>* eff_hint = nullptr);
 
 // the merge's Gram route (see merge_records): eligibility, and the finish from
 // W = P P^T (M x jacobi_cols_pad slot, consumed); false when the kappa guard rejects
@@ -88,9 +92,9 @@ void sparse_gram(const DevMatrix& a, const Partition& p, uint64_t d_lo, uint64_t
 // exactly zero, so the columns past eff[d] are zero
 std::vector<uint32_t> record_eff_cols(const double* payload, const std::vector<uint64_t>& offset,
                                       const std::vector<uint32_t>& kept, uint32_t M, uint32_t r_lo, uint32_t r_hi,
-                                      cudaStream_t s);
+                                      cudaStream_t s, const std::vector<uint32_t>* hint = nullptr);
 void records_gram(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
-                  uint32_t M, double* G, cudaStream_t s);
+                  uint32_t M, double* G, cudaStream_t s, const std::vector<uint32_t>* eff_hint = nullptr);
 void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32_t* d_status, double* d_ratio,
                       cudaStream_t s);
 // the Gram of the stacked records of the given leaves (block ranges [first, second)):
@@ -98,7 +102,8 @@ void cholesky_batched(double* const* d_mats, uint32_t n_mats, uint32_t M, uint32
 // pairwise tree -- so a rank's aligned power-of-two run of leaves is a node of the
 // whole matrix's tree. G: M x M column-major (full).
 void leaf_gram_tree(const double* payload, const std::vector<uint64_t>& offset, const std::vector<uint32_t>& kept,
-                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s);
+                    uint32_t M, const std::vector<std::pair<uint32_t, uint32_t>>& leaves, double* G, cudaStream_t s,
+                    const std::vector<uint32_t>* eff_hint = nullptr);
 // pairwise tree sum of n M x M matrices stored back to back; the result in mats[0, M*M)
 void gram_tree_sum(double* mats, uint64_t n, uint32_t M, cudaStream_t s);
 // symmetric diagonal ordering of nb Grams (slots of `stride` doubles, M x M,
