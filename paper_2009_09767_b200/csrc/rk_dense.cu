@@ -1994,6 +1994,18 @@ __global__ void __launch_bounds__(256) finalize_write_kernel(const FinalJob* job
     s_sig[tx] = j < J.k ? J.scratch[o & kOrderSrc] : 0.0;
   }
   __syncthreads();
+  // a tile whose 32 columns all have sigma = 0 (deficient: u = 0, payload = 0): zeros out, no read of W
+  // (c3: ~370 of every block's 512 columns)
+  if (!J.v_out && __syncthreads_and(s_sig[tx] == 0.0 && ((s_src[tx] & kOrderDef) != 0u || j0 + tx >= J.k))) {
+    for (int r = ty; r < 32; r += 8) {
+      const uint32_t i = i0 + r, j = j0 + tx;
+      if (i < J.rows && j < J.k) {
+        if (J.u) J.u[(uint64_t)i * J.k + j] = 0.0;
+        if (J.payload) J.payload[(uint64_t)i * J.k + j] = 0.0;
+      }
+    }
+    return;
+  }
   auto pass = [&](const double* src_base, uint64_t ld, uint32_t nrows, double* out_u, double* out_p, bool is_v) {
     if (i0 >= nrows) return;
     for (int c = ty; c < 32; c += 8) {
