@@ -257,31 +257,66 @@ __global__ void inverse_solve_kernel(uint32_t M, const double* __restrict__ work
   double scale = 1.0;  // z = scale * y, y kept unnormalised between passes
   for (int it = 0; it < 3; ++it) {
     // forward: L^{-1} with the row interchanges
+    // the recurrences read Zt one element ahead of (forward) or at (backward) the one they
+    // write; eight elements are loaded before the eight dependent steps that use and
+    // overwrite them, so the chain waits for one L2 round trip per eight steps, not per step
+    constexpr uint32_t kB = 8;
     double zi = it == 0 ? 1.0 : Zt[j] * scale;
-#pragma unroll 8
-    for (uint32_t i = 0; i + 1 < M; ++i) {
-      const uint64_t at = (uint64_t)i * M + j;
-      const double zn = it == 0 ? 1.0 : Zt[at + M] * scale;
-      const double m = __ldg(dl + at);
-      if (__ldg(pivw + at)) {
-        Zt[at] = zn;
-        zi = fma(-m, zn, zi);
-      } else {
-        Zt[at] = zi;
-        zi = fma(-m, zi, zn);
+    for (uint32_t i0 = 0; i0 + 1 < M; i0 += kB) {
+      double zn[kB], mm[kB];
+      uint8_t pv[kB];
+#pragma unroll
+      for (uint32_t u = 0; u < kB; ++u) {
+        const uint32_t i = i0 + u;
+        if (i + 1 < M) {
+          const uint64_t at = (uint64_t)i * M + j;
+          zn[u] = it == 0 ? 1.0 : Zt[at + M] * scale;
+          mm[u] = __ldg(dl + at);
+          pv[u] = __ldg(pivw + at);
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kB; ++u) {
+        const uint32_t i = i0 + u;
+        if (i + 1 < M) {
+          const uint64_t at = (uint64_t)i * M + j;
+          if (pv[u]) {
+            Zt[at] = zn[u];
+            zi = fma(-mm[u], zn[u], zi);
+          } else {
+            Zt[at] = zi;
+            zi = fma(-mm[u], zi, zn[u]);
+          }
+        }
       }
     }
     Zt[(uint64_t)(M - 1) * M + j] = zi;
     // backward: U z = y
     double z1 = 0.0, z2 = 0.0, nrm = 0.0;
-#pragma unroll 8
-    for (int i = (int)M - 1; i >= 0; --i) {
-      const uint64_t at = (uint64_t)i * M + j;
-      const double zz = (Zt[at] - __ldg(u1 + at) * z1 - __ldg(u2 + at) * z2) / __ldg(u0 + at);
-      Zt[at] = zz;
-      z2 = z1;
-      z1 = zz;
-      nrm = fma(zz, zz, nrm);
+    for (int i0 = (int)M - 1; i0 >= 0; i0 -= (int)kB) {
+      double y[kB], a0[kB], a1[kB], a2[kB];
+#pragma unroll
+      for (int u = 0; u < (int)kB; ++u) {
+        const int i = i0 - u;
+        if (i >= 0) {
+          const uint64_t at = (uint64_t)i * M + j;
+          y[u] = Zt[at];
+          a0[u] = __ldg(u0 + at);
+          a1[u] = __ldg(u1 + at);
+          a2[u] = __ldg(u2 + at);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < (int)kB; ++u) {
+        const int i = i0 - u;
+        if (i >= 0) {
+          const double zz = (y[u] - a1[u] * z1 - a2[u] * z2) / a0[u];
+          Zt[(uint64_t)i * M + j] = zz;
+          z2 = z1;
+          z1 = zz;
+          nrm = fma(zz, zz, nrm);
+        }
+      }
     }
     scale = 1.0 / sqrt(nrm);
   }
