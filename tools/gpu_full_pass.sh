@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 final check: GPU tests (c5 full size included), the default bench line (c3, e2e + cpu_baseline),
+# The full GPU pass of a round (run on the box from the repo root): GPU tests (c5 full size included), the default bench line (c3, e2e + cpu_baseline),
 # the reference arm, c1 / c2 / c4 lines, the two-rank gloo dry run.
 out=gpurun_out/r02g; mkdir -p $out
 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > $out/pytest.log 2>&1
