@@ -196,13 +196,14 @@ def test_variant_switches_agree(env, tuning_env, ref):
     assert np.array_equal(res.svd.v, vr)
 
 
-@pytest.mark.parametrize("env", [("RK_JACOBI_SMEM", "0"), ("RK_JACOBI_SMEM_CL", "1"), ("RK_APPLY_Q", "panel"),
-                                 ("RK_PRESENCE", "csr")])
+@pytest.mark.parametrize("env", [("RK_JACOBI_SMEM", "0"), ("RK_JACOBI_SMEM_CL", "1"), ("RK_JACOBI_CARRY", "0"),
+                                 ("RK_APPLY_Q", "panel"), ("RK_PRESENCE", "csr")])
 def test_wide_block_variants_agree(env, tuning_env, ref):
     """c3's route (wide blocks: QR of X = T^T, Jacobi on R, apply_q; NeighborChecker) against the
     reference's run_pipeline on a 16-block slice, with the round-2 kernels switched off one at a
     time: the direct Jacobi instead of the shared-memory Gram-assisted one, one-CTA jobs only (the
-    larger R factors then take the direct kernel), apply_q reflector by reflector instead of
+    larger R factors then take the direct kernel), the full 16 x 16 Gram every step instead of carried
+    diagonal blocks, apply_q reflector by reflector instead of
     compact-WY, the rank check from the CSR instead of the CSC slices."""
     tuning_env(*env)
     cfg = configs.CONFIGS["c3"]
